@@ -1,0 +1,176 @@
+/*
+ * sparsepaint_b200.h -- C-ABI of libsparsepaint_b200.so, the sm_100a
+ * implementation of the data-optimization hot path of arXiv 2401.06747
+ * (reference package `sparsepaint` 0.1.0 under /root/reference/pkg).
+ *
+ * Conventions
+ *   - every entry returns 0 on success, < 0 on failure; the message is
+ *     available from sp_last_error() (thread-local).  Nothing throws.
+ *   - pointers named x/u/out/... are DEVICE pointers unless suffixed _h.
+ *   - images are planar (C, H, W), contiguous, dtype code 0 = float32,
+ *     1 = float64 (MultigridConfig.dtype, solver.py:49-82); masks are
+ *     (H, W) uint8 (0/1), labels int32, seeds int64 (m, 2) rows (y, x).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All work
+ *     is stream-ordered; calls return before the GPU finishes unless stated.
+ *   - buffers are caller-owned; temporaries come from the stream-ordered
+ *     allocator; handles (sp_hier_*) own their device pyramids.
+ *
+ * Boundary B1 below replaces, entry by entry, the 16-name kernel table the
+ * reference selects at import time (kernels/__init__.py:12-29, 43-66); the
+ * Python binding paper_2401_06747_b200/kernels/cuda_impl.py exposes them
+ * with the reference's numpy signatures so that
+ * `monkeypatch.setattr(sparsepaint.kernels, name, cuda_impl.<name>)`
+ * (test_backends.py:132-152) drives the reference orchestration on the GPU.
+ * Boundary B2 is the device-resident path behind the public entry points
+ * inpaint / delaunay_densify / voronoi_richardson_init / ras_tonal /
+ * cgnr_tonal (sparsepaint/__init__.py:9-56).
+ */
+#ifndef SPARSEPAINT_B200_H
+#define SPARSEPAINT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+#define SP_DTYPE_F32 0
+#define SP_DTYPE_F64 1
+
+const char* sp_last_error(void);
+int sp_abi_version(void);
+
+/* ======================= B1: kernel table ================================ */
+
+/* numba_impl.py:13-36  negated_laplacian(x, inv_h2) */
+int sp_negated_laplacian(int dtype, const void* x, void* out, int C, int H, int W,
+                         double inv_h2, void* stream);
+/* numba_impl.py:39-65  inpaint_matvec(x, mask, inv_h2) */
+int sp_inpaint_matvec(int dtype, const void* x, const uint8_t* mask, void* out, int C,
+                      int H, int W, double inv_h2, void* stream);
+/* numba_impl.py:68-98  sym_matvec(x, mask, inv_h2) */
+int sp_sym_matvec(int dtype, const void* x, const uint8_t* mask, void* out, int C, int H,
+                  int W, double inv_h2, void* stream);
+/* numba_impl.py:101-121  sym_rhs(b, mask, inv_h2) */
+int sp_sym_rhs(int dtype, const void* b, const uint8_t* mask, void* out, int C, int H,
+               int W, double inv_h2, void* stream);
+/* numba_impl.py:124-144  ct_apply(w, mask, inv_h2) */
+int sp_ct_apply(int dtype, const void* w, const uint8_t* mask, void* out, int C, int H,
+                int W, double inv_h2, void* stream);
+/* numba_impl.py:147-158  sym_residual(u, bsym, mask, inv_h2) -> (r, norms);
+ * norms is a device double[C] */
+int sp_sym_residual(int dtype, const void* u, const void* bsym, const uint8_t* mask,
+                    void* r, double* norms, int C, int H, int W, double inv_h2,
+                    void* stream);
+/* numba_impl.py:161-263  oras_apply(u, r, mask, xs, ys, bh, bw, gamma, taus, cap,
+ * weights, inv_h2) -- mutates u.  xs_h/ys_h/taus_h are HOST arrays, weights a
+ * device (nby*nbx, bh, bw) array of dtype.  Synchronizes the stream. */
+int sp_oras_apply(int dtype, void* u, const void* r, const uint8_t* mask,
+                  const int64_t* xs_h, int nbx, const int64_t* ys_h, int nby, int bh,
+                  int bw, double gamma, const double* taus_h, long cap,
+                  const void* weights, double inv_h2, int C, int H, int W, void* stream);
+/* numba_impl.py:266-284  restrict_values(fine) -> (C, ceil(H/2), ceil(W/2)) */
+int sp_restrict_values(int dtype, const void* fine, void* out, int C, int H, int W,
+                       void* stream);
+/* numba_impl.py:287-313  restrict_mask(mask, values) -> (cmask, cvals) */
+int sp_restrict_mask(int dtype, const uint8_t* mask, const void* values, uint8_t* cmask,
+                     void* cvals, int C, int H, int W, void* stream);
+/* numba_impl.py:316-348  prolongate(coarse, h, w) */
+int sp_prolongate(int dtype, const void* coarse, void* out, int C, int ch, int cw, int H,
+                  int W, void* stream);
+/* numba_impl.py:351-396  jfa_run(labels, seeds, steps); steps_h is HOST int64 */
+int sp_jfa_run(const int32_t* labels, int32_t* out, const int64_t* seeds, long m,
+               const int64_t* steps_h, int nsteps, int H, int W, void* stream);
+/* numba_impl.py:399-409  jfa_dist2(labels, seeds) -> int64 (H, W); out may be
+ * NULL; dmax (device uint64, may be NULL) receives max d^2 (geometry.py:108-110) */
+int sp_jfa_dist2(const int32_t* labels, const int64_t* seeds, long m, int64_t* out, int H,
+                 int W, uint64_t* dmax, void* stream);
+/* numba_impl.py:412-439  fs_dither(dens) -> uint8 (serial, bit-exact) */
+int sp_fs_dither(const double* dens, uint8_t* out, int H, int W, void* stream);
+/* numba_impl.py:442-466  assign_triangles(tris, vy, vx, h, w) -> int32 */
+int sp_assign_triangles(const int64_t* tris, long ntris, const int64_t* vy,
+                        const int64_t* vx, int H, int W, int32_t* out, void* stream);
+/* numba_impl.py:469-481  fallback_assign(assign, labels, seed_min_tri) */
+int sp_fallback_assign(const int32_t* assign, const int32_t* labels,
+                       const int32_t* seed_min_tri, int32_t* out, int H, int W,
+                       void* stream);
+/* numba_impl.py:484-498  reduce_cells(assign, err, ntris) -> (sums, amax, amax_val) */
+int sp_reduce_cells(const int32_t* assign, const double* err, long ntris, double* sums,
+                    int64_t* amax_idx, double* amax_val, int H, int W, void* stream);
+
+/* helpers used by the device-resident path */
+int sp_masked_sym_rhs(int dtype, const void* x, const uint8_t* mask, void* out, int C,
+                      int H, int W, void* stream); /* sym_rhs(where(mask, x, 0)) */
+int sp_enforce(int dtype, void* u, const void* src, const uint8_t* mask, int C, int H,
+               int W, int zero_off, void* stream); /* u[mask] = src[mask] */
+
+/* deterministic per-channel reductions over C planes of n elements; out is a
+ * device double[C].  mode 0: sum x^2, 1: sum x*y, 2: sum (x - z)^2 with z a
+ * double array (tonal.py:86-97 _mse/_chan_dot, grid.py:188-193 quality) */
+int sp_chan_reduce(int dtype, int mode, const void* x, const void* y, const double* z, long n,
+                   int C, double* out, void* stream);
+/* e = sum_c (u_c - f_c)^2 in double, f double (spatial.py:184-186 _error_map) */
+int sp_error_map(int dtype, const void* u, const double* f, double* e, int C, long n,
+                 void* stream);
+
+/* ======================= B2: device-resident solver ====================== */
+
+/* GridHierarchy (solver.py:205-372).  One handle per (dtype, C, H, W, cfg);
+ * sp_hier_set_mask rebuilds the mask/value pyramid in place, so a handle is
+ * reused across the masks of a densification run. */
+typedef struct sp_solve_report {
+  int iterations; /* V-cycles run (SolverReport.iterations) */
+  int converged;
+  int nres;       /* entries used in residuals[] */
+  int pad;
+  double residuals[256]; /* relative residual before each V-cycle */
+} sp_solve_report;
+
+int sp_hier_create(void** out, int dtype, int C, int H, int W, int block, int overlap,
+                   int levels, int pre, int post, double alpha, double rho,
+                   int with_values);
+int sp_hier_destroy(void* hier);
+int sp_hier_levels(void* hier, int* nlevels, int* dims, int cap);
+int sp_hier_use_graphs(void* hier, int on);
+int sp_hier_set_mask(void* hier, const uint8_t* mask, const void* values, void* stream);
+int sp_hier_level_mask(void* hier, int level, uint8_t* out, void* stream);
+/* solve_sym (solver.py:328-372): init_mode 0 = zeros, 1 = u holds the warm
+ * start, 2 = FMG cascade (needs values); tol < 0 = run exactly `cycles`
+ * V-cycles.  Synchronizes the stream once per V-cycle in tolerance mode. */
+int sp_hier_solve(void* hier, const void* bsym, void* u, int init_mode, double tol,
+                  int cycles, int max_cycles, sp_solve_report* rep, void* stream);
+int sp_hier_vcycle(void* hier, const void* bsym, void* u, void* stream);
+
+/* ================ B2: densification geometry workspace ================== */
+/* One workspace per (H, W).  Replaces, per densification iteration,
+ * jump_flood_voronoi (geometry.py:92-110), delaunay_from_voronoi (:113-185),
+ * accumulate_errors / voronoi_cell_errors (:197-244) and the pick loop of
+ * delaunay_densify (spatial.py:245-259). */
+int sp_geo_create(void** out, int H, int W);
+int sp_geo_destroy(void* geo);
+/* seeds = row-major nonzero of mask; start_hint < 1 means None; returns m,
+ * max_radius = sqrt(max d^2) and the number of JFA passes.  Syncs. */
+int sp_geo_voronoi(void* geo, const uint8_t* mask, double start_hint, long* m,
+                   double* max_radius, int* nsteps, void* stream);
+int sp_geo_delaunay(void* geo, long* ntris, void* stream); /* syncs */
+/* err: device double (H, W); voronoi != 0 buckets by cell instead of triangle */
+int sp_geo_accumulate(void* geo, const double* err, int voronoi, void* stream);
+/* marks the argmax pixels of the `want` best eligible buckets in mask */
+int sp_geo_select(void* geo, uint8_t* mask, long nbuckets, long want, long* picked,
+                  void* stream);
+/* spatial.py:189-197 */
+int sp_geo_fill_highest_error(void* geo, const double* err, uint8_t* mask, long want,
+                              void* stream);
+/* load caller labels (H,W) i32 + seed rows sy/sx (m) i32 into the workspace */
+int sp_geo_load(void* geo, const int32_t* labels, const int32_t* sy, const int32_t* sx,
+                long m, void* stream);
+int sp_geo_export(void* geo, int32_t* labels, int32_t* sy, int32_t* sx, int32_t* tris,
+                  double* sums, int64_t* amax, double* amax_val, long nbuckets,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEPAINT_B200_H */

@@ -1,0 +1,152 @@
+"""ctypes binding of libsparsepaint_b200.so (include/sparsepaint_b200.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, every entry point raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparsepaint_b200.so")
+
+c_int, c_long, c_double, c_void_p = ctypes.c_int, ctypes.c_long, ctypes.c_double, ctypes.c_void_p
+P = c_void_p
+
+# name -> argtypes (restype is always int)
+_SIGS = {
+    "sp_abi_version": [],
+    "sp_negated_laplacian": [c_int, P, P, c_int, c_int, c_int, c_double, P],
+    "sp_inpaint_matvec": [c_int, P, P, P, c_int, c_int, c_int, c_double, P],
+    "sp_sym_matvec": [c_int, P, P, P, c_int, c_int, c_int, c_double, P],
+    "sp_sym_rhs": [c_int, P, P, P, c_int, c_int, c_int, c_double, P],
+    "sp_ct_apply": [c_int, P, P, P, c_int, c_int, c_int, c_double, P],
+    "sp_sym_residual": [c_int, P, P, P, P, P, c_int, c_int, c_int, c_double, P],
+    "sp_oras_apply": [c_int, P, P, P, P, c_int, P, c_int, c_int, c_int, c_double, P, c_long,
+                      P, c_double, c_int, c_int, c_int, P],
+    "sp_restrict_values": [c_int, P, P, c_int, c_int, c_int, P],
+    "sp_restrict_mask": [c_int, P, P, P, P, c_int, c_int, c_int, P],
+    "sp_prolongate": [c_int, P, P, c_int, c_int, c_int, c_int, c_int, P],
+    "sp_jfa_run": [P, P, P, c_long, P, c_int, c_int, c_int, P],
+    "sp_jfa_dist2": [P, P, c_long, P, c_int, c_int, P, P],
+    "sp_fs_dither": [P, P, c_int, c_int, P],
+    "sp_assign_triangles": [P, c_long, P, P, c_int, c_int, P, P],
+    "sp_fallback_assign": [P, P, P, P, c_int, c_int, P],
+    "sp_reduce_cells": [P, P, c_long, P, P, P, c_int, c_int, P],
+    "sp_masked_sym_rhs": [c_int, P, P, P, c_int, c_int, c_int, P],
+    "sp_enforce": [c_int, P, P, P, c_int, c_int, c_int, c_int, P],
+    "sp_chan_reduce": [c_int, c_int, P, P, P, c_long, c_int, P, P],
+    "sp_error_map": [c_int, P, P, P, c_int, c_long, P],
+    "sp_hier_create": [P, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                       c_double, c_double, c_int],
+    "sp_hier_destroy": [P],
+    "sp_hier_levels": [P, P, P, c_int],
+    "sp_hier_use_graphs": [P, c_int],
+    "sp_hier_set_mask": [P, P, P, P],
+    "sp_hier_level_mask": [P, c_int, P, P],
+    "sp_hier_solve": [P, P, P, c_int, c_double, c_int, c_int, P, P],
+    "sp_hier_vcycle": [P, P, P, P],
+    "sp_geo_create": [P, c_int, c_int],
+    "sp_geo_destroy": [P],
+    "sp_geo_voronoi": [P, P, c_double, P, P, P, P],
+    "sp_geo_delaunay": [P, P, P],
+    "sp_geo_accumulate": [P, P, c_int, P],
+    "sp_geo_select": [P, P, c_long, c_long, P, P],
+    "sp_geo_fill_highest_error": [P, P, P, c_long, P],
+    "sp_geo_load": [P, P, P, P, c_long, P],
+    "sp_geo_export": [P, P, P, P, P, P, P, P, c_long, P],
+}
+
+_lib = None
+
+
+class SolveReport(ctypes.Structure):
+    _fields_ = [("iterations", c_int), ("converged", c_int), ("nres", c_int),
+                ("pad", c_int), ("residuals", c_double * 256)]
+
+
+def load(require_cuda: bool = True):
+    """Load the library (no GPU needed just to load); raise loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: run `python -m paper_2401_06747_b200.build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = c_int
+        lib.sp_last_error.restype = ctypes.c_char_p
+        lib.sp_last_error.argtypes = []
+        _lib = lib
+    if require_cuda and not torch.cuda.is_available():
+        raise RuntimeError("paper_2401_06747_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS) + ["sp_last_error"]
+
+
+def call(name, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.sp_last_error().decode(errors="replace")
+        if rc == -3:
+            raise ValueError(msg)
+        raise RuntimeError(f"{name} failed ({rc}): {msg}")
+    return rc
+
+
+def stream():
+    return c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return c_void_p(t.data_ptr())
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(c_void_p)
+    raise TypeError(type(t))
+
+
+DTYPE_CODE = {torch.float32: 0, torch.float64: 1}
+NP_TO_TORCH = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+               np.dtype(np.uint8): torch.uint8, np.dtype(np.int32): torch.int32,
+               np.dtype(np.int64): torch.int64}
+
+
+def dcode(t):
+    try:
+        return DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}: float32 or float64") from None
+
+
+def device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_dev(a, dtype=None):
+    """numpy / tensor -> contiguous CUDA tensor (optionally cast)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        arr = np.ascontiguousarray(a)
+        t = torch.from_numpy(arr)
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    if not t.is_cuda:
+        t = t.to(device(), non_blocking=False)
+    return t.contiguous()

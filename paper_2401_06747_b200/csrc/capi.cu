@@ -1,0 +1,444 @@
+// capi.cu -- the C-ABI boundary (declared in include/sparsepaint_b200.h).
+//
+// Plain pointers and sizes only; every entry returns 0 on success and a
+// negative code on failure with the message in sp_last_error().  Nothing
+// throws across the boundary.  Device buffers are caller-owned (PyTorch on
+// the Python side); temporaries come from the stream-ordered allocator.
+#include <stdarg.h>
+
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+#include "solver.cuh"
+#include "geometry.cuh"
+#include "../../include/sparsepaint_b200.h"
+
+namespace sp {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+const char* last_error() { return g_err; }
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename T>
+int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src,
+                      double tau_scale, const int* ys, const int* xs, int nby, int nbx,
+                      int bh, int bw, int H, int W, int C, double gamma, long cap,
+                      double inv_h2, T* corr, cudaStream_t s);
+template <typename T>
+int oras_blend_launch(T* u, const T* corr, const T* weights, const int* ys, const int* xs,
+                      const int* row_k0, const int* row_n, const int* col_k0,
+                      const int* col_n, int nby, int nbx, int bh, int bw, int H, int W,
+                      int C, int overlap, cudaStream_t s);
+void cover_tables(const std::vector<int>& starts, int size, int dim, std::vector<int>& k0,
+                  std::vector<int>& n);
+template <typename T>
+int chan_reduce(int mode, const T* x, const T* y, const double* z, size_t n, int C,
+                double* partial, unsigned* counter, double* out, cudaStream_t s);
+template <typename T>
+int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStream_t s);
+
+}  // namespace sp
+
+using namespace sp;
+
+#define STREAM(s) ((cudaStream_t)(s))
+#define DISPATCH(dtype, CALL_F32, CALL_F64)                                   \
+  do {                                                                        \
+    if ((dtype) == SP_F32) return CALL_F32;                                   \
+    if ((dtype) == SP_F64) return CALL_F64;                                   \
+    set_error("unsupported dtype code %d", (int)(dtype));                     \
+    return -2;                                                                \
+  } while (0)
+
+extern "C" {
+
+const char* sp_last_error(void) { return last_error(); }
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+// ---- B1: kernel table (kernels/__init__.py:12-29) ---------------------------
+
+int sp_negated_laplacian(int dtype, const void* x, void* out, int C, int H, int W,
+                         double inv_h2, void* s) {
+  DISPATCH(dtype, neglap<float>((const float*)x, (float*)out, C, H, W, inv_h2, STREAM(s)),
+           neglap<double>((const double*)x, (double*)out, C, H, W, inv_h2, STREAM(s)));
+}
+
+int sp_inpaint_matvec(int dtype, const void* x, const uint8_t* m, void* out, int C, int H,
+                      int W, double inv_h2, void* s) {
+  DISPATCH(dtype,
+           inpaint_matvec<float>((const float*)x, m, (float*)out, C, H, W, inv_h2, STREAM(s)),
+           inpaint_matvec<double>((const double*)x, m, (double*)out, C, H, W, inv_h2, STREAM(s)));
+}
+
+int sp_sym_matvec(int dtype, const void* x, const uint8_t* m, void* out, int C, int H, int W,
+                  double inv_h2, void* s) {
+  DISPATCH(dtype,
+           sym_matvec<float>((const float*)x, m, (float*)out, C, H, W, inv_h2, STREAM(s)),
+           sym_matvec<double>((const double*)x, m, (double*)out, C, H, W, inv_h2, STREAM(s)));
+}
+
+int sp_sym_rhs(int dtype, const void* b, const uint8_t* m, void* out, int C, int H, int W,
+               double inv_h2, void* s) {
+  DISPATCH(dtype,
+           sym_rhs<float>((const float*)b, m, (float*)out, nullptr, C, H, W, inv_h2, STREAM(s)),
+           sym_rhs<double>((const double*)b, m, (double*)out, nullptr, C, H, W, inv_h2,
+                           STREAM(s)));
+}
+
+int sp_ct_apply(int dtype, const void* w, const uint8_t* m, void* out, int C, int H, int W,
+                double inv_h2, void* s) {
+  DISPATCH(dtype,
+           ct_apply<float>((const float*)w, m, (float*)out, C, H, W, inv_h2, STREAM(s)),
+           ct_apply<double>((const double*)w, m, (double*)out, C, H, W, inv_h2, STREAM(s)));
+}
+
+int sp_masked_sym_rhs(int dtype, const void* x, const uint8_t* m, void* out, int C, int H,
+                      int W, void* s) {
+  DISPATCH(dtype, masked_sym_rhs<float>((const float*)x, m, (float*)out, C, H, W, STREAM(s)),
+           masked_sym_rhs<double>((const double*)x, m, (double*)out, C, H, W, STREAM(s)));
+}
+
+int sp_sym_residual(int dtype, const void* u, const void* bsym, const uint8_t* m, void* r,
+                    double* norms, int C, int H, int W, double inv_h2, void* s) {
+  cudaStream_t st = STREAM(s);
+  size_t np = residual_partials(H, W);
+  Scratch scr(st);
+  SP_TRY(scr.alloc(sizeof(double) * C * np + 256));
+  unsigned* counter = (unsigned*)((char*)scr.p + sizeof(double) * C * np);
+  SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+  double* part = (double*)scr.p;
+  DISPATCH(dtype,
+           residual<float>((const float*)u, (const float*)bsym, m, (float*)r, part, counter,
+                           norms, C, H, W, inv_h2, st),
+           residual<double>((const double*)u, (const double*)bsym, m, (double*)r, part,
+                            counter, norms, C, H, W, inv_h2, st));
+}
+
+int sp_oras_apply(int dtype, void* u, const void* r, const uint8_t* m, const int64_t* xs_h,
+                  int nbx, const int64_t* ys_h, int nby, int bh, int bw, double gamma,
+                  const double* taus_h, long cap, const void* weights, double inv_h2, int C,
+                  int H, int W, void* s) {
+  cudaStream_t st = STREAM(s);
+  if (bh > H || bw > W || bh < 1 || bw < 1) {
+    set_error("block (%d, %d) does not fit the grid (%d, %d)", bh, bw, H, W);
+    return -2;
+  }
+  std::vector<int> ys(nby), xs(nbx), rk0, rn, ck0, cn;
+  for (int i = 0; i < nby; ++i) ys[i] = (int)ys_h[i];
+  for (int i = 0; i < nbx; ++i) xs[i] = (int)xs_h[i];
+  for (int i = 1; i < nby; ++i)
+    if (ys[i] < ys[i - 1]) { set_error("block starts must be sorted"); return -2; }
+  for (int i = 1; i < nbx; ++i)
+    if (xs[i] < xs[i - 1]) { set_error("block starts must be sorted"); return -2; }
+  cover_tables(ys, bh, H, rk0, rn);
+  cover_tables(xs, bw, W, ck0, cn);
+  for (int y = 0; y < H; ++y)
+    if (rn[y] > 3) { set_error("more than 3 blocks cover row %d", y); return -2; }
+  for (int x = 0; x < W; ++x)
+    if (cn[x] > 3) { set_error("more than 3 blocks cover column %d", x); return -2; }
+  size_t es = dtype == SP_F64 ? 8 : 4;
+  size_t ncorr = (size_t)C * nby * nbx * bh * bw;
+  size_t ints = (size_t)nby + nbx + 2 * (size_t)H + 2 * (size_t)W;
+  Scratch scr(st);
+  SP_TRY(scr.alloc(es * ncorr + sizeof(double) * C + sizeof(int) * ints + 64));
+  char* base = (char*)scr.p;
+  void* corr = base;
+  double* taus = (double*)(base + es * ncorr);
+  int* ip = (int*)(taus + C);
+  int *dys = ip, *dxs = dys + nby, *drk0 = dxs + nbx, *drn = drk0 + H, *dck0 = drn + H,
+      *dcn = dck0 + W;
+  std::vector<int> packed;
+  packed.reserve(ints);
+  packed.insert(packed.end(), ys.begin(), ys.end());
+  packed.insert(packed.end(), xs.begin(), xs.end());
+  packed.insert(packed.end(), rk0.begin(), rk0.end());
+  packed.insert(packed.end(), rn.begin(), rn.end());
+  packed.insert(packed.end(), ck0.begin(), ck0.end());
+  packed.insert(packed.end(), cn.begin(), cn.end());
+  SP_CUDA(cudaMemcpyAsync(taus, taus_h, sizeof(double) * C, cudaMemcpyHostToDevice, st));
+  SP_CUDA(cudaMemcpyAsync(ip, packed.data(), sizeof(int) * ints, cudaMemcpyHostToDevice, st));
+  if (dtype == SP_F32) {
+    SP_TRY(oras_local_launch<float>((const float*)r, m, taus, 1.0, dys, dxs, nby, nbx, bh, bw,
+                                    H, W, C, gamma, cap, inv_h2, (float*)corr, st));
+    SP_TRY(oras_blend_launch<float>((float*)u, (const float*)corr, (const float*)weights, dys,
+                                    dxs, drk0, drn, dck0, dcn, nby, nbx, bh, bw, H, W, C, 0,
+                                    st));
+  } else if (dtype == SP_F64) {
+    SP_TRY(oras_local_launch<double>((const double*)r, m, taus, 1.0, dys, dxs, nby, nbx, bh,
+                                     bw, H, W, C, gamma, cap, inv_h2, (double*)corr, st));
+    SP_TRY(oras_blend_launch<double>((double*)u, (const double*)corr, (const double*)weights,
+                                     dys, dxs, drk0, drn, dck0, dcn, nby, nbx, bh, bw, H, W, C,
+                                     0, st));
+  } else {
+    set_error("unsupported dtype code %d", dtype);
+    return -2;
+  }
+  // keep the host staging vectors alive until the copies are consumed
+  SP_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int sp_restrict_values(int dtype, const void* f, void* out, int C, int H, int W, void* s) {
+  DISPATCH(dtype, restrict_values<float>((const float*)f, (float*)out, C, H, W, STREAM(s)),
+           restrict_values<double>((const double*)f, (double*)out, C, H, W, STREAM(s)));
+}
+
+int sp_restrict_mask(int dtype, const uint8_t* m, const void* v, uint8_t* cm, void* cv, int C,
+                     int H, int W, void* s) {
+  DISPATCH(dtype,
+           restrict_mask<float>(m, (const float*)v, cm, (float*)cv, C, H, W, STREAM(s)),
+           restrict_mask<double>(m, (const double*)v, cm, (double*)cv, C, H, W, STREAM(s)));
+}
+
+int sp_prolongate(int dtype, const void* co, void* out, int C, int ch, int cw, int H, int W,
+                  void* s) {
+  DISPATCH(dtype,
+           prolongate<float>((const float*)co, (float*)out, C, ch, cw, H, W, STREAM(s)),
+           prolongate<double>((const double*)co, (double*)out, C, ch, cw, H, W, STREAM(s)));
+}
+
+int sp_enforce(int dtype, void* u, const void* src, const uint8_t* m, int C, int H, int W,
+               int zero_off, void* s) {
+  DISPATCH(dtype, enforce<float>((float*)u, (const float*)src, m, C, H, W, zero_off, STREAM(s)),
+           enforce<double>((double*)u, (const double*)src, m, C, H, W, zero_off, STREAM(s)));
+}
+
+// ---- vector reductions (deterministic; tonal.py:86-97, grid.py:188-193) ------
+// mode 0: out[c] = sum x_c^2; 1: sum x_c*y_c; 2: sum (x_c - z_c)^2 (z double)
+int sp_chan_reduce(int dtype, int mode, const void* x, const void* y, const double* z, long n,
+                   int C, double* out, void* s) {
+  cudaStream_t st = STREAM(s);
+  Scratch scr(st);
+  SP_TRY(scr.alloc(sizeof(double) * 1024 * (size_t)C + 64));
+  unsigned* counter = (unsigned*)((double*)scr.p + 1024 * (size_t)C);
+  SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+  DISPATCH(dtype,
+           chan_reduce<float>(mode, (const float*)x, (const float*)y, z, (size_t)n, C,
+                              (double*)scr.p, counter, out, st),
+           chan_reduce<double>(mode, (const double*)x, (const double*)y, z, (size_t)n, C,
+                               (double*)scr.p, counter, out, st));
+}
+
+int sp_error_map(int dtype, const void* u, const double* f, double* e, int C, long n, void* s) {
+  DISPATCH(dtype, error_map<float>((const float*)u, f, e, C, (size_t)n, STREAM(s)),
+           error_map<double>((const double*)u, f, e, C, (size_t)n, STREAM(s)));
+}
+
+// ---- B2: device-resident hierarchy (solver.py:205-372) ----------------------
+
+int sp_hier_create(void** out, int dtype, int C, int H, int W, int block, int overlap,
+                   int levels, int pre, int post, double alpha, double rho, int with_values) {
+  if (dtype != SP_F32 && dtype != SP_F64) {
+    set_error("unsupported dtype code %d", dtype);
+    return -2;
+  }
+  HierCfg cfg;
+  cfg.block = block;
+  cfg.overlap = overlap;
+  cfg.levels = levels;
+  cfg.pre = pre;
+  cfg.post = post;
+  cfg.alpha = alpha;
+  cfg.rho = rho;
+  Hier* h = nullptr;
+  SP_TRY(hier_create(&h, dtype, C, H, W, cfg, with_values));
+  *out = h;
+  return 0;
+}
+
+int sp_hier_destroy(void* h) {
+  delete (Hier*)h;
+  return 0;
+}
+
+int sp_hier_levels(void* hp, int* nlevels, int* dims, int cap) {
+  Hier* h = (Hier*)hp;
+  *nlevels = (int)h->lv.size();
+  for (int i = 0; i < (int)h->lv.size() && 2 * i + 1 < cap; ++i) {
+    dims[2 * i] = h->lv[i].H;
+    dims[2 * i + 1] = h->lv[i].W;
+  }
+  return 0;
+}
+
+int sp_hier_use_graphs(void* hp, int on) {
+  Hier* h = (Hier*)hp;
+  h->use_graphs = on != 0;
+  if (!h->use_graphs && h->graph_exec) {
+    cudaGraphExecDestroy(h->graph_exec);
+    h->graph_exec = nullptr;
+  }
+  return 0;
+}
+
+int sp_hier_set_mask(void* h, const uint8_t* mask, const void* values, void* s) {
+  return hier_set_mask((Hier*)h, mask, values, STREAM(s));
+}
+
+// level mask / values read-back (tests: restrict_mask chain parity)
+int sp_hier_level_mask(void* hp, int lv, uint8_t* out, void* s) {
+  Hier* h = (Hier*)hp;
+  if (lv < 0 || lv >= (int)h->lv.size()) { set_error("bad level %d", lv); return -2; }
+  Level& L = h->lv[lv];
+  SP_CUDA(cudaMemcpyAsync(out, L.mask, (size_t)L.H * L.W, cudaMemcpyDeviceToDevice, STREAM(s)));
+  return 0;
+}
+
+int sp_hier_solve(void* h, const void* bsym, void* u, int init_mode, double tol, int cycles,
+                  int max_cycles, sp_solve_report* rep, void* s) {
+  static_assert(sizeof(sp_solve_report) == sizeof(SolveReport), "report layout");
+  return hier_solve((Hier*)h, bsym, u, init_mode, tol, cycles, max_cycles, STREAM(s),
+                    (SolveReport*)rep);
+}
+
+int sp_hier_vcycle(void* h, const void* bsym, void* u, void* s) {
+  return hier_vcycle((Hier*)h, bsym, u, STREAM(s));
+}
+
+
+// ---- B1: geometry kernels ----------------------------------------------------
+
+int sp_jfa_run(const int32_t* labels, int32_t* out, const int64_t* seeds, long m,
+               const int64_t* steps_h, int nsteps, int H, int W, void* s) {
+  cudaStream_t st = STREAM(s);
+  size_t n = (size_t)H * W;
+  Scratch scr(st);
+  SP_TRY(scr.alloc(sizeof(int) * (2 * n + 2 * (size_t)(m > 0 ? m : 1))));
+  int* a = (int*)scr.p;
+  int* b = a + n;
+  int* sy = b + n;
+  int* sx = sy + (m > 0 ? m : 1);
+  SP_TRY(seeds_to_soa((const long long*)seeds, m, sy, sx, st));
+  SP_CUDA(cudaMemcpyAsync(a, labels, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+  int* res = nullptr;
+  SP_TRY(jfa_passes(a, b, sy, sx, (const long long*)steps_h, nsteps, H, W, &res, st));
+  SP_CUDA(cudaMemcpyAsync(out, res, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int sp_jfa_dist2(const int32_t* labels, const int64_t* seeds, long m, int64_t* out, int H,
+                   int W, uint64_t* dmax, void* s) {
+  cudaStream_t st = STREAM(s);
+  Scratch scr(st);
+  SP_TRY(scr.alloc(sizeof(int) * 2 * (size_t)(m > 0 ? m : 1)));
+  int* sy = (int*)scr.p;
+  int* sx = sy + (m > 0 ? m : 1);
+  SP_TRY(seeds_to_soa((const long long*)seeds, m, sy, sx, st));
+  return dist2(labels, sy, sx, (long long*)out, (unsigned long long*)dmax, H, W, st);
+}
+
+int sp_fs_dither(const double* dens, uint8_t* out, int H, int W, void* s) {
+  return fs_dither(dens, out, H, W, STREAM(s));
+}
+
+int sp_assign_triangles(const int64_t* tris, long ntris, const int64_t* vy, const int64_t* vx,
+                        int H, int W, int32_t* out, void* s) {
+  return assign_tris<long long>((const long long*)tris, ntris, (const long long*)vy,
+                                (const long long*)vx, H, W, out, true, STREAM(s));
+}
+
+int sp_fallback_assign(const int32_t* assign, const int32_t* labels, const int32_t* smt,
+                       int32_t* out, int H, int W, void* s) {
+  return fallback(assign, labels, smt, out, (size_t)H * W, STREAM(s));
+}
+
+int sp_reduce_cells(const int32_t* assign, const double* err, long ntris, double* sums,
+                    int64_t* amax_idx, double* amax_val, int H, int W, void* s) {
+  return reduce_cells(assign, err, ntris, sums, (long long*)amax_idx, amax_val, H, W,
+                      STREAM(s));
+}
+
+// ---- B2: densification geometry workspace -------------------------------------
+
+int sp_geo_create(void** out, int H, int W) {
+  Geo* g = nullptr;
+  SP_TRY(geo_create(&g, H, W));
+  *out = g;
+  return 0;
+}
+
+int sp_geo_destroy(void* g) {
+  delete (Geo*)g;
+  return 0;
+}
+
+int sp_geo_voronoi(void* g, const uint8_t* mask, double start_hint, long* m, double* max_radius,
+                   int* nsteps, void* s) {
+  return geo_voronoi((Geo*)g, mask, start_hint, m, max_radius, nsteps, STREAM(s));
+}
+
+int sp_geo_delaunay(void* g, long* ntris, void* s) {
+  return geo_delaunay((Geo*)g, ntris, STREAM(s));
+}
+
+int sp_geo_accumulate(void* g, const double* err, int voronoi, void* s) {
+  return geo_accumulate((Geo*)g, err, voronoi, STREAM(s));
+}
+
+int sp_geo_select(void* g, uint8_t* mask, long nbuckets, long want, long* picked, void* s) {
+  return geo_select((Geo*)g, mask, nbuckets, want, picked, STREAM(s));
+}
+
+int sp_geo_fill_highest_error(void* g, const double* err, uint8_t* mask, long want, void* s) {
+  return fill_highest_error((Geo*)g, err, mask, want, STREAM(s));
+}
+
+// load caller-provided labels (H,W) i32 and seed rows sy/sx (m) i32 into the
+// workspace (delaunay_from_voronoi / accumulate on user VoronoiLabels)
+int sp_geo_load(void* gp, const int32_t* labels, const int32_t* sy, const int32_t* sx, long m,
+                void* s) {
+  Geo* g = (Geo*)gp;
+  cudaStream_t st = STREAM(s);
+  size_t n = (size_t)g->H * g->W;
+  if (m < 0 || (size_t)m > n) { set_error("bad seed count %ld", m); return -2; }
+  SP_CUDA(cudaMemcpyAsync(g->lab_a, labels, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+  if (m) {
+    SP_CUDA(cudaMemcpyAsync(g->sy, sy, sizeof(int) * m, cudaMemcpyDeviceToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(g->sx, sx, sizeof(int) * m, cudaMemcpyDeviceToDevice, st));
+  }
+  g->m = m;
+  g->T = 0;
+  return 0;
+}
+
+// copies of the workspace state for the public API objects (any pointer may
+// be NULL): labels (H,W) i32, seed rows sy/sx (m) i32, triangles (T,3) i32,
+// bucket sums / argmax / argmax value (T, or m for the Voronoi partition)
+int sp_geo_export(void* gp, int32_t* labels, int32_t* sy, int32_t* sx, int32_t* tris,
+                  double* sums, int64_t* amax, double* amax_val, long nbuckets, void* s) {
+  Geo* g = (Geo*)gp;
+  cudaStream_t st = STREAM(s);
+  size_t n = (size_t)g->H * g->W;
+  if (labels) SP_CUDA(cudaMemcpyAsync(labels, g->lab_a, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+  if (sy) SP_CUDA(cudaMemcpyAsync(sy, g->sy, sizeof(int) * g->m, cudaMemcpyDeviceToDevice, st));
+  if (sx) SP_CUDA(cudaMemcpyAsync(sx, g->sx, sizeof(int) * g->m, cudaMemcpyDeviceToDevice, st));
+  if (tris && g->T) SP_CUDA(cudaMemcpyAsync(tris, g->tris, sizeof(int) * 3 * g->T, cudaMemcpyDeviceToDevice, st));
+  if (nbuckets > 0) {
+    if (sums) SP_CUDA(cudaMemcpyAsync(sums, g->sums, sizeof(double) * nbuckets, cudaMemcpyDeviceToDevice, st));
+    if (amax) SP_CUDA(cudaMemcpyAsync(amax, g->amax, sizeof(int64_t) * nbuckets, cudaMemcpyDeviceToDevice, st));
+    if (amax_val) SP_CUDA(cudaMemcpyAsync(amax_val, g->amax_val, sizeof(double) * nbuckets, cudaMemcpyDeviceToDevice, st));
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// common.cuh -- shared helpers for the sm_100a data-optimization kernels.
+//
+// All kernels are compiled with --fmad=false (see build.py): the reference
+// kernels (numba_impl.py) never contract a*b+c, and the exact-parity kernels
+// (stencils, transfers, geometry, dithering) rely on the same rounding.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+namespace sp {
+
+// ---- error plumbing -------------------------------------------------------
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define SP_CUDA(expr)                                                          \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::sp::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,               \
+                      cudaGetErrorString(_e));                                 \
+      return -1;                                                               \
+    }                                                                          \
+  } while (0)
+
+#define SP_CHECK_LAUNCH()                                                      \
+  do {                                                                         \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      ::sp::set_error("%s:%d launch: %s", __FILE__, __LINE__,                  \
+                      cudaGetErrorString(_e));                                 \
+      return -1;                                                               \
+    }                                                                          \
+  } while (0)
+
+#define SP_TRY(expr)                                                           \
+  do {                                                                         \
+    int _rc = (expr);                                                          \
+    if (_rc != 0) return _rc;                                                  \
+  } while (0)
+
+enum DType { SP_F32 = 0, SP_F64 = 1 };
+
+inline unsigned cdiv(long a, long b) { return (unsigned)((a + b - 1) / b); }
+
+// number of SMs of the current device (cached)
+int num_sms();
+
+// ---- device helpers ---------------------------------------------------------
+
+// deterministic CTA-wide double sum: warp butterfly, then every thread adds
+// the per-warp partials in warp order.  `scratch` holds >= nwarps doubles and
+// must not be reused by the next call until after a __syncthreads() (callers
+// alternate two scratch arrays).
+template <int NT>
+__device__ __forceinline__ double cta_sum(double v, double* scratch) {
+  constexpr int NW = NT / 32;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;  // 1-D or 2-D CTAs
+  if ((tid & 31) == 0) scratch[tid >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) s += scratch[w];
+  return s;
+}
+
+// solver.py:134-139 _starts(dim, size, stride): min(i*stride, dim-size)
+__host__ __device__ __forceinline__ int block_start(int k, int stride, int dim,
+                                                    int size) {
+  int s = k * stride;
+  int lim = dim - size;
+  return s < lim ? s : lim;
+}
+
+__host__ __device__ __forceinline__ int num_starts(int dim, int size, int stride) {
+  if (dim <= size) return 1;
+  return (dim - size + stride - 1) / stride + 1;
+}
+
+// RAII stream-ordered scratch (cudaMallocAsync / cudaFreeAsync)
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  int alloc(size_t bytes) {
+    if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) {
+      set_error("cudaMallocAsync(%zu) failed", bytes);
+      return -1;
+    }
+    return 0;
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+}  // namespace sp

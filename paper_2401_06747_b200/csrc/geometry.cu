@@ -1,0 +1,709 @@
+// geometry.cu -- jump flooding, Delaunay-from-Voronoi, triangle buckets and
+// pixel selection (sm_100a).  Everything here is integer or order-exact and
+// therefore bit-identical to the reference:
+//   jfa pass            numba_impl.py:351-396   (one thread per pixel)
+//   jfa_dist2 / max     numba_impl.py:399-409, geometry.py:108-110
+//   corner scan         geometry.py:140-181     (packed 63-bit keys, radix
+//                                                sort + unique == np.unique)
+//   assign_triangles    numba_impl.py:442-466   (lowest index wins ==
+//                                                atomicMin, order-independent)
+//   seed_min_triangle   geometry.py:188-194     (atomicMin)
+//   fallback_assign     numba_impl.py:469-481
+//   reduce_cells        numba_impl.py:484-498   (stable sort of pixels by
+//                                                triangle, then a sequential
+//                                                row-major double sum per
+//                                                triangle: same adds, same
+//                                                order; first strict max)
+//   selection           spatial.py:245-259      (stable sort on ~bits(sum))
+//   fill_highest_error  spatial.py:189-197
+//   fs_dither           numba_impl.py:412-439   (serial; `aa` baseline only)
+#include <cub/cub.cuh>
+
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "geometry.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr int BX = 32, BY = 8;
+
+template <typename D>
+__global__ void k_jfa_pass(const int* __restrict__ cur, int* __restrict__ nxt,
+                           const int* __restrict__ sy, const int* __restrict__ sx,
+                           int step, int H, int W) {
+  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+  if (x >= W || y >= H) return;
+  int best = cur[(size_t)y * W + x];
+  D bd;
+  if (best >= 0) {
+    D dy = (D)y - (D)sy[best], dx = (D)x - (D)sx[best];
+    bd = dy * dy + dx * dx;
+  } else {
+    bd = (D)4 * ((D)H * (D)H + (D)W * (D)W);
+  }
+#pragma unroll
+  for (int oy = -1; oy <= 1; ++oy) {
+    int ny = y + oy * step;
+    if (ny < 0 || ny >= H) continue;
+#pragma unroll
+    for (int ox = -1; ox <= 1; ++ox) {
+      if (oy == 0 && ox == 0) continue;
+      int nx = x + ox * step;
+      if (nx < 0 || nx >= W) continue;
+      int cand = cur[(size_t)ny * W + nx];
+      if (cand < 0) continue;
+      D dy = (D)y - (D)sy[cand], dx = (D)x - (D)sx[cand];
+      D cd = dy * dy + dx * dx;
+      if (cd < bd || (cd == bd && best >= 0 && cand < best)) {
+        bd = cd;
+        best = cand;
+      }
+    }
+  }
+  nxt[(size_t)y * W + x] = best;
+}
+
+__global__ void k_dist2(const int* __restrict__ lab, const int* __restrict__ sy,
+                        const int* __restrict__ sx, long long* __restrict__ out,
+                        unsigned long long* __restrict__ dmax, int H, int W) {
+  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+  long long d = 0;
+  bool live = x < W && y < H;
+  if (live) {
+    int s = lab[(size_t)y * W + x];
+    long long dy = (long long)y - sy[s], dx = (long long)x - sx[s];
+    d = dy * dy + dx * dx;
+    if (out) out[(size_t)y * W + x] = d;
+  }
+  if (dmax) {
+    unsigned long long v = (unsigned long long)d;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = w > v ? w : v;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(dmax, v);
+  }
+}
+
+__global__ void k_seeds_i64_to_soa(const long long* __restrict__ seeds, long m,
+                                   int* __restrict__ sy, int* __restrict__ sx) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  sy[i] = (int)seeds[2 * i];
+  sx[i] = (int)seeds[2 * i + 1];
+}
+
+// seeds are the row-major np.nonzero order (geometry.py:99-105)
+__global__ void k_seed_init(const int* __restrict__ idx, long m, int W, int* __restrict__ sy,
+                            int* __restrict__ sx, int* __restrict__ lab) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int p = idx[i];
+  sy[i] = p / W;
+  sx[i] = p - (p / W) * W;
+  lab[p] = (int)i;
+}
+
+__global__ void k_fill_i32(int* __restrict__ p, size_t n, int v) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_mask_flags(const uint8_t* __restrict__ m, uint8_t* __restrict__ flags,
+                             size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = m[i] != 0;
+}
+
+// ---- corner scan (geometry.py:140-181) ----------------------------------------
+__device__ __forceinline__ unsigned long long tri_key(unsigned a, unsigned b, unsigned c) {
+  // a < b < c after sorting; 21 bits each
+  return ((unsigned long long)a << 42) | ((unsigned long long)b << 21) | (unsigned long long)c;
+}
+
+__device__ __forceinline__ void sort3(unsigned& a, unsigned& b, unsigned& c) {
+  unsigned t;
+  if (a > b) { t = a; a = b; b = t; }
+  if (b > c) { t = b; b = c; c = t; }
+  if (a > b) { t = a; a = b; b = t; }
+}
+
+__global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
+                              unsigned long long* __restrict__ keys,
+                              unsigned long long* __restrict__ nkeys) {
+  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+  unsigned long long k0 = 0, k1 = 0;
+  int nk = 0;
+  if (x < W - 1 && y < H - 1) {
+    size_t p = (size_t)y * W + x;
+    int tl = lab[p], tr = lab[p + 1], bl = lab[p + W], br = lab[p + W + 1];
+    int s0 = tl, s1 = tr, s2 = bl, s3 = br, t;
+    // sort 4
+    if (s0 > s1) { t = s0; s0 = s1; s1 = t; }
+    if (s2 > s3) { t = s2; s2 = s3; s3 = t; }
+    if (s0 > s2) { t = s0; s0 = s2; s2 = t; }
+    if (s1 > s3) { t = s1; s1 = s3; s3 = t; }
+    if (s1 > s2) { t = s1; s1 = s2; s2 = t; }
+    bool d0 = s1 == s0, d1 = s2 == s1, d2 = s3 == s2;
+    int nd = 4 - (int)d0 - (int)d1 - (int)d2;
+    if (nd == 3) {
+      unsigned a = s0, b = d0 ? s2 : s1, c = d2 ? s2 : s3;
+      k0 = tri_key(a, b, c);
+      nk = 1;
+    } else if (nd == 4) {
+      int a = tl, b = tr, c = bl, d = br;
+      int d1lo = min(a, d), d1hi = max(a, d), d2lo = min(b, c), d2hi = max(b, c);
+      bool use1 = (d1lo < d2lo) || (d1lo == d2lo && d1hi <= d2hi);
+      unsigned p0, p1, p2, q0, q1, q2;
+      if (use1) { p0 = a; p1 = b; p2 = d; q0 = a; q1 = c; q2 = d; }
+      else { p0 = a; p1 = b; p2 = c; q0 = b; q1 = c; q2 = d; }
+      sort3(p0, p1, p2);
+      sort3(q0, q1, q2);
+      k0 = tri_key(p0, p1, p2);
+      k1 = tri_key(q0, q1, q2);
+      nk = 2;
+    }
+  }
+  // warp-aggregated append
+  unsigned lane = threadIdx.x & 31;
+  unsigned cnt = (unsigned)nk;
+  unsigned incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (unsigned)o) incl += v;
+  }
+  unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && total) base = atomicAdd(nkeys, (unsigned long long)total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  unsigned long long pos = base + incl - cnt;
+  if (nk >= 1) keys[pos] = k0;
+  if (nk == 2) keys[pos + 1] = k1;
+}
+
+__global__ void k_decode_tris(const unsigned long long* __restrict__ keys, long T,
+                              int* __restrict__ tris) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T) return;
+  unsigned long long k = keys[i];
+  tris[3 * i] = (int)(k >> 42);
+  tris[3 * i + 1] = (int)((k >> 21) & 0x1FFFFFull);
+  tris[3 * i + 2] = (int)(k & 0x1FFFFFull);
+}
+
+// ---- rasterization (numba_impl.py:442-466) --------------------------------
+template <typename V>
+__global__ void k_assign_tris(const V* __restrict__ tris, long T, const V* __restrict__ vy,
+                              const V* __restrict__ vx, int H, int W, int* __restrict__ assign) {
+  long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  for (long t = warp; t < T; t += nwarps) {
+    long long ay = vy[tris[3 * t]], ax = vx[tris[3 * t]];
+    long long by = vy[tris[3 * t + 1]], bx = vx[tris[3 * t + 1]];
+    long long cy = vy[tris[3 * t + 2]], cx = vx[tris[3 * t + 2]];
+    long long ylo = max(0LL, min(ay, min(by, cy))), yhi = min((long long)H - 1, max(ay, max(by, cy)));
+    long long xlo = max(0LL, min(ax, min(bx, cx))), xhi = min((long long)W - 1, max(ax, max(bx, cx)));
+    if (ylo > yhi || xlo > xhi) continue;
+    long long bw = xhi - xlo + 1;
+    long long area = (yhi - ylo + 1) * bw;
+    for (long long q = lane; q < area; q += 32) {
+      long long y = ylo + q / bw, x = xlo + q % bw;
+      long long e0 = (bx - ax) * (y - ay) - (by - ay) * (x - ax);
+      long long e1 = (cx - bx) * (y - by) - (cy - by) * (x - bx);
+      long long e2 = (ax - cx) * (y - cy) - (ay - cy) * (x - cx);
+      if ((e0 >= 0 && e1 >= 0 && e2 >= 0) || (e0 <= 0 && e1 <= 0 && e2 <= 0))
+        atomicMin(&assign[y * W + x], (int)t);
+    }
+  }
+}
+
+__global__ void k_unset_to_neg(int* __restrict__ a, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && a[i] == INT_MAX) a[i] = -1;
+}
+
+template <typename V>
+__global__ void k_seed_min_tri(const V* __restrict__ tris, long T, int* __restrict__ smt) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * T) return;
+  atomicMin(&smt[tris[i]], (int)(i / 3));
+}
+
+__global__ void k_fallback(const int* __restrict__ assign, const int* __restrict__ lab,
+                           const int* __restrict__ smt, int* __restrict__ out, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int t = assign[i];
+  if (t < 0 || t == INT_MAX) {
+    t = smt[lab[i]];
+    if (t < 0 || t == INT_MAX) t = 0;
+  }
+  out[i] = t;
+}
+
+__global__ void k_iota(int* __restrict__ p, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int)i;
+}
+
+__global__ void k_segment_bounds(const int* __restrict__ keys, size_t n, int* __restrict__ start,
+                                 int* __restrict__ end) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int k = keys[i];
+  if (i == 0 || keys[i - 1] != k) start[k] = (int)i;
+  if (i == n - 1 || keys[i + 1] != k) end[k] = (int)i + 1;
+}
+
+// sequential row-major double sum + first strict max per segment
+__global__ void k_reduce_segments(const int* __restrict__ start, const int* __restrict__ end,
+                                  const int* __restrict__ pix, const double* __restrict__ err,
+                                  long ntris, double* __restrict__ sums,
+                                  long long* __restrict__ amax_idx,
+                                  double* __restrict__ amax_val) {
+  long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntris) return;
+  int b = start[t], e = end[t];
+  double s = 0.0, best = -1.0;
+  long long bi = -1;
+  for (int i = b; i < e; ++i) {
+    int p = pix[i];
+    double v = err[p];
+    s += v;
+    if (v > best) { best = v; bi = p; }
+  }
+  sums[t] = s;
+  if (amax_idx) amax_idx[t] = bi;
+  if (amax_val) amax_val[t] = best;
+}
+
+__global__ void k_fs_dither(const double* __restrict__ dens, double* __restrict__ buf,
+                            uint8_t* __restrict__ out, int H, int W) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (size_t i = 0; i < (size_t)H * W; ++i) buf[i] = dens[i];
+  for (int y = 0; y < H; ++y) {
+    int x0 = (y % 2 == 0) ? 0 : W - 1, x1 = (y % 2 == 0) ? W : -1, sgn = (y % 2 == 0) ? 1 : -1;
+    for (int x = x0; x != x1; x += sgn) {
+      size_t k = (size_t)y * W + x;
+      double val = buf[k];
+      int bit = val >= 0.5 ? 1 : 0;
+      out[k] = (uint8_t)bit;
+      double e = val - (double)bit;
+      int xn = x + sgn;
+      if (xn >= 0 && xn < W) buf[k + sgn] += e * (7.0 / 16.0);
+      if (y + 1 < H) {
+        int xb = x - sgn;
+        if (xb >= 0 && xb < W) buf[k + W - sgn] += e * (3.0 / 16.0);
+        buf[k + W] += e * (5.0 / 16.0);
+        if (xn >= 0 && xn < W) buf[k + W + sgn] += e * (1.0 / 16.0);
+      }
+    }
+  }
+}
+
+// ---- selection (spatial.py:245-259) -----------------------------------------
+__global__ void k_valid_flags(const long long* __restrict__ amax,
+                              const uint8_t* __restrict__ mask, long T,
+                              uint8_t* __restrict__ flags) {
+  long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  long long px = amax[t];
+  flags[t] = px >= 0 && !mask[px];
+}
+
+__global__ void k_not_mask(const uint8_t* __restrict__ mask, size_t n,
+                           uint8_t* __restrict__ flags) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = !mask[i];
+}
+
+// descending non-negative doubles: complement of the IEEE bit pattern
+__global__ void k_desc_keys(const int* __restrict__ idx, long n, const double* __restrict__ v,
+                            unsigned long long* __restrict__ keys) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ~(unsigned long long)__double_as_longlong(v[idx[i]]);
+}
+
+__global__ void k_apply_picks(const int* __restrict__ order, long npick,
+                              const long long* __restrict__ amax, uint8_t* __restrict__ mask) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < npick) mask[amax[order[i]]] = 1;
+}
+
+__global__ void k_set_mask(const int* __restrict__ idx, long n, uint8_t* __restrict__ mask) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) mask[idx[i]] = 1;
+}
+
+inline dim3 grid2(int W, int H) { return dim3(cdiv(W, BX), cdiv(H, BY)); }
+
+int bits_for(long n) {
+  int b = 1;
+  while ((1L << b) < n + 1 && b < 31) ++b;
+  return b;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// helpers shared with the B1 wrappers and the B2 workspace
+// ---------------------------------------------------------------------------
+
+int jfa_passes(int* a, int* b, const int* sy, const int* sx, const long long* steps,
+               int nsteps, int H, int W, int** result, cudaStream_t s) {
+  bool small = 4.0 * ((double)H * H + (double)W * W) < 2.0e9;
+  int* cur = a;
+  int* nxt = b;
+  for (int i = 0; i < nsteps; ++i) {
+    if (small)
+      k_jfa_pass<int><<<grid2(W, H), dim3(BX, BY), 0, s>>>(cur, nxt, sy, sx, (int)steps[i], H, W);
+    else
+      k_jfa_pass<long long><<<grid2(W, H), dim3(BX, BY), 0, s>>>(cur, nxt, sy, sx,
+                                                                  (int)steps[i], H, W);
+    SP_CHECK_LAUNCH();
+    int* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  *result = cur;
+  return 0;
+}
+
+int dist2(const int* lab, const int* sy, const int* sx, long long* out,
+          unsigned long long* dmax, int H, int W, cudaStream_t s) {
+  if (dmax) SP_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
+  k_dist2<<<grid2(W, H), dim3(BX, BY), 0, s>>>(lab, sy, sx, out, dmax, H, W);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+int seeds_to_soa(const long long* seeds, long m, int* sy, int* sx, cudaStream_t s) {
+  if (m <= 0) return 0;
+  k_seeds_i64_to_soa<<<cdiv(m, 256), 256, 0, s>>>(seeds, m, sy, sx);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+int fs_dither(const double* dens, uint8_t* out, int H, int W, cudaStream_t s) {
+  Scratch scr(s);
+  SP_TRY(scr.alloc(sizeof(double) * (size_t)H * W));
+  k_fs_dither<<<1, 1, 0, s>>>(dens, (double*)scr.p, out, H, W);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename V>
+int assign_tris(const V* tris, long T, const V* vy, const V* vx, int H, int W, int* assign,
+                bool neg_unset, cudaStream_t s) {
+  size_t n = (size_t)H * W;
+  k_fill_i32<<<cdiv(n, 256), 256, 0, s>>>(assign, n, INT_MAX);
+  SP_CHECK_LAUNCH();
+  if (T > 0) {
+    long warps = std::min<long>(T, (long)num_sms() * 64);
+    k_assign_tris<V><<<cdiv(warps * 32, 256), 256, 0, s>>>(tris, T, vy, vx, H, W, assign);
+    SP_CHECK_LAUNCH();
+  }
+  if (neg_unset) {
+    k_unset_to_neg<<<cdiv(n, 256), 256, 0, s>>>(assign, n);
+    SP_CHECK_LAUNCH();
+  }
+  return 0;
+}
+template int assign_tris<long long>(const long long*, long, const long long*, const long long*,
+                                    int, int, int*, bool, cudaStream_t);
+template int assign_tris<int>(const int*, long, const int*, const int*, int, int, int*, bool,
+                              cudaStream_t);
+
+int fallback(const int* assign, const int* lab, const int* smt, int* out, size_t n,
+             cudaStream_t s) {
+  k_fallback<<<cdiv(n, 256), 256, 0, s>>>(assign, lab, smt, out, n);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename V>
+int seed_min_tri(const V* tris, long T, int* smt, long m, cudaStream_t s) {
+  k_fill_i32<<<cdiv(m, 256), 256, 0, s>>>(smt, (size_t)m, INT_MAX);
+  SP_CHECK_LAUNCH();
+  if (T > 0) {
+    k_seed_min_tri<V><<<cdiv(3 * T, 256), 256, 0, s>>>(tris, T, smt);
+    SP_CHECK_LAUNCH();
+  }
+  return 0;
+}
+template int seed_min_tri<int>(const int*, long, int*, long, cudaStream_t);
+
+// per-segment sequential reduction; `assign` values must lie in [0, nseg)
+int reduce_cells(const int* assign, const double* err, long nseg, double* sums,
+                 long long* amax_idx, double* amax_val, int H, int W, cudaStream_t s) {
+  size_t n = (size_t)H * W;
+  int nbits = bits_for(nseg);
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const int*)nullptr, (int*)nullptr,
+                                  (const int*)nullptr, (int*)nullptr, (int)n, 0, nbits, s);
+  Scratch scr(s);
+  size_t ints = 3 * n + 2 * (size_t)nseg + 64;
+  SP_TRY(scr.alloc(tmp_bytes + sizeof(int) * ints));
+  int* keys_out = (int*)scr.p;
+  int* vals_in = keys_out + n;
+  int* vals_out = vals_in + n;
+  int* start = vals_out + n;
+  int* end = start + nseg;
+  void* tmp = (void*)(end + nseg + 32);
+  k_iota<<<cdiv(n, 256), 256, 0, s>>>(vals_in, n);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, assign, keys_out, vals_in, vals_out,
+                                          (int)n, 0, nbits, s));
+  SP_CUDA(cudaMemsetAsync(start, 0, sizeof(int) * 2 * nseg, s));
+  k_segment_bounds<<<cdiv(n, 256), 256, 0, s>>>(keys_out, n, start, end);
+  SP_CHECK_LAUNCH();
+  if (nseg > 0) {
+    k_reduce_segments<<<cdiv(nseg, 128), 128, 0, s>>>(start, end, vals_out, err, nseg, sums,
+                                                      amax_idx, amax_val);
+    SP_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// B2 workspace
+// ---------------------------------------------------------------------------
+
+Geo::~Geo() {
+  for (void* p : {(void*)lab_a, (void*)lab_b, (void*)sy, (void*)sx, (void*)keys,
+                  (void*)nkeys, (void*)tris, (void*)assign, (void*)smt, (void*)sums,
+                  (void*)amax, (void*)amax_val, (void*)dmax, (void*)flags, (void*)idx,
+                  (void*)nsel, (void*)h_small})
+    if (p) {
+      if (p == (void*)h_small) cudaFreeHost(p);
+      else cudaFree(p);
+    }
+}
+
+int geo_create(Geo** out, int H, int W) {
+  *out = nullptr;
+  Geo* g = new Geo();
+  g->H = H;
+  g->W = W;
+  size_t n = (size_t)H * W;
+  size_t ncorner = (size_t)(H > 1 ? H - 1 : 0) * (W > 1 ? W - 1 : 0);
+  g->key_cap = 2 * ncorner + 2;
+  g->tri_cap = g->key_cap;
+  bool ok = cudaMalloc(&g->lab_a, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->lab_b, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->sy, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->sx, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->idx, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->flags, n) == cudaSuccess &&
+            cudaMalloc(&g->keys, sizeof(unsigned long long) * g->key_cap) == cudaSuccess &&
+            cudaMalloc(&g->nkeys, sizeof(unsigned long long) * 4) == cudaSuccess &&
+            cudaMalloc(&g->tris, sizeof(int) * 3 * g->tri_cap) == cudaSuccess &&
+            cudaMalloc(&g->assign, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->smt, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->sums, sizeof(double) * g->tri_cap) == cudaSuccess &&
+            cudaMalloc(&g->amax, sizeof(long long) * g->tri_cap) == cudaSuccess &&
+            cudaMalloc(&g->amax_val, sizeof(double) * g->tri_cap) == cudaSuccess &&
+            cudaMalloc(&g->dmax, sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMalloc(&g->nsel, sizeof(int) * 4) == cudaSuccess &&
+            cudaMallocHost(&g->h_small, 64) == cudaSuccess;
+  if (!ok) {
+    set_error("geometry workspace allocation failed (%d x %d)", H, W);
+    delete g;
+    return -1;
+  }
+  *out = g;
+  return 0;
+}
+
+// geometry.py:76-89
+static std::vector<long long> steps_for(int max_dim, double hint) {
+  long long start;
+  if (hint >= 1.0) {
+    double lg = std::ceil(std::log2(std::max(1.0, hint)));
+    start = 1LL << std::max(0, (int)lg);
+    start = std::min(start, (long long)std::max(1, max_dim / 2));
+  } else if (max_dim >= 2) {
+    start = 1LL << ((int)std::ceil(std::log2((double)max_dim)) - 1);
+  } else {
+    start = 1;
+  }
+  std::vector<long long> out{1};
+  for (long long v = start; v >= 1; v /= 2) out.push_back(v);
+  return out;
+}
+
+int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* radius,
+                int* nsteps_out, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  size_t n = (size_t)H * W;
+  // seeds: row-major nonzero (cub select on a counting iterator)
+  k_mask_flags<<<cdiv(n, 256), 256, 0, s>>>(mask, g->flags, n);
+  SP_CHECK_LAUNCH();
+  cub::CountingInputIterator<int> it(0);
+  size_t tmp_bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, g->flags, g->idx, g->nsel, (int)n, s);
+  {
+    Scratch scr(s);
+    SP_TRY(scr.alloc(tmp_bytes));
+    SP_CUDA(cub::DeviceSelect::Flagged(scr.p, tmp_bytes, it, g->flags, g->idx, g->nsel, (int)n, s));
+  }
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  long m = ((int*)g->h_small)[0];
+  if (m == 0) {
+    set_error("mask has no stored pixels to seed from");
+    return -3;
+  }
+  g->m = m;
+  k_fill_i32<<<cdiv(n, 256), 256, 0, s>>>(g->lab_a, n, -1);
+  SP_CHECK_LAUNCH();
+  k_seed_init<<<cdiv(m, 256), 256, 0, s>>>(g->idx, m, W, g->sy, g->sx, g->lab_a);
+  SP_CHECK_LAUNCH();
+  std::vector<long long> steps = steps_for(std::max(H, W), hint);
+  int* res = nullptr;
+  SP_TRY(jfa_passes(g->lab_a, g->lab_b, g->sy, g->sx, steps.data(), (int)steps.size(), H, W,
+                    &res, s));
+  if (res != g->lab_a) std::swap(g->lab_a, g->lab_b);  // labels live in lab_a
+  SP_TRY(dist2(g->lab_a, g->sy, g->sx, nullptr, g->dmax, H, W, s));
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  unsigned long long d2 = ((unsigned long long*)g->h_small)[0];
+  *m_out = m;
+  *radius = std::sqrt((double)d2);
+  if (nsteps_out) *nsteps_out = (int)steps.size();
+  g->T = 0;
+  return 0;
+}
+
+int geo_delaunay(Geo* g, long* T_out, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  g->T = 0;
+  *T_out = 0;
+  if (H < 2 || W < 2 || g->m < 3) return 0;
+  if (g->m >= (1L << 21)) {
+    set_error("more than 2^21 stored pixels: triangle keys would overflow");
+    return -2;
+  }
+  SP_CUDA(cudaMemsetAsync(g->nkeys, 0, sizeof(unsigned long long) * 2, s));
+  k_corner_scan<<<grid2(W, H), dim3(BX, BY), 0, s>>>(g->lab_a, H, W, g->keys, g->nkeys);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  long nk = (long)((unsigned long long*)g->h_small)[0];
+  if (nk == 0) return 0;
+  // sort + unique (np.unique(axis=0) on sorted triples == sorted packed keys)
+  int nbits = bits_for(g->m - 1);
+  int endbit = 42 + nbits;
+  size_t sort_bytes = 0, uniq_bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                 (unsigned long long*)nullptr, (int)nk, 0, endbit, s);
+  cub::DeviceSelect::Unique(nullptr, uniq_bytes, (const unsigned long long*)nullptr,
+                            (unsigned long long*)nullptr, (int*)nullptr, (int)nk, s);
+  Scratch scr(s);
+  SP_TRY(scr.alloc(sizeof(unsigned long long) * nk + std::max(sort_bytes, uniq_bytes) + 256));
+  unsigned long long* sorted = (unsigned long long*)scr.p;
+  void* tmp = (void*)(sorted + nk + 16);
+  SP_CUDA(cub::DeviceRadixSort::SortKeys(tmp, sort_bytes, g->keys, sorted, (int)nk, 0, endbit, s));
+  SP_CUDA(cub::DeviceSelect::Unique(tmp, uniq_bytes, sorted, g->keys, g->nsel, (int)nk, s));
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  long T = ((int*)g->h_small)[0];
+  k_decode_tris<<<cdiv(T, 256), 256, 0, s>>>(g->keys, T, g->tris);
+  SP_CHECK_LAUNCH();
+  g->T = T;
+  *T_out = T;
+  return 0;
+}
+
+// geometry.py:197-223 (partition="delaunay") or :226-244 ("voronoi")
+int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  size_t n = (size_t)H * W;
+  if (voronoi) {
+    return reduce_cells(g->lab_a, err, g->m, g->sums, g->amax, g->amax_val, H, W, s);
+  }
+  if (g->T == 0) return 0;
+  SP_TRY(assign_tris<int>(g->tris, g->T, g->sy, g->sx, H, W, g->assign, false, s));
+  SP_TRY(seed_min_tri<int>(g->tris, g->T, g->smt, g->m, s));
+  SP_TRY(fallback(g->assign, g->lab_a, g->smt, g->assign, n, s));
+  return reduce_cells(g->assign, err, g->T, g->sums, g->amax, g->amax_val, H, W, s);
+}
+
+// Ordered selection of the `want` first entries of sort((-value, index))
+// among flagged indices; `apply(order, k)` consumes the sorted index list.
+// Order-preserving compaction (cub select) + one stable radix sort on the
+// complemented key == np.lexsort((index, -value)).
+template <typename Apply>
+static int top_by_desc(const uint8_t* flags, const double* vals, long n, long want,
+                       int* nsel, long* taken, cudaStream_t s, Apply apply) {
+  *taken = 0;
+  if (want <= 0 || n <= 0) return 0;
+  cub::CountingInputIterator<int> it(0);
+  size_t sel_bytes = 0, sort_bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, sel_bytes, it, flags, (int*)nullptr, nsel, (int)n, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (const int*)nullptr,
+                                  (int*)nullptr, (int)n, 0, 64, s);
+  size_t nn = (size_t)n;
+  Scratch scr(s);
+  SP_TRY(scr.alloc(2 * sizeof(unsigned long long) * nn + 2 * sizeof(int) * nn +
+                   std::max(sel_bytes, sort_bytes) + 512));
+  unsigned long long* k_in = (unsigned long long*)scr.p;
+  unsigned long long* k_out = k_in + nn;
+  int* v_in = (int*)(k_out + nn);
+  int* v_out = v_in + nn;
+  void* tmp = (void*)(v_out + nn + 16);
+  SP_CUDA(cub::DeviceSelect::Flagged(tmp, sel_bytes, it, flags, v_in, nsel, (int)n, s));
+  int nv_h = 0;
+  SP_CUDA(cudaMemcpyAsync(&nv_h, nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  long nv = nv_h;
+  if (nv == 0) return 0;
+  k_desc_keys<<<cdiv(nv, 256), 256, 0, s>>>(v_in, nv, vals, k_in);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, k_in, k_out, v_in, v_out, (int)nv,
+                                          0, 64, s));
+  long k = std::min(nv, want);
+  SP_TRY(apply(v_out, k));
+  *taken = k;
+  return 0;
+}
+
+// spatial.py:245-259: picks the argmax pixel of the `want` highest-error
+// buckets whose argmax is not stored yet; updates mask in place.
+int geo_select(Geo* g, uint8_t* mask, long nbuckets, long want, long* picked,
+               cudaStream_t s) {
+  *picked = 0;
+  if (want <= 0 || nbuckets <= 0) return 0;
+  k_valid_flags<<<cdiv(nbuckets, 256), 256, 0, s>>>(g->amax, mask, nbuckets, g->flags);
+  SP_CHECK_LAUNCH();
+  return top_by_desc(g->flags, g->sums, nbuckets, want, g->nsel, picked, s,
+                     [&](const int* order, long k) {
+                       k_apply_picks<<<cdiv(k, 256), 256, 0, s>>>(order, k, g->amax, mask);
+                       SP_CHECK_LAUNCH();
+                       return 0;
+                     });
+}
+
+// spatial.py:189-197: store the `want` highest-error free pixels
+int fill_highest_error(Geo* g, const double* err, uint8_t* mask, long want, cudaStream_t s) {
+  size_t n = (size_t)g->H * g->W;
+  k_not_mask<<<cdiv(n, 256), 256, 0, s>>>(mask, n, g->flags);
+  SP_CHECK_LAUNCH();
+  long taken = 0;
+  return top_by_desc(g->flags, err, (long)n, want, g->nsel, &taken, s,
+                     [&](const int* order, long k) {
+                       k_set_mask<<<cdiv(k, 256), 256, 0, s>>>(order, k, mask);
+                       SP_CHECK_LAUNCH();
+                       return 0;
+                     });
+}
+
+}  // namespace sp

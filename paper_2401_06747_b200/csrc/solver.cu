@@ -1,0 +1,354 @@
+// solver.cu -- device-resident multigrid-ORAS hierarchy (native runtime).
+//
+// Reference: solver.py:205-372 (GridHierarchy build / _smooth / _vcycle /
+// _cascade / solve_sym).  The whole level pyramid (masks, iterates,
+// right-hand sides, residuals, ORAS corrections) lives in HBM and is reused
+// across mask changes of the same geometry.  A V-cycle is recorded once into
+// a CUDA graph and replayed; the only host synchronisation in a solve is the
+// read-back of the per-channel residual norms for the tolerance test
+// (solver.py:358-368), exactly one 8*C-byte copy per V-cycle.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "kernels.cuh"
+#include "solver.cuh"
+
+namespace sp {
+
+template <typename T>
+int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src,
+                      double tau_scale, const int* ys, const int* xs, int nby, int nbx,
+                      int bh, int bw, int H, int W, int C, double gamma, long cap,
+                      double inv_h2, T* corr, cudaStream_t s);
+template <typename T>
+int oras_blend_launch(T* u, const T* corr, const T* weights, const int* ys, const int* xs,
+                      const int* row_k0, const int* row_n, const int* col_k0,
+                      const int* col_n, int nby, int nbx, int bh, int bw, int H, int W,
+                      int C, int overlap, cudaStream_t s);
+
+// covering tables for sorted block starts (host)
+void cover_tables(const std::vector<int>& starts, int size, int dim, std::vector<int>& k0,
+                  std::vector<int>& n) {
+  k0.assign(dim, 0);
+  n.assign(dim, 0);
+  for (int y = 0; y < dim; ++y) {
+    int first = -1, cnt = 0;
+    for (size_t k = 0; k < starts.size(); ++k) {
+      if (starts[k] <= y && y < starts[k] + size) {
+        if (first < 0) first = (int)k;
+        ++cnt;
+      }
+    }
+    k0[y] = first < 0 ? 0 : first;
+    n[y] = cnt;
+  }
+}
+
+static int dalloc(void** p, size_t bytes) {
+  *p = nullptr;
+  if (!bytes) return 0;
+  SP_CUDA(cudaMalloc(p, bytes));
+  return 0;
+}
+
+Hier::~Hier() {
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  if (cap_stream) cudaStreamDestroy(cap_stream);
+  for (auto& L : lv) {
+    for (void* p : {(void*)L.mask, L.values, L.u, L.b, L.r, L.corr, (void*)L.partial,
+                    (void*)L.counter, (void*)L.norms, (void*)L.ys, (void*)L.xs,
+                    (void*)L.row_k0, (void*)L.row_n, (void*)L.col_k0, (void*)L.col_n})
+      if (p) cudaFree(p);
+  }
+  if (h_norms) cudaFreeHost(h_norms);
+}
+
+int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
+                int with_values) {
+  *out = nullptr;
+  if (H < 1 || W < 1 || C < 1) {
+    set_error("bad hierarchy shape (%d, %d, %d)", C, H, W);
+    return -2;
+  }
+  if (cfg.block < cfg.overlap + 2 || cfg.overlap < 1) {
+    set_error("block size must be at least overlap + 2");
+    return -2;
+  }
+  Hier* h = new Hier();
+  h->dtype = dtype;
+  h->C = C;
+  h->cfg = cfg;
+  h->gamma = (1.0 - cfg.alpha) / (1.0 + cfg.alpha);
+  const size_t es = dtype == SP_F64 ? 8 : 4;
+  int hh = H, ww = W, level = 0;
+  while (true) {
+    Level L{};
+    L.H = hh;
+    L.W = ww;
+    L.bh = std::min(cfg.block, hh);
+    L.bw = std::min(cfg.block, ww);
+    int stride = cfg.block - cfg.overlap;
+    L.nby = num_starts(hh, L.bh, stride);
+    L.nbx = num_starts(ww, L.bw, stride);
+    std::vector<int> ys(L.nby), xs(L.nbx);
+    for (int k = 0; k < L.nby; ++k) ys[k] = block_start(k, stride, hh, L.bh);
+    for (int k = 0; k < L.nbx; ++k) xs[k] = block_start(k, stride, ww, L.bw);
+    std::vector<int> rk0, rn, ck0, cn;
+    cover_tables(ys, L.bh, hh, rk0, rn);
+    cover_tables(xs, L.bw, ww, ck0, cn);
+    // solver.py:262-264: tau_c = rho * (bh*bw / N) * ||r_c||^2, cap = bh*bw
+    L.tau_scale = cfg.rho * ((double)(L.bh * L.bw) / (double)((long)hh * ww));
+    size_t plane = (size_t)hh * ww, nb = (size_t)L.nby * L.nbx;
+    size_t vec = es * C * plane;
+    int rc = 0;
+    rc |= dalloc((void**)&L.mask, plane);
+    rc |= dalloc(&L.u, vec);
+    rc |= dalloc(&L.b, vec);
+    rc |= dalloc(&L.r, vec);
+    rc |= dalloc(&L.corr, es * C * nb * L.bh * L.bw);
+    if (with_values) rc |= dalloc(&L.values, vec);
+    L.npart = residual_partials(hh, ww);
+    rc |= dalloc((void**)&L.partial, sizeof(double) * std::max((size_t)C * L.npart, red_partials() * 4));
+    rc |= dalloc((void**)&L.counter, sizeof(unsigned));
+    rc |= dalloc((void**)&L.norms, sizeof(double) * C);
+    rc |= dalloc((void**)&L.ys, sizeof(int) * L.nby);
+    rc |= dalloc((void**)&L.xs, sizeof(int) * L.nbx);
+    rc |= dalloc((void**)&L.row_k0, sizeof(int) * hh);
+    rc |= dalloc((void**)&L.row_n, sizeof(int) * hh);
+    rc |= dalloc((void**)&L.col_k0, sizeof(int) * ww);
+    rc |= dalloc((void**)&L.col_n, sizeof(int) * ww);
+    h->lv.push_back(L);
+    if (rc) { delete h; return -1; }
+    Level& B = h->lv.back();
+    if (cudaMemset(B.counter, 0, sizeof(unsigned)) != cudaSuccess ||
+        cudaMemcpy(B.ys, ys.data(), sizeof(int) * B.nby, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(B.xs, xs.data(), sizeof(int) * B.nbx, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(B.row_k0, rk0.data(), sizeof(int) * hh, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(B.row_n, rn.data(), sizeof(int) * hh, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(B.col_k0, ck0.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(B.col_n, cn.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error("hierarchy upload failed");
+      delete h;
+      return -1;
+    }
+    ++level;
+    // solver.py:238-243: auto levels coarsen until max(h, w) <= block
+    if (cfg.levels > 0) {
+      if (level >= cfg.levels || std::max(hh, ww) <= 2) break;
+    } else if (std::max(hh, ww) <= cfg.block) {
+      break;
+    }
+    hh = (hh + 1) / 2;
+    ww = (ww + 1) / 2;
+  }
+  if (cudaMallocHost((void**)&h->h_norms, sizeof(double) * C) != cudaSuccess) {
+    set_error("pinned alloc failed");
+    delete h;
+    return -1;
+  }
+  *out = h;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+
+template <typename T>
+static int set_mask_t(Hier* h, const uint8_t* mask, const T* values, cudaStream_t s) {
+  Level& L0 = h->lv[0];
+  size_t plane = (size_t)L0.H * L0.W;
+  SP_CUDA(cudaMemcpyAsync(L0.mask, mask, plane, cudaMemcpyDeviceToDevice, s));
+  bool vals = values != nullptr && L0.values != nullptr;
+  if (vals)
+    SP_CUDA(cudaMemcpyAsync(L0.values, values, sizeof(T) * h->C * plane,
+                            cudaMemcpyDeviceToDevice, s));
+  for (size_t i = 1; i < h->lv.size(); ++i) {
+    Level& F = h->lv[i - 1];
+    Level& G = h->lv[i];
+    SP_TRY(restrict_mask<T>(F.mask, vals ? (const T*)F.values : nullptr, G.mask,
+                            vals ? (T*)G.values : nullptr, h->C, F.H, F.W, s));
+  }
+  h->has_values = vals;
+  return 0;
+}
+
+int hier_set_mask(Hier* h, const uint8_t* mask, const void* values, cudaStream_t s) {
+  if (h->dtype == SP_F64) return set_mask_t<double>(h, mask, (const double*)values, s);
+  return set_mask_t<float>(h, mask, (const float*)values, s);
+}
+
+// ---- V-cycle ----------------------------------------------------------------
+
+template <typename T>
+static int residual_lv(Hier* h, int lv, bool with_norms, cudaStream_t s) {
+  Level& L = h->lv[lv];
+  return residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
+                     with_norms ? L.norms : nullptr, h->C, L.H, L.W, 1.0, s);
+}
+
+template <typename T>
+static int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
+  Level& L = h->lv[lv];
+  for (int sw = 0; sw < sweeps; ++sw) {
+    if (!(sw == 0 && first_done)) SP_TRY(residual_lv<T>(h, lv, true, s));
+    SP_TRY(oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
+                                L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
+                                (long)L.bh * L.bw, 1.0, (T*)L.corr, s));
+    SP_TRY(oras_blend_launch<T>((T*)L.u, (const T*)L.corr, nullptr, L.ys, L.xs, L.row_k0,
+                                L.row_n, L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw,
+                                L.H, L.W, h->C, h->cfg.overlap, s));
+  }
+  return 0;
+}
+
+// solver.py:283-300; `first_done`: level lv's residual r/norms for the
+// current u are already in place (computed by the caller's tolerance check)
+template <typename T>
+static int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
+  const HierCfg& cfg = h->cfg;
+  int last = (int)h->lv.size() - 1;
+  if (lv == last) return smooth_lv<T>(h, lv, cfg.pre + cfg.post, first_done, s);
+  SP_TRY(smooth_lv<T>(h, lv, cfg.pre, first_done, s));
+  Level& F = h->lv[lv];
+  Level& G = h->lv[lv + 1];
+  SP_TRY(residual_restrict<T>((const T*)F.u, (const T*)F.b, F.mask, (T*)G.r, h->C, F.H,
+                              F.W, 1.0, s));
+  SP_TRY(sym_rhs<T>((const T*)G.r, G.mask, (T*)G.b, (T*)G.u, h->C, G.H, G.W, 1.0, s));
+  SP_TRY(vcycle_lv<T>(h, lv + 1, false, s));
+  SP_TRY(prolong_add_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H,
+                                G.W, F.H, F.W, s));
+  SP_TRY(smooth_lv<T>(h, lv, cfg.post, false, s));
+  return 0;
+}
+
+template <typename T>
+static int run_vcycle(Hier* h, cudaStream_t s) {
+  // precondition: level-0 r/norms are current (residual_lv(0) ran)
+  if (!h->use_graphs) return vcycle_lv<T>(h, 0, true, s);
+  if (!h->graph_exec) {
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); the graph is launched on `s`
+    if (!h->cap_stream) SP_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    SP_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = vcycle_lv<T>(h, 0, true, h->cap_stream);
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    if (rc) { if (e == cudaSuccess) cudaGraphDestroy(g); return rc; }
+    SP_CUDA(e);
+    cudaError_t ie = cudaGraphInstantiate(&h->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    SP_CUDA(ie);
+  }
+  SP_CUDA(cudaGraphLaunch(h->graph_exec, s));
+  return 0;
+}
+
+template <typename T>
+static int cascade_t(Hier* h, cudaStream_t s) {
+  int last = (int)h->lv.size() - 1;
+  Level& Lc = h->lv[last];
+  // solver.py:302-317: coarsest: u = 0, b = level rhs, enforce, smooth 1
+  SP_TRY(masked_sym_rhs<T>((const T*)Lc.values, Lc.mask, (T*)Lc.b, h->C, Lc.H, Lc.W, s));
+  SP_TRY(enforce<T>((T*)Lc.u, (const T*)Lc.b, Lc.mask, h->C, Lc.H, Lc.W, 1, s));
+  SP_TRY(smooth_lv<T>(h, last, 1, false, s));
+  for (int lv = last - 1; lv >= 0; --lv) {
+    Level& F = h->lv[lv];
+    Level& G = h->lv[lv + 1];
+    SP_TRY(masked_sym_rhs<T>((const T*)F.values, F.mask, (T*)F.b, h->C, F.H, F.W, s));
+    SP_TRY(prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H,
+                              G.W, F.H, F.W, s));
+    SP_TRY(smooth_lv<T>(h, lv, 1, false, s));
+  }
+  return 0;
+}
+
+template <typename T>
+static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, int cycles,
+                   int max_cycles, cudaStream_t s, SolveReport* rep) {
+  Level& L0 = h->lv[0];
+  const int C = h->C;
+  size_t n = (size_t)C * L0.H * L0.W;
+  rep->iterations = 0;
+  rep->nres = 0;
+  rep->converged = 0;
+  if (init_mode == 1) {
+    SP_CUDA(cudaMemcpyAsync(L0.u, u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  } else if (init_mode == 2 && h->lv.size() > 1) {
+    if (!h->has_values) {
+      set_error("hierarchy was built without stored values");
+      return -2;
+    }
+    SP_TRY(cascade_t<T>(h, s));
+  } else {
+    SP_CUDA(cudaMemsetAsync(L0.u, 0, sizeof(T) * n, s));
+  }
+  SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s));
+  if (tol < 0) {
+    // solver.py:345-350: exactly `cycles` V-cycles, converged = True
+    for (int c = 0; c < cycles; ++c) {
+      SP_TRY(residual_lv<T>(h, 0, true, s));
+      SP_TRY(run_vcycle<T>(h, s));
+    }
+    rep->iterations = cycles;
+    rep->converged = 1;
+  } else {
+    // solver.py:351-369
+    double bnorm = 0.0;
+    {
+      // solver.py:355-358: ||b~|| over all channels, double
+      SP_TRY(dot_self<T>((const T*)L0.b, n, L0.partial, L0.counter, L0.norms, s));
+      SP_CUDA(cudaMemcpyAsync(h->h_norms, L0.norms, sizeof(double), cudaMemcpyDeviceToHost, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+      bnorm = std::sqrt(h->h_norms[0]);
+    }
+    double scale = bnorm > 0 ? bnorm : 1.0;
+    int cap = max_cycles;
+    int done = 0;
+    while (true) {
+      SP_TRY(residual_lv<T>(h, 0, true, s));
+      SP_CUDA(cudaMemcpyAsync(h->h_norms, L0.norms, sizeof(double) * C,
+                              cudaMemcpyDeviceToHost, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+      double tot = 0.0;
+      for (int c = 0; c < C; ++c) tot += h->h_norms[c];
+      double rel = std::sqrt(tot) / scale;
+      if (rep->nres < SP_MAX_RES) rep->residuals[rep->nres++] = rel;
+      if (rel <= tol) { rep->converged = 1; break; }
+      if (done >= cap) break;
+      SP_TRY(run_vcycle<T>(h, s));
+      ++done;
+    }
+    rep->iterations = done;
+  }
+  SP_CUDA(cudaMemcpyAsync(u_io, L0.u, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
+               int cycles, int max_cycles, cudaStream_t s, SolveReport* rep) {
+  if (h->dtype == SP_F64)
+    return solve_t<double>(h, (const double*)bsym, (double*)u_io, init_mode, tol, cycles,
+                           max_cycles, s, rep);
+  return solve_t<float>(h, (const float*)bsym, (float*)u_io, init_mode, tol, cycles,
+                        max_cycles, s, rep);
+}
+
+template <typename T>
+static int vcycle_once_t(Hier* h, const T* bsym, T* u_io, cudaStream_t s) {
+  Level& L0 = h->lv[0];
+  size_t n = (size_t)h->C * L0.H * L0.W;
+  SP_CUDA(cudaMemcpyAsync(L0.u, u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  SP_TRY(residual_lv<T>(h, 0, true, s));
+  SP_TRY(run_vcycle<T>(h, s));
+  SP_CUDA(cudaMemcpyAsync(u_io, L0.u, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s) {
+  if (h->dtype == SP_F64) return vcycle_once_t<double>(h, (const double*)bsym, (double*)u_io, s);
+  return vcycle_once_t<float>(h, (const float*)bsym, (float*)u_io, s);
+}
+
+}  // namespace sp

@@ -1,0 +1,64 @@
+// solver.cuh -- device-resident multigrid hierarchy (see solver.cu).
+#pragma once
+#include <algorithm>
+#include <vector>
+
+#include "kernels.cuh"
+
+#define SP_MAX_RES 256
+
+namespace sp {
+
+struct HierCfg {
+  int block = 32, overlap = 6, levels = 0, pre = 1, post = 1;
+  double alpha = 1.0, rho = 0.25;
+};
+
+struct Level {
+  int H, W, bh, bw, nby, nbx;
+  double tau_scale;
+  uint8_t* mask;
+  void *values, *u, *b, *r, *corr;
+  double* partial;
+  size_t npart;
+  unsigned* counter;
+  double* norms;
+  int *ys, *xs, *row_k0, *row_n, *col_k0, *col_n;
+};
+
+struct Hier {
+  int dtype = 0, C = 1;
+  HierCfg cfg;
+  double gamma = 0.0;
+  bool has_values = false;
+  bool use_graphs = true;
+  std::vector<Level> lv;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  double* h_norms = nullptr;
+  ~Hier();
+};
+
+// C-layout report (mirrors include/sparsepaint_b200.h sp_solve_report)
+struct SolveReport {
+  int iterations;
+  int converged;
+  int nres;
+  int pad;
+  double residuals[SP_MAX_RES];
+};
+
+int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
+                int with_values);
+int hier_set_mask(Hier* h, const uint8_t* mask, const void* values, cudaStream_t s);
+int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
+               int cycles, int max_cycles, cudaStream_t s, SolveReport* rep);
+int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s);
+
+// vec.cu: deterministic reductions (fixed CTA count per size)
+size_t red_partials();  // doubles needed in `partial` per reduced channel
+template <typename T>
+int dot_self(const T* x, size_t n, double* partial, unsigned* counter, double* out,
+             cudaStream_t s);
+
+}  // namespace sp

@@ -1,0 +1,309 @@
+"""Pixel-grid containers and the stencil/transfer operators (grid.py parity).
+
+Mirrors /root/reference/pkg/src/sparsepaint/grid.py:20-218.  ``Image`` and
+``Mask`` accept numpy arrays (the reference's contract) or CUDA tensors.
+Objects produced by the device pipeline keep their data in HBM; the numpy
+view ``.data`` / ``.indicator`` is materialized on first access, after which
+the host array is the source of truth (so in-place edits by user code, which
+the reference's tests do, are honoured).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, dcode, ptr, stream
+
+
+@dataclass
+class StencilSpec:
+    """grid.py:20-35."""
+
+    h: float = 1.0
+    boundary: str = "reflect"
+
+    def __post_init__(self):
+        if self.h <= 0:
+            raise ValueError("grid spacing h must be positive")
+        if self.boundary != "reflect":
+            raise ValueError("only reflecting boundaries are supported")
+
+    @property
+    def inv_h2(self) -> float:
+        return 1.0 / (self.h * self.h)
+
+
+DEFAULT_STENCIL = StencilSpec()
+
+
+class Image:
+    """(channels, height, width) float image (grid.py:41-83)."""
+
+    def __init__(self, data):
+        if isinstance(data, torch.Tensor):
+            t = data
+            if t.dim() == 2:
+                t = t[None]
+            if t.dim() != 3:
+                raise ValueError("image data must be 2-D or (channels, H, W)")
+            if not t.is_floating_point():
+                t = t.to(torch.float64)
+            self._dev = t.contiguous()
+            self._host = None
+        else:
+            arr = np.asarray(data)
+            if arr.ndim == 2:
+                arr = arr[None]
+            if arr.ndim != 3:
+                raise ValueError("image data must be 2-D or (channels, H, W)")
+            if not np.issubdtype(arr.dtype, np.floating):
+                arr = arr.astype(np.float64)
+            if arr.size and not np.all(np.isfinite(arr)):
+                raise ValueError("image values must be finite")
+            self._host = arr
+            self._dev = None
+
+    # -- storage -----------------------------------------------------------
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+            self._dev = None
+        return self._host
+
+    @data.setter
+    def data(self, value):
+        self.__init__(value)
+
+    def tensor(self, dtype=None) -> torch.Tensor:
+        """Device tensor (C, H, W); uploads host data when host-sourced."""
+        if self._dev is not None:
+            t = self._dev
+            if not t.is_cuda:
+                t = t.to(_lib.device())
+        else:
+            t = _lib.to_dev(self._host)
+        if dtype is not None and t.dtype != dtype:
+            t = t.to(dtype)
+        return t.contiguous()
+
+    @property
+    def shape(self):
+        return tuple(self._dev.shape) if self._host is None else self._host.shape
+
+    @property
+    def channels(self) -> int:
+        return self.shape[0]
+
+    @property
+    def height(self) -> int:
+        return self.shape[1]
+
+    @property
+    def width(self) -> int:
+        return self.shape[2]
+
+    @property
+    def dtype(self):
+        if self._host is None:
+            return {torch.float32: np.dtype(np.float32),
+                    torch.float64: np.dtype(np.float64)}.get(self._dev.dtype,
+                                                            np.dtype(np.float64))
+        return self._host.dtype
+
+    def copy(self) -> "Image":
+        if self._host is None:
+            return Image(self._dev.clone())
+        return Image(self._host.copy())
+
+    def astype(self, dtype) -> "Image":
+        return Image(self.data.astype(dtype))
+
+    @classmethod
+    def zeros(cls, channels, height, width, dtype=np.float64) -> "Image":
+        return cls(np.zeros((channels, height, width), dtype=dtype))
+
+    def __repr__(self):
+        where = "device" if self._host is None else "host"
+        return f"Image(shape={self.shape}, dtype={self.dtype}, {where})"
+
+
+class Mask:
+    """Binary indicator (H, W) (grid.py:86-114)."""
+
+    def __init__(self, indicator):
+        if isinstance(indicator, torch.Tensor):
+            if indicator.dim() != 2:
+                raise ValueError("mask must be 2-D")
+            self._dev = (indicator != 0).to(torch.uint8).contiguous()
+            self._host = None
+        else:
+            arr = np.asarray(indicator)
+            if arr.ndim != 2:
+                raise ValueError("mask must be 2-D")
+            self._host = (arr != 0).astype(np.uint8)
+            self._dev = None
+
+    @property
+    def indicator(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+            self._dev = None
+        return self._host
+
+    @indicator.setter
+    def indicator(self, value):
+        self.__init__(value)
+
+    def tensor(self) -> torch.Tensor:
+        if self._dev is not None:
+            return self._dev if self._dev.is_cuda else self._dev.to(_lib.device())
+        return _lib.to_dev(self._host)
+
+    @property
+    def shape(self):
+        return tuple(self._dev.shape) if self._host is None else self._host.shape
+
+    @property
+    def height(self) -> int:
+        return self.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.shape[1]
+
+    @property
+    def count(self) -> int:
+        if self._host is None:
+            return int(self._dev.sum(dtype=torch.int64).item())
+        return int(self._host.sum())
+
+    def density(self) -> float:
+        return self.count / (self.height * self.width)
+
+    def copy(self) -> "Mask":
+        if self._host is None:
+            return Mask(self._dev.clone())
+        return Mask(self._host.copy())
+
+    def __repr__(self):
+        return f"Mask(shape={self.shape})"
+
+
+@dataclass
+class QualityReport:
+    """grid.py:117-141."""
+
+    mse: float
+    psnr: float = field(init=False)
+
+    def __post_init__(self):
+        if self.mse < 0:
+            raise ValueError("mse must be nonnegative")
+        self.psnr = math.inf if self.mse == 0.0 else 10.0 * math.log10(255.0 ** 2 / self.mse)
+
+    @property
+    def exact(self) -> bool:
+        return self.mse == 0.0
+
+    def psnr_label(self) -> str:
+        return "exact" if self.exact else f"{self.psnr:.4f}"
+
+    def __str__(self):
+        return f"mse={self.mse:.6g} psnr={self.psnr_label()}"
+
+
+def _check_mask_shape(img, mask):
+    if (img.height, img.width) != (mask.height, mask.width):
+        raise ValueError("image and mask dimensions disagree")
+
+
+def _float(img: Image):
+    t = img.tensor()
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    return t
+
+
+def _stencil(name, img, mask, stencil):
+    x = _float(img)
+    c, h, w = x.shape
+    out = torch.empty_like(x)
+    if mask is None:
+        call(name, dcode(x), ptr(x), ptr(out), c, h, w, stencil.inv_h2, stream())
+    else:
+        _check_mask_shape(img, mask)
+        m = mask.tensor()
+        call(name, dcode(x), ptr(x), ptr(m), ptr(out), c, h, w, stencil.inv_h2, stream())
+    return Image(out)
+
+
+def apply_negated_laplacian(img: Image, stencil: StencilSpec = DEFAULT_STENCIL) -> Image:
+    """grid.py:154-157."""
+    return _stencil("sp_negated_laplacian", img, None, stencil)
+
+
+def apply_inpainting_matrix(img, mask, stencil=DEFAULT_STENCIL) -> Image:
+    """grid.py:160-165."""
+    return _stencil("sp_inpaint_matvec", img, mask, stencil)
+
+
+def apply_symmetrized_matrix(img, mask, stencil=DEFAULT_STENCIL) -> Image:
+    """grid.py:168-173."""
+    return _stencil("sp_sym_matvec", img, mask, stencil)
+
+
+def symmetrized_rhs(f, mask, stencil=DEFAULT_STENCIL) -> Image:
+    """grid.py:176-185."""
+    return _stencil("sp_sym_rhs", f, mask, stencil)
+
+
+def quality(reference: Image, test: Image) -> QualityReport:
+    """grid.py:188-193 (MSE in double over all channels)."""
+    if reference.shape != test.shape:
+        raise ValueError(f"shape mismatch: {reference.shape} vs {test.shape}")
+    from .vec import mse_t
+    return QualityReport(mse=mse_t(reference.tensor(), test.tensor()))
+
+
+def restrict(img: Image) -> Image:
+    """grid.py:196-200."""
+    if img.height < 2 and img.width < 2:
+        raise ValueError("nothing to restrict: image is a single pixel")
+    x = _float(img)
+    c, h, w = x.shape
+    out = torch.empty((c, (h + 1) // 2, (w + 1) // 2), dtype=x.dtype, device=x.device)
+    call("sp_restrict_values", dcode(x), ptr(x), ptr(out), c, h, w, stream())
+    return Image(out)
+
+
+def restrict_mask(mask: Mask, values: Image):
+    """grid.py:203-208."""
+    _check_mask_shape(values, mask)
+    m = mask.tensor()
+    v = _float(values)
+    c = v.shape[0]
+    h, w = m.shape
+    cm = torch.empty(((h + 1) // 2, (w + 1) // 2), dtype=torch.uint8, device=m.device)
+    cv = torch.empty((c,) + tuple(cm.shape), dtype=v.dtype, device=v.device)
+    call("sp_restrict_mask", dcode(v), ptr(m), ptr(v), ptr(cm), ptr(cv), c, h, w, stream())
+    return Mask(cm), Image(cv)
+
+
+def prolongate(coarse: Image, height: int, width: int) -> Image:
+    """grid.py:211-213."""
+    x = _float(coarse)
+    c, ch, cw = x.shape
+    out = torch.empty((c, height, width), dtype=x.dtype, device=x.device)
+    call("sp_prolongate", dcode(x), ptr(x), ptr(out), c, ch, cw, height, width, stream())
+    return Image(out)
+
+
+def clamp_to_bytes(img: Image) -> np.ndarray:
+    """grid.py:216-218 (host-side export helper)."""
+    return np.clip(np.rint(img.data), 0, 255).astype(np.uint8)

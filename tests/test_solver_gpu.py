@@ -1,0 +1,60 @@
+"""Device-resident multigrid solver (B2) vs the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(dtype, tol):
+    from paper_2401_06747_b200 import MultigridConfig
+    return MultigridConfig(dtype=dtype, tol=tol, max_cycles=200)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("shape,density", [((1, 64, 64), 0.1), ((3, 37, 53), 0.08),
+                                           ((1, 256, 256), 0.1)])
+def test_inpaint_matches_oracle(dtype, shape, density):
+    import paper_2401_06747_b200 as sp
+    f = O.synth(shape[1], shape[2], shape[0], 0)
+    mask = (np.random.default_rng(1).random(shape[1:]) < density).astype(np.uint8)
+    tol = 1e-6 if dtype == "float32" else 1e-10
+    u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), _cfg(dtype, tol))
+    uo, repo = O.inpaint(f, mask, O.SolverCfg(dtype=dtype, tol=tol, max_cycles=200))
+    assert rep.converged
+    assert rep.residuals[-1] <= tol
+    rel = np.linalg.norm(u.data - uo) / np.linalg.norm(uo)
+    assert rel <= (1e-4 if dtype == "float32" else 1e-8)
+    assert np.array_equal(u.data[:, mask > 0], f.astype(u.data.dtype)[:, mask > 0])
+
+
+def test_inpaint_default_tol_tracks_oracle_iterations():
+    import paper_2401_06747_b200 as sp
+    f = O.synth(256, 256, 1, 0)
+    mask = (np.random.default_rng(1).random((256, 256)) < 0.10).astype(np.uint8)
+    u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask))
+    uo, repo = O.inpaint(f, mask)
+    assert abs(rep.iterations - repo.iterations) <= 1
+    rel = np.linalg.norm(u.data - uo) / np.linalg.norm(uo)
+    assert rel <= 1e-3
+
+
+def test_warm_start_and_fixed_cycles():
+    import paper_2401_06747_b200 as sp
+    f = O.synth(96, 80, 3, 2)
+    mask = (np.random.default_rng(5).random((96, 80)) < 0.05).astype(np.uint8)
+    u0, _ = sp.inpaint(sp.Image(f), sp.Mask(mask))
+    uo0, _ = O.inpaint(f, mask)
+    cfg = sp.MultigridConfig(tol=None, cycles=2)
+    u1, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), cfg, init=u0)
+    uo1, _ = O.inpaint(f, mask, O.SolverCfg(tol=None, cycles=2), init=uo0)
+    assert rep.iterations == 2 and rep.converged
+    assert np.linalg.norm(u1.data - uo1) / np.linalg.norm(uo1) <= 1e-4
+
+
+def test_empty_mask_raises():
+    import paper_2401_06747_b200 as sp
+    with pytest.raises(ValueError):
+        sp.inpaint(sp.Image(np.ones((1, 8, 8))), sp.Mask(np.zeros((8, 8))))
