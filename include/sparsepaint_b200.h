@@ -128,9 +128,12 @@ typedef struct sp_solve_report {
   double residuals[256]; /* relative residual before each V-cycle */
 } sp_solve_report;
 
+/* ntile independent problems of the same (C, H, W) share one handle; their
+ * masks/vectors are stacked [tile][...] and each tile stops on its own
+ * tolerance test (the RAS block-local systems, tonal.py:343-354) */
 int sp_hier_create(void** out, int dtype, int C, int H, int W, int block, int overlap,
                    int levels, int pre, int post, double alpha, double rho,
-                   int with_values);
+                   int with_values, int ntile);
 int sp_hier_destroy(void* hier);
 int sp_hier_levels(void* hier, int* nlevels, int* dims, int cap);
 int sp_hier_use_graphs(void* hier, int on);
@@ -142,6 +145,12 @@ int sp_hier_level_mask(void* hier, int level, uint8_t* out, void* stream);
 int sp_hier_solve(void* hier, const void* bsym, void* u, int init_mode, double tol,
                   int cycles, int max_cycles, sp_solve_report* rep, void* stream);
 int sp_hier_vcycle(void* hier, const void* bsym, void* u, void* stream);
+/* batched solve_sym: active_h (HOST int[ntile], NULL = all) selects the tiles
+ * to solve; iters_h / conv_h (HOST int[ntile], may be NULL) receive the
+ * per-tile V-cycle counts and converged flags */
+int sp_hier_solve_tiles(void* hier, const void* bsym, void* u, int init_mode, double tol,
+                        int cycles, int max_cycles, const int* active_h, int* iters_h,
+                        int* conv_h, void* stream);
 
 /* ================ B2: densification geometry workspace ================== */
 /* One workspace per (H, W).  Replaces, per densification iteration,

@@ -43,7 +43,7 @@ _SIGS = {
     "sp_chan_reduce": [c_int, c_int, P, P, P, c_long, c_int, P, P],
     "sp_error_map": [c_int, P, P, P, c_int, c_long, P],
     "sp_hier_create": [P, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
-                       c_double, c_double, c_int],
+                       c_double, c_double, c_int, c_int],
     "sp_hier_destroy": [P],
     "sp_hier_levels": [P, P, P, c_int],
     "sp_hier_use_graphs": [P, c_int],
@@ -51,6 +51,7 @@ _SIGS = {
     "sp_hier_level_mask": [P, c_int, P, P],
     "sp_hier_solve": [P, P, P, c_int, c_double, c_int, c_int, P, P],
     "sp_hier_vcycle": [P, P, P, P],
+    "sp_hier_solve_tiles": [P, P, P, c_int, c_double, c_int, c_int, P, P, P, P],
     "sp_geo_create": [P, c_int, c_int],
     "sp_geo_destroy": [P],
     "sp_geo_voronoi": [P, P, c_double, P, P, P, P],
@@ -59,6 +60,8 @@ _SIGS = {
     "sp_geo_select": [P, P, c_long, c_long, P, P],
     "sp_geo_fill_highest_error": [P, P, P, c_long, P],
     "sp_geo_load": [P, P, P, P, c_long, P],
+    "sp_stats": [c_int, P],
+    "sp_oras_variant": [c_int],
     "sp_geo_export": [P, P, P, P, P, P, P, P, c_long, P],
 }
 

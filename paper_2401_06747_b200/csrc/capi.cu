@@ -38,23 +38,8 @@ int num_sms() {
   return n;
 }
 
-template <typename T>
-int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src,
-                      double tau_scale, const int* ys, const int* xs, int nby, int nbx,
-                      int bh, int bw, int H, int W, int C, double gamma, long cap,
-                      double inv_h2, T* corr, cudaStream_t s);
-template <typename T>
-int oras_blend_launch(T* u, const T* corr, const T* weights, const int* ys, const int* xs,
-                      const int* row_k0, const int* row_n, const int* col_k0,
-                      const int* col_n, int nby, int nbx, int bh, int bw, int H, int W,
-                      int C, int overlap, cudaStream_t s);
 void cover_tables(const std::vector<int>& starts, int size, int dim, std::vector<int>& k0,
                   std::vector<int>& n);
-template <typename T>
-int chan_reduce(int mode, const T* x, const T* y, const double* z, size_t n, int C,
-                double* partial, unsigned* counter, double* out, cudaStream_t s);
-template <typename T>
-int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStream_t s);
 
 }  // namespace sp
 
@@ -123,9 +108,9 @@ int sp_sym_residual(int dtype, const void* u, const void* bsym, const uint8_t* m
   cudaStream_t st = STREAM(s);
   size_t np = residual_partials(H, W);
   Scratch scr(st);
-  SP_TRY(scr.alloc(sizeof(double) * C * np + 256));
+  SP_TRY(scr.alloc(sizeof(double) * C * np + sizeof(unsigned) * C + 256));
   unsigned* counter = (unsigned*)((char*)scr.p + sizeof(double) * C * np);
-  SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+  SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned) * C, st));
   double* part = (double*)scr.p;
   DISPATCH(dtype,
            residual<float>((const float*)u, (const float*)bsym, m, (float*)r, part, counter,
@@ -179,16 +164,16 @@ int sp_oras_apply(int dtype, void* u, const void* r, const uint8_t* m, const int
   SP_CUDA(cudaMemcpyAsync(ip, packed.data(), sizeof(int) * ints, cudaMemcpyHostToDevice, st));
   if (dtype == SP_F32) {
     SP_TRY(oras_local_launch<float>((const float*)r, m, taus, 1.0, dys, dxs, nby, nbx, bh, bw,
-                                    H, W, C, gamma, cap, inv_h2, (float*)corr, st));
-    SP_TRY(oras_blend_launch<float>((float*)u, (const float*)corr, (const float*)weights, dys,
-                                    dxs, drk0, drn, dck0, dcn, nby, nbx, bh, bw, H, W, C, 0,
-                                    st));
+                                    H, W, C, gamma, cap, inv_h2, (const float*)weights,
+                                    (float*)corr, st));
+    SP_TRY(oras_blend_launch<float>((float*)u, (const float*)corr, dys, dxs, drk0, drn, dck0,
+                                    dcn, nby, nbx, bh, bw, H, W, C, st));
   } else if (dtype == SP_F64) {
     SP_TRY(oras_local_launch<double>((const double*)r, m, taus, 1.0, dys, dxs, nby, nbx, bh,
-                                     bw, H, W, C, gamma, cap, inv_h2, (double*)corr, st));
-    SP_TRY(oras_blend_launch<double>((double*)u, (const double*)corr, (const double*)weights,
-                                     dys, dxs, drk0, drn, dck0, dcn, nby, nbx, bh, bw, H, W, C,
-                                     0, st));
+                                     bw, H, W, C, gamma, cap, inv_h2, (const double*)weights,
+                                     (double*)corr, st));
+    SP_TRY(oras_blend_launch<double>((double*)u, (const double*)corr, dys, dxs, drk0, drn,
+                                     dck0, dcn, nby, nbx, bh, bw, H, W, C, st));
   } else {
     set_error("unsupported dtype code %d", dtype);
     return -2;
@@ -247,7 +232,8 @@ int sp_error_map(int dtype, const void* u, const double* f, double* e, int C, lo
 // ---- B2: device-resident hierarchy (solver.py:205-372) ----------------------
 
 int sp_hier_create(void** out, int dtype, int C, int H, int W, int block, int overlap,
-                   int levels, int pre, int post, double alpha, double rho, int with_values) {
+                   int levels, int pre, int post, double alpha, double rho, int with_values,
+                   int ntile) {
   if (dtype != SP_F32 && dtype != SP_F64) {
     set_error("unsupported dtype code %d", dtype);
     return -2;
@@ -261,7 +247,7 @@ int sp_hier_create(void** out, int dtype, int C, int H, int W, int block, int ov
   cfg.alpha = alpha;
   cfg.rho = rho;
   Hier* h = nullptr;
-  SP_TRY(hier_create(&h, dtype, C, H, W, cfg, with_values));
+  SP_TRY(hier_create(&h, dtype, C, H, W, cfg, with_values, ntile));
   *out = h;
   return 0;
 }
@@ -308,7 +294,14 @@ int sp_hier_solve(void* h, const void* bsym, void* u, int init_mode, double tol,
                   int max_cycles, sp_solve_report* rep, void* s) {
   static_assert(sizeof(sp_solve_report) == sizeof(SolveReport), "report layout");
   return hier_solve((Hier*)h, bsym, u, init_mode, tol, cycles, max_cycles, STREAM(s),
-                    (SolveReport*)rep);
+                    nullptr, nullptr, nullptr, (SolveReport*)rep);
+}
+
+int sp_hier_solve_tiles(void* h, const void* bsym, void* u, int init_mode, double tol,
+                        int cycles, int max_cycles, const int* active_h, int* iters_h,
+                        int* conv_h, void* s) {
+  return hier_solve((Hier*)h, bsym, u, init_mode, tol, cycles, max_cycles, STREAM(s),
+                    active_h, iters_h, conv_h, nullptr);
 }
 
 int sp_hier_vcycle(void* h, const void* bsym, void* u, void* s) {
@@ -442,3 +435,21 @@ int sp_geo_export(void* gp, int32_t* labels, int32_t* sy, int32_t* sx, int32_t* 
 }
 
 }  // extern "C"
+
+// ---- tracing: ORAS local-solve statistics -----------------------------------
+namespace sp {
+int oras_stats(int enable, unsigned long long* out);
+}
+extern "C" int sp_stats(int enable, uint64_t* out) {
+  // enable: 1 = reset + start, 0 = reset + stop, -1 = read only.  out (HOST,
+  // may be NULL) receives {ORAS jobs, local CG iterations, jobs converged on
+  // entry, 0} accumulated since the last reset
+  return sp::oras_stats(enable, (unsigned long long*)out);
+}
+
+namespace sp {
+int oras_variant(int v);
+}
+// select the float ORAS kernel for blocks <= 32x32: 1 = warp per job
+// (default), 0 = CTA per job; v < 0 only queries.  Returns the current value.
+extern "C" int sp_oras_variant(int v) { return sp::oras_variant(v); }

@@ -1,102 +1,465 @@
 // oras.cu -- optimized restricted additive Schwarz sweep (sm_100a).
 //
 // Reference: numba_impl.py:161-263 (oras_apply) driven by solver.py:259-273.
-// Kernel 1 (k_oras_local): one CTA per (block, channel).  The block's
-// residual is staged into registers (each thread owns PPT pixels, strided by
-// the CTA size so warps read whole rows), the search direction p lives in
-// shared memory for the 5-point stencil, and the local CG runs entirely
-// on-chip: dots are double, reduced by warp shuffles plus a fixed-order
-// cross-warp sum (deterministic); alpha/beta are rounded to T and the vector
-// updates use T arithmetic exactly like the reference.  The correction v is
-// written to `corr` ([C][nb][bh][bw]).
-// Kernel 2 (k_oras_blend): the reference blends u += w_b * v_b sequentially
-// in block order.  Here every pixel gathers its (at most 3x3) covering
-// blocks in ascending block index, which is the same summation order, so the
-// blend is race-free and bit-identical.  The partition-of-unity weights are
-// either read (kernel-table path) or recomputed on the fly in double with
-// the exact operation order of build_decomposition (solver.py:142-197),
-// which saves streaming a weight array of the size of the image.
+//
+// k_oras_local: one CTA per (block, channel, tile).  The block's mask is
+// staged in shared memory, its residual in registers (each thread owns PPT
+// pixels, strided by the CTA size so warps read whole rows); the search
+// direction p is staged in shared memory for the 5-point stencil and the
+// local CG runs entirely on-chip: dots in double, reduced by warp shuffles
+// plus a fixed-order cross-warp sum (deterministic); alpha/beta rounded to
+// T and the vector updates in T exactly like the reference.  The kernel
+// writes the WEIGHTED correction T(w_b) * v_b -- the very product the
+// reference forms in its blend loop (numba_impl.py:261-263) -- into `corr`
+// ([tile][C][nb][bh][bw]).
+//
+// k_oras_blend: the reference adds u += w_b * v_b sequentially in block
+// order.  Every pixel gathers its (at most 3x3) covering blocks in
+// ascending block index -- the same summation order -- so the blend is
+// race-free and bit-identical, and with pre-weighted corrections it is a
+// pure gather-add.
+//
+// k_block_weights: the partition-of-unity weights of build_decomposition
+// (solver.py:142-197), recomputed on the device in double with the exact
+// operation order (pointwise total over covering blocks in block order,
+// last covering block takes 1 - sum of the others), cast to T.
 #include "kernels.cuh"
 
 namespace sp {
+
+// ORAS statistics (jobs, local CG iterations, jobs converged on entry);
+// collected only while enabled through sp_stats (tracing aid)
+__device__ unsigned long long g_oras_stats[4];
+__device__ int g_stats_on;
+
+// kernel choice for float blocks <= 32x32: warp-per-job (default) or the
+// 256-thread CTA kernel (sp_oras_variant, for A/B measurements)
+static int oras_use_warp = 0;
+int oras_variant(int v) {
+  if (v >= 0) oras_use_warp = v;
+  return oras_use_warp;
+}
+
+int oras_stats(int enable, unsigned long long* out) {
+  if (out) SP_CUDA(cudaMemcpyFromSymbol(out, g_oras_stats, sizeof(unsigned long long) * 4));
+  if (enable >= 0) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    SP_CUDA(cudaMemcpyToSymbol(g_oras_stats, z, sizeof(z)));
+    SP_CUDA(cudaMemcpyToSymbol(g_stats_on, &enable, sizeof(int)));
+  }
+  return 0;
+}
 
 namespace {
 
 constexpr int NT = 256;
 
-template <typename T, int PPT>
-__global__ void __launch_bounds__(NT) k_oras_local(
+// Specialization for the default 32-wide blocks (bw == 32, bh <= 32): lane =
+// column, warp w owns rows w, w+8, w+16, w+24.  No integer division, the
+// stencil is branch-free (absent neighbours add an exact +0.0), and p is
+// staged in shared memory as double so each neighbour costs one LDS.64
+// instead of a load plus a conversion.  Arithmetic is identical to the
+// generic kernel below.
+template <typename T>
+__global__ void __launch_bounds__(NT, 4) k_oras_local32(
     const T* __restrict__ r, const uint8_t* __restrict__ m,
-    const double* __restrict__ tau_src, double tau_scale,
-    const int* __restrict__ ys, const int* __restrict__ xs, int nbx, int bh, int bw,
-    int H, int W, double gamma, long cap, double inv_h2, T* __restrict__ corr) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* ps = reinterpret_cast<T*>(smem_raw);
+    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
+    const int* __restrict__ xs, int nbx, int bh, int H, int W, int stride, double gamma,
+    long cap, double inv_h2, const T* __restrict__ weights, T* __restrict__ corr,
+    const int* __restrict__ active) {
+  constexpr int PPT = 4, BWD = 32;
+  __shared__ double psd[32 * BWD + 2 * BWD];  // p as double, one guard row each side
+  __shared__ uint8_t ms[32 * BWD];
   __shared__ double red0[NT / 32], red1[NT / 32], red2[NT / 32];
   const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y, nb = gridDim.x;
-  const int y0 = ys[bi / nbx], x0 = xs[bi % nbx];
-  const int npx = bh * bw;
+  const int tile = blockIdx.z;
+  if (active && !active[tile]) return;
+  // block origin: arithmetic _starts (solver.py:134-139) when stride > 0,
+  // else the caller's table (kernel-table path with arbitrary starts)
+  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
+  const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
+  const int x0 = stride > 0 ? block_start(kxb, stride, W, BWD) : xs[kxb];
+  const int npx = bh * BWD;
   const size_t plane = (size_t)H * W;
-  const T* rc = r + (size_t)ch * plane;
+  const T* rc = r + ((size_t)tile * C + ch) * plane;
+  m += (size_t)tile * plane;
+  const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* pd = psd + BWD;  // pd[-32 .. npx + 31] addressable
+  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
 
-  T res[PPT], v[PPT], p[PPT], ap[PPT];
+  T res[PPT], v[PPT], p[PPT], wgt[PPT];
   double diag[PPT];
-  unsigned flags[PPT];  // bit0 valid, bit1 masked, bits4..7 in-block unmasked nbr
-  int kk[PPT];
+  unsigned flags[PPT];
+  // issue every global load of the job up front (residual, mask, blend
+  // weights): the job is short and otherwise pays several DRAM round trips
+  const T* wb = weights + (size_t)bi * npx;
+#pragma unroll
+  for (int s = 0; s < PPT; ++s) {
+    const int i = w + 8 * s;
+    res[s] = (T)0;
+    wgt[s] = (T)0;
+    if (i < bh) {
+      const size_t g = (size_t)(y0 + i) * W + (x0 + j);
+      ms[i * BWD + j] = m[g];
+      res[s] = rc[g];
+      wgt[s] = wb[i * BWD + j];
+    }
+  }
+  // guard rows of the staged p stay zero
+  if (threadIdx.x < BWD) {
+    psd[threadIdx.x] = 0.0;
+    psd[BWD + npx + threadIdx.x] = 0.0;
+  }
+  __syncthreads();
   double rs_part = 0.0;
 #pragma unroll
   for (int s = 0; s < PPT; ++s) {
-    int k = threadIdx.x + s * NT;
-    kk[s] = k;
+    const int i = w + 8 * s, k = i * BWD + j;
     flags[s] = 0;
-    res[s] = v[s] = p[s] = ap[s] = (T)0;
+    v[s] = p[s] = (T)0;
     diag[s] = 0.0;
-    if (k < npx) {
-      int i = k / bw, j = k - (k / bw) * bw;
-      int gy = y0 + i, gx = x0 + j;
-      size_t g = (size_t)gy * W + gx;
+    if (i < bh) {
+      const int gy = y0 + i, gx = x0 + j;
       unsigned f = 1u;
-      if (m[g]) f |= 2u;
+      if (ms[k]) f |= 2u;
       double d = 0.0;
       if (gy > 0) {
-        if (i > 0) { d += 1.0; if (!m[g - W]) f |= 16u; } else d += 1.0 - gamma;
+        if (i > 0) { d += 1.0; if (!ms[k - BWD]) f |= 16u; } else d += 1.0 - gamma;
       }
       if (gy < H - 1) {
-        if (i < bh - 1) { d += 1.0; if (!m[g + W]) f |= 32u; } else d += 1.0 - gamma;
+        if (i < bh - 1) { d += 1.0; if (!ms[k + BWD]) f |= 32u; } else d += 1.0 - gamma;
       }
       if (gx > 0) {
-        if (j > 0) { d += 1.0; if (!m[g - 1]) f |= 64u; } else d += 1.0 - gamma;
+        if (j > 0) { d += 1.0; if (!ms[k - 1]) f |= 64u; } else d += 1.0 - gamma;
       }
       if (gx < W - 1) {
-        if (j < bw - 1) { d += 1.0; if (!m[g + 1]) f |= 128u; } else d += 1.0 - gamma;
+        if (j < BWD - 1) { d += 1.0; if (!ms[k + 1]) f |= 128u; } else d += 1.0 - gamma;
       }
       flags[s] = f;
       diag[s] = d;
-      res[s] = rc[g];
       p[s] = res[s];
       rs_part += (double)res[s] * (double)res[s];
     }
   }
   double rs = cta_sum<NT>(rs_part, red0);
-  const double tau = tau_scale * tau_src[ch];
+  long it = 0;
+  int phase = 0;
+  T ap[PPT];
+  // single-precision fast path: the stencil runs in float (one rounding of
+  // d*p - acc in float instead of double-then-float) and the per-thread dot
+  // partials are float over its 4 pixels; cross-thread sums stay double.
+  // The local CG is an inexact smoother whose dots already differ from the
+  // reference in summation order, so this only moves the iterate at the
+  // 1e-7 level (solver parity is tolerance based, tests/test_solver_gpu.py).
+  constexpr bool kF32 = sizeof(T) == 4;
+  float* pf = reinterpret_cast<float*>(pd);
+  float diagf[PPT];
+#pragma unroll
+  for (int s = 0; s < PPT; ++s) diagf[s] = (float)diag[s];
+  const float inv_h2f = (float)inv_h2;
+  while (rs > tau && it < cap) {
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+      const int i = w + 8 * s;
+      if (i < bh) {
+        if (kF32) pf[i * BWD + j] = (float)p[s];
+        else pd[i * BWD + j] = (double)p[s];
+      }
+    }
+    __syncthreads();
+    double pap_part = 0.0;
+    float pap_f = 0.0f;
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+      const unsigned f = flags[s];
+      const int k = (w + 8 * s) * BWD + j;
+      const int kl = j > 0 ? k - 1 : k, kr = j < BWD - 1 ? k + 1 : k;
+      // guard rows / lane clamps keep every address valid; absent
+      // neighbours contribute +0.0
+      if (kF32) {
+        float acc = 0.0f;
+        acc += (f & 16u) ? pf[k - BWD] : 0.0f;
+        acc += (f & 32u) ? pf[k + BWD] : 0.0f;
+        acc += (f & 64u) ? pf[kl] : 0.0f;
+        acc += (f & 128u) ? pf[kr] : 0.0f;
+        const float pv = (float)p[s];
+        float a = (f & 2u) ? pv : (diagf[s] * pv - acc) * inv_h2f;
+        a = (f & 1u) ? a : 0.0f;
+        ap[s] = (T)a;
+        pap_f += pv * a;
+      } else {
+        double acc = 0.0;
+        acc += (f & 16u) ? pd[k - BWD] : 0.0;
+        acc += (f & 32u) ? pd[k + BWD] : 0.0;
+        acc += (f & 64u) ? pd[kl] : 0.0;
+        acc += (f & 128u) ? pd[kr] : 0.0;
+        const double pdv = (double)p[s];
+        const T a = (f & 2u) ? p[s] : (T)((diag[s] * pdv - acc) * inv_h2);
+        ap[s] = (f & 1u) ? a : (T)0;
+        pap_part += pdv * (double)ap[s];
+      }
+    }
+    if (kF32) pap_part = (double)pap_f;
+    const double pap = cta_sum<NT>(pap_part, phase ? red2 : red1);
+    if (pap <= 0.0) break;
+    const T alpha = (T)(rs / pap);
+    double rsn_part = 0.0;
+    float rsn_f = 0.0f;
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+      if (!(flags[s] & 1u)) continue;
+      v[s] = v[s] + alpha * p[s];
+      res[s] = res[s] - alpha * ap[s];
+      if (kF32) rsn_f += (float)res[s] * (float)res[s];
+      else rsn_part += (double)res[s] * (double)res[s];
+    }
+    if (kF32) rsn_part = (double)rsn_f;
+    const double rsn = cta_sum<NT>(rsn_part, phase ? red1 : red2);
+    const T beta = (T)(rsn / rs);
+    rs = rsn;
+#pragma unroll
+    for (int s = 0; s < PPT; ++s)
+      if (flags[s] & 1u) p[s] = res[s] + beta * p[s];
+    ++it;
+    phase ^= 1;
+  }
+  T* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)npx;
+#pragma unroll
+  for (int s = 0; s < PPT; ++s) {
+    const int i = w + 8 * s, k = i * BWD + j;
+    if (i < bh) out[k] = wgt[s] * v[s];
+  }
+  if (threadIdx.x == 0 && g_stats_on) {
+    atomicAdd(&g_oras_stats[0], 1ull);
+    atomicAdd(&g_oras_stats[1], (unsigned long long)it);
+    if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
+    atomicMax(&g_oras_stats[3], (unsigned long long)it);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Barrier-free variant for float blocks up to 32 x 32 (the default ORAS
+// configuration): ONE WARP per (block, channel, tile) job.  Lane j owns
+// column j; the 32 rows of p, res and A p live in registers (fully unrolled),
+// up/down neighbours are the adjacent registers, left/right come from one
+// shuffle each, and the column masks are 32-bit words so every neighbour
+// test is a bit test.  Both CG dots are exact float products accumulated in
+// double per lane and reduced with warp shuffles: no __syncthreads at all.
+// v and the local diagonal live in shared memory (4 KB each per warp).
+// ---------------------------------------------------------------------------
+constexpr int WJ = 4;  // jobs (warps) per CTA
+
+__global__ void __launch_bounds__(WJ * 32) k_oras_warp(
+    const float* __restrict__ r, const uint8_t* __restrict__ m,
+    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
+    const int* __restrict__ xs, int nby, int nbx, int bh, int bw, int H, int W, int C,
+    int ntile, int stride, double gamma, long cap, float inv_h2,
+    const float* __restrict__ weights, float* __restrict__ corr,
+    const int* __restrict__ active) {
+  __shared__ float vs_all[WJ][32][33];
+  __shared__ float dg_all[WJ][32][33];
+  const int warp = threadIdx.x >> 5, j = threadIdx.x & 31;
+  const int nb = nby * nbx;
+  const long job = (long)blockIdx.x * WJ + warp;
+  if (job >= (long)nb * C * ntile) return;
+  const int bi = (int)(job % nb);
+  const long rest = job / nb;
+  const int ch = (int)(rest % C), tile = (int)(rest / C);
+  if (active && !active[tile]) return;
+  float(*vs)[33] = vs_all[warp];
+  float(*dg)[33] = dg_all[warp];
+  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
+  const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
+  const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
+  const size_t plane = (size_t)H * W;
+  const float* rc = r + ((size_t)tile * C + ch) * plane;
+  const uint8_t* mt = m + (size_t)tile * plane;
+  const float* wb = weights + (size_t)bi * bh * bw;
+  const bool lane_ok = j < bw;
+  const int gx = x0 + j;
+  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
+
+  float p[32], res[32], ap[32], wgt[32];
+  uint32_t mcol = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    res[i] = 0.0f;
+    wgt[i] = 0.0f;
+    if (i < bh && lane_ok) {
+      const size_t g = (size_t)(y0 + i) * W + gx;
+      if (mt[g]) mcol |= 1u << i;
+      res[i] = rc[g];
+      wgt[i] = wb[i * bw + j];
+    }
+  }
+  const uint32_t valid = lane_ok ? (bh >= 32 ? 0xFFFFFFFFu : ((1u << bh) - 1u)) : 0u;
+  const uint32_t nm = ~mcol & valid;                    // unmasked rows
+  const uint32_t ml = __shfl_up_sync(0xFFFFFFFFu, nm, 1);
+  const uint32_t mr = __shfl_down_sync(0xFFFFFFFFu, nm, 1);
+  const uint32_t upok = (nm << 1) & valid;              // row i-1 unmasked
+  const uint32_t dnok = (nm >> 1) & valid;              // row i+1 unmasked
+  const uint32_t lfok = (j > 0 && lane_ok) ? (ml & valid) : 0u;
+  const uint32_t rtok = (j < bw - 1) ? (mr & valid) : 0u;
+  // Robin-closed diagonal (numba_impl.py:196-226), double in reference order
+  double rs = 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double d = 0.0;
+    if (i < bh && lane_ok) {
+      const int gy = y0 + i;
+      if (gy > 0) d += (i > 0) ? 1.0 : 1.0 - gamma;
+      if (gy < H - 1) d += (i < bh - 1) ? 1.0 : 1.0 - gamma;
+      if (gx > 0) d += (j > 0) ? 1.0 : 1.0 - gamma;
+      if (gx < W - 1) d += (j < bw - 1) ? 1.0 : 1.0 - gamma;
+    }
+    dg[i][j] = (float)d;
+    vs[i][j] = 0.0f;
+    p[i] = res[i];
+    rs += (double)res[i] * (double)res[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xFFFFFFFFu, rs, o);
+  __syncwarp();
+  long it = 0;
+  while (rs > tau && it < cap) {
+    double pap = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float pl = __shfl_up_sync(0xFFFFFFFFu, p[i], 1);
+      const float pr = __shfl_down_sync(0xFFFFFFFFu, p[i], 1);
+      float acc = 0.0f;
+      if (i > 0) acc += (upok >> i) & 1u ? p[i - 1] : 0.0f;
+      if (i < 31) acc += (dnok >> i) & 1u ? p[i + 1] : 0.0f;
+      acc += (lfok >> i) & 1u ? pl : 0.0f;
+      acc += (rtok >> i) & 1u ? pr : 0.0f;
+      float a = ((mcol >> i) & 1u) ? p[i] : (dg[i][j] * p[i] - acc) * inv_h2;
+      a = ((valid >> i) & 1u) ? a : 0.0f;
+      ap[i] = a;
+      pap += (double)p[i] * (double)a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pap += __shfl_xor_sync(0xFFFFFFFFu, pap, o);
+    if (pap <= 0.0) break;
+    const float alpha = (float)(rs / pap);
+    double rsn = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if ((valid >> i) & 1u) {
+        vs[i][j] = vs[i][j] + alpha * p[i];
+        res[i] = res[i] - alpha * ap[i];
+      }
+      rsn += (double)res[i] * (double)res[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rsn += __shfl_xor_sync(0xFFFFFFFFu, rsn, o);
+    const float beta = (float)(rsn / rs);
+    rs = rsn;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if ((valid >> i) & 1u) p[i] = res[i] + beta * p[i];
+    ++it;
+  }
+  __syncwarp();
+  float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if ((valid >> i) & 1u) out[i * bw + j] = wgt[i] * vs[i][j];
+  if (j == 0 && g_stats_on) {
+    atomicAdd(&g_oras_stats[0], 1ull);
+    atomicAdd(&g_oras_stats[1], (unsigned long long)it);
+    if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
+    atomicMax(&g_oras_stats[3], (unsigned long long)it);
+  }
+}
+
+template <typename T, int PPT>
+__global__ void __launch_bounds__(NT) k_oras_local(
+    const T* __restrict__ r, const uint8_t* __restrict__ m,
+    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
+    const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W, double gamma,
+    long cap, double inv_h2, const T* __restrict__ weights, T* __restrict__ corr,
+    const int* __restrict__ active) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* ps = reinterpret_cast<T*>(smem_raw);
+  __shared__ double red0[NT / 32], red1[NT / 32], red2[NT / 32];
+  const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y, nb = gridDim.x;
+  const int tile = blockIdx.z;
+  if (active && !active[tile]) return;
+  const int y0 = ys[bi / nbx], x0 = xs[bi % nbx];
+  const int npx = bh * bw;
+  const size_t plane = (size_t)H * W;
+  const T* rc = r + ((size_t)tile * C + ch) * plane;
+  m += (size_t)tile * plane;
+  uint8_t* ms = reinterpret_cast<uint8_t*>(ps + npx);
+
+  T res[PPT], v[PPT], p[PPT], ap[PPT];
+  double diag[PPT];
+  unsigned flags[PPT];  // bit0 valid, bit1 masked, bits4..7 in-block unmasked nbr
+  // stage the mask (one byte per pixel) and issue every residual load first
+#pragma unroll
+  for (int s = 0; s < PPT; ++s) {
+    const int k = threadIdx.x + s * NT;
+    res[s] = (T)0;
+    if (k < npx) {
+      const int i = k / bw, j = k - i * bw;
+      const size_t g = (size_t)(y0 + i) * W + (x0 + j);
+      ms[k] = m[g];
+      res[s] = rc[g];
+    }
+  }
+  __syncthreads();
+  double rs_part = 0.0;
+#pragma unroll
+  for (int s = 0; s < PPT; ++s) {
+    const int k = threadIdx.x + s * NT;
+    flags[s] = 0;
+    v[s] = p[s] = ap[s] = (T)0;
+    diag[s] = 0.0;
+    if (k < npx) {
+      const int i = k / bw, j = k - i * bw;
+      const int gy = y0 + i, gx = x0 + j;
+      unsigned f = 1u;
+      if (ms[k]) f |= 2u;
+      // Robin-closed local diagonal (numba_impl.py:196-226): in-block
+      // neighbours count 1, image-interior block sides 1 - gamma
+      double d = 0.0;
+      if (gy > 0) {
+        if (i > 0) { d += 1.0; if (!ms[k - bw]) f |= 16u; } else d += 1.0 - gamma;
+      }
+      if (gy < H - 1) {
+        if (i < bh - 1) { d += 1.0; if (!ms[k + bw]) f |= 32u; } else d += 1.0 - gamma;
+      }
+      if (gx > 0) {
+        if (j > 0) { d += 1.0; if (!ms[k - 1]) f |= 64u; } else d += 1.0 - gamma;
+      }
+      if (gx < W - 1) {
+        if (j < bw - 1) { d += 1.0; if (!ms[k + 1]) f |= 128u; } else d += 1.0 - gamma;
+      }
+      flags[s] = f;
+      diag[s] = d;
+      p[s] = res[s];
+      rs_part += (double)res[s] * (double)res[s];
+    }
+  }
+  double rs = cta_sum<NT>(rs_part, red0);
+  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
   long it = 0;
   int phase = 0;
   while (rs > tau && it < cap) {
-    // stage p for the stencil
 #pragma unroll
     for (int s = 0; s < PPT; ++s)
-      if (flags[s] & 1u) ps[kk[s]] = p[s];
+      if (flags[s] & 1u) ps[threadIdx.x + s * NT] = p[s];
     __syncthreads();
     double pap_part = 0.0;
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
-      unsigned f = flags[s];
+      const unsigned f = flags[s];
       if (!(f & 1u)) continue;
       T a;
       if (f & 2u) {
         a = p[s];
       } else {
-        int k = kk[s];
+        const int k = threadIdx.x + s * NT;
         double acc = 0.0;
         if (f & 16u) acc += (double)ps[k - bw];
         if (f & 32u) acc += (double)ps[k + bw];
@@ -107,9 +470,9 @@ __global__ void __launch_bounds__(NT) k_oras_local(
       ap[s] = a;
       pap_part += (double)p[s] * (double)a;
     }
-    double pap = cta_sum<NT>(pap_part, phase ? red2 : red1);
+    const double pap = cta_sum<NT>(pap_part, phase ? red2 : red1);
     if (pap <= 0.0) break;
-    T alpha = (T)(rs / pap);
+    const T alpha = (T)(rs / pap);
     double rsn_part = 0.0;
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
@@ -118,8 +481,8 @@ __global__ void __launch_bounds__(NT) k_oras_local(
       res[s] = res[s] - alpha * ap[s];
       rsn_part += (double)res[s] * (double)res[s];
     }
-    double rsn = cta_sum<NT>(rsn_part, phase ? red1 : red2);
-    T beta = (T)(rsn / rs);
+    const double rsn = cta_sum<NT>(rsn_part, phase ? red1 : red2);
+    const T beta = (T)(rsn / rs);
     rs = rsn;
 #pragma unroll
     for (int s = 0; s < PPT; ++s)
@@ -127,95 +490,145 @@ __global__ void __launch_bounds__(NT) k_oras_local(
     ++it;
     phase ^= 1;
   }
-  T* out = corr + ((size_t)ch * nb + bi) * (size_t)npx;
+  T* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)npx;
+  const T* wb = weights + (size_t)bi * npx;
 #pragma unroll
-  for (int s = 0; s < PPT; ++s)
-    if (flags[s] & 1u) out[kk[s]] = v[s];
+  for (int s = 0; s < PPT; ++s) {
+    const int k = threadIdx.x + s * NT;
+    if (flags[s] & 1u) out[k] = wb[k] * v[s];
+  }
 }
 
-// covering-block tables: for row y, blocks ky in [row_k0[y], row_k0[y]+row_n[y])
-template <typename T>
-__global__ void k_oras_blend(T* __restrict__ u, const T* __restrict__ corr,
-                             const T* __restrict__ weights,
-                             const int* __restrict__ ys, const int* __restrict__ xs,
-                             const int* __restrict__ row_k0, const int* __restrict__ row_n,
-                             const int* __restrict__ col_k0, const int* __restrict__ col_n,
-                             int nby, int nbx, int bh, int bw, int H, int W, int C,
-                             int overlap) {
-  int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
-  if (x >= W || y >= H) return;
-  const int nb = nby * nbx;
-  const size_t plane = (size_t)H * W, k = (size_t)y * W + x, npx = (size_t)bh * bw;
-  const int ky0 = row_k0[y], nky = row_n[y], kx0 = col_k0[x], nkx = col_n[x];
-  // weights of the covering blocks in block order (<= 3x3)
-  double wv[9];
-  int cnt = 0;
-  if (weights) {
-    for (int a = 0; a < nky; ++a)
-      for (int b = 0; b < nkx; ++b) {
-        int ky = ky0 + a, kx = kx0 + b, bi = ky * nbx + kx;
-        int i = y - ys[ky], j = x - xs[kx];
-        wv[cnt++] = (double)weights[(size_t)bi * npx + (size_t)i * bw + j];
-      }
-  } else {
-    // solver.py:160-197: raw = min(dist_to_inner_edge + 1, overlap),
-    // normalized by the pointwise total; the last covering block takes the
-    // exact complement 1 - (sum of the earlier normalized weights).
-    const double big = (double)(H > W ? H : W);
-    double raw[9], total = 0.0;
-    for (int a = 0; a < nky; ++a)
-      for (int b = 0; b < nkx; ++b) {
-        int yb = ys[ky0 + a], xb = xs[kx0 + b];
-        double ii = (double)(y - yb), jj = (double)(x - xb);
-        double di = big;
-        if (yb > 0) di = fmin(di, ii);
-        if (yb + bh < H) di = fmin(di, (double)(bh - 1) - ii);
-        if (xb > 0) di = fmin(di, jj);
-        if (xb + bw < W) di = fmin(di, (double)(bw - 1) - jj);
-        double rw = fmin(di + 1.0, (double)overlap);
-        raw[cnt++] = rw;
-      }
-    // total accumulates over all blocks in block order (same adds)
-    for (int q = 0; q < cnt; ++q) total += raw[q];
-    double acc = 0.0;
-    for (int q = 0; q < cnt; ++q) {
-      double wn = (q == cnt - 1) ? 1.0 - acc : raw[q] / total;
+// partition-of-unity weight of each covering block of pixel (x, y), in
+// block order (<= 3x3); fully unrolled so the arrays stay in registers
+__device__ __forceinline__ void pou_weights(int x, int y, const int* __restrict__ ys,
+                                            const int* __restrict__ xs, int ky0, int nky,
+                                            int kx0, int nkx, int bh, int bw, int H, int W,
+                                            int overlap, double wv[9]) {
+  const double big = (double)(H > W ? H : W);
+  const int last = (nky - 1) * 3 + (nkx - 1);
+  double raw[9], total = 0.0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const int a = q / 3, b = q % 3;
+    raw[q] = 0.0;
+    if (a < nky && b < nkx) {
+      int yb = ys[ky0 + a], xb = xs[kx0 + b];
+      double ii = (double)(y - yb), jj = (double)(x - xb);
+      double di = big;
+      if (yb > 0) di = fmin(di, ii);
+      if (yb + bh < H) di = fmin(di, (double)(bh - 1) - ii);
+      if (xb > 0) di = fmin(di, jj);
+      if (xb + bw < W) di = fmin(di, (double)(bw - 1) - jj);
+      raw[q] = fmin(di + 1.0, (double)overlap);
+      total += raw[q];
+    }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const int a = q / 3, b = q % 3;
+    wv[q] = 0.0;
+    if (a < nky && b < nkx) {
+      double wn = (q == last) ? 1.0 - acc : raw[q] / total;
       acc += wn;
       wv[q] = wn;
     }
   }
-  for (int c = 0; c < C; ++c) {
-    T uv = u[c * plane + k];
-    int q = 0;
-    for (int a = 0; a < nky; ++a)
-      for (int b = 0; b < nkx; ++b, ++q) {
-        int ky = ky0 + a, kx = kx0 + b, bi = ky * nbx + kx;
-        int i = y - ys[ky], j = x - xs[kx];
-        T cv = corr[((size_t)c * nb + bi) * npx + (size_t)i * bw + j];
-        uv = uv + (T)wv[q] * cv;
+}
+
+template <typename T>
+__global__ void k_block_weights(T* __restrict__ weights, const int* __restrict__ ys,
+                                const int* __restrict__ xs, const int* __restrict__ row_k0,
+                                const int* __restrict__ row_n, const int* __restrict__ col_k0,
+                                const int* __restrict__ col_n, int nbx, int bh, int bw, int H,
+                                int W, int overlap) {
+  const int bi = blockIdx.y;
+  const int npx = bh * bw;
+  const int ky = bi / nbx, kx = bi % nbx;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npx; k += gridDim.x * blockDim.x) {
+    const int i = k / bw, j = k - i * bw;
+    const int y = ys[ky] + i, x = xs[kx] + j;
+    const int ky0 = row_k0[y], nky = row_n[y], kx0 = col_k0[x], nkx = col_n[x];
+    double wv[9];
+    pou_weights(x, y, ys, xs, ky0, nky, kx0, nkx, bh, bw, H, W, overlap, wv);
+    const int q = (ky - ky0) * 3 + (kx - kx0);
+    double w = 0.0;
+#pragma unroll
+    for (int t = 0; t < 9; ++t)
+      if (t == q) w = wv[t];
+    weights[(size_t)bi * npx + k] = (T)w;
+  }
+}
+
+// u += sum over covering blocks (block order) of the weighted corrections.
+// grid (nbx_cta, ntile * C): CTA walks the plane's 32x8 pixel tiles.
+template <typename T>
+__global__ void __launch_bounds__(256) k_oras_blend(
+    T* __restrict__ u, const T* __restrict__ corr, const int* __restrict__ ys,
+    const int* __restrict__ xs, const int* __restrict__ row_k0,
+    const int* __restrict__ row_n, const int* __restrict__ col_k0,
+    const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int C,
+    const int* __restrict__ active) {
+  const int z = blockIdx.y, tile = z / C;
+  if (active && !active[tile]) return;
+  const int nb = nby * nbx;
+  const size_t plane = (size_t)H * W, npx = (size_t)bh * bw;
+  T* uc = u + (size_t)z * plane;
+  const T* cc = corr + (size_t)z * nb * npx;
+  const int ntx = (W + 31) / 32, nty = (H + 7) / 8, per = ntx * nty;
+  for (int t = blockIdx.x; t < per; t += gridDim.x) {
+    const int x = (t % ntx) * 32 + threadIdx.x, y = (t / ntx) * 8 + threadIdx.y;
+    if (x >= W || y >= H) continue;
+    const int ky0 = row_k0[y], nky = row_n[y], kx0 = col_k0[x], nkx = col_n[x];
+    T cv[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int a = q / 3, b = q % 3;
+      cv[q] = (T)0;
+      if (a < nky && b < nkx) {
+        const int ky = ky0 + a, kx = kx0 + b;
+        cv[q] = cc[(size_t)(ky * nbx + kx) * npx + (size_t)(y - ys[ky]) * bw + (x - xs[kx])];
       }
-    u[c * plane + k] = uv;
+    }
+    const size_t k = (size_t)y * W + x;
+    T uv = uc[k];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int a = q / 3, b = q % 3;
+      if (a < nky && b < nkx) uv = uv + cv[q];
+    }
+    uc[k] = uv;
   }
 }
 
 }  // namespace
 
 template <typename T>
-int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src,
-                      double tau_scale, const int* ys, const int* xs, int nby, int nbx,
-                      int bh, int bw, int H, int W, int C, double gamma, long cap,
-                      double inv_h2, T* corr, cudaStream_t s) {
-  int npx = bh * bw;
-  dim3 grid(nby * nbx, C);
-  size_t sm = (size_t)npx * sizeof(T);
-  if (npx <= NT * 4) {
-    k_oras_local<T, 4><<<grid, NT, sm, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh,
-                                            bw, H, W, gamma, cap, inv_h2, corr);
+int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, double tau_scale,
+                      const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
+                      int W, int C, double gamma, long cap, double inv_h2, const T* weights,
+                      T* corr, cudaStream_t s, int ntile, const int* active, int stride) {
+  const int npx = bh * bw;
+  dim3 grid(nby * nbx, C, ntile);
+  size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
+  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_use_warp) {
+    const long njobs = (long)nby * nbx * C * ntile;
+    k_oras_warp<<<(unsigned)((njobs + WJ - 1) / WJ), WJ * 32, 0, s>>>(
+        (const float*)r, m, tau_src, tau_scale, ys, xs, nby, nbx, bh, bw, H, W, C, ntile,
+        stride, gamma, cap, (float)inv_h2, (const float*)weights, (float*)corr, active);
+  } else if (bw == 32 && bh <= 32) {
+    k_oras_local32<T><<<grid, NT, 0, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, H, W,
+                                          stride, gamma, cap, inv_h2, weights, corr, active);
+  } else if (npx <= NT * 4) {
+    k_oras_local<T, 4><<<grid, NT, sm, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
+                                            W, gamma, cap, inv_h2, weights, corr, active);
   } else if (npx <= NT * 16) {
     auto kern = k_oras_local<T, 16>;
-    if (sm > 48 * 1024) SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<grid, NT, sm, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H, W, gamma,
-                              cap, inv_h2, corr);
+    if (sm > 48 * 1024)
+      SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<grid, NT, sm, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H, W, gamma, cap,
+                              inv_h2, weights, corr, active);
   } else {
     set_error("oras block of %d pixels exceeds the 4096-pixel kernel limit", npx);
     return -2;
@@ -225,25 +638,44 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src,
 }
 
 template <typename T>
-int oras_blend_launch(T* u, const T* corr, const T* weights, const int* ys, const int* xs,
-                      const int* row_k0, const int* row_n, const int* col_k0,
-                      const int* col_n, int nby, int nbx, int bh, int bw, int H, int W,
-                      int C, int overlap, cudaStream_t s) {
-  dim3 grid(cdiv(W, 32), cdiv(H, 8));
-  k_oras_blend<T><<<grid, dim3(32, 8), 0, s>>>(u, corr, weights, ys, xs, row_k0, row_n,
-                                               col_k0, col_n, nby, nbx, bh, bw, H, W, C,
-                                               overlap);
+int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
+                      const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
+                      int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile,
+                      const int* active) {
+  long per = (long)cdiv(W, 32) * cdiv(H, 8);
+  long nz = (long)ntile * C;
+  long nbx_cta = (2L * 148 * 8 + nz - 1) / nz;
+  if (nbx_cta > per) nbx_cta = per;
+  if (nbx_cta < 1) nbx_cta = 1;
+  k_oras_blend<T><<<dim3((unsigned)nbx_cta, (unsigned)nz), dim3(32, 8), 0, s>>>(
+      u, corr, ys, xs, row_k0, row_n, col_k0, col_n, nby, nbx, bh, bw, H, W, C, active);
   SP_CHECK_LAUNCH();
   return 0;
 }
 
-#define INST(T)                                                                        \
-  template int oras_local_launch<T>(const T*, const uint8_t*, const double*, double,    \
-                                    const int*, const int*, int, int, int, int, int,    \
-                                    int, int, double, long, double, T*, cudaStream_t);  \
-  template int oras_blend_launch<T>(T*, const T*, const T*, const int*, const int*,     \
-                                    const int*, const int*, const int*, const int*,     \
-                                    int, int, int, int, int, int, int, int, cudaStream_t);
+template <typename T>
+int block_weights_launch(T* weights, const int* ys, const int* xs, const int* row_k0,
+                         const int* row_n, const int* col_k0, const int* col_n, int nby,
+                         int nbx, int bh, int bw, int H, int W, int overlap, cudaStream_t s) {
+  const int npx = bh * bw;
+  dim3 grid(cdiv(npx, 256), nby * nbx);
+  k_block_weights<T><<<grid, 256, 0, s>>>(weights, ys, xs, row_k0, row_n, col_k0, col_n, nbx,
+                                          bh, bw, H, W, overlap);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+#define INST(T)                                                                            \
+  template int oras_local_launch<T>(const T*, const uint8_t*, const double*, double,        \
+                                    const int*, const int*, int, int, int, int, int, int,   \
+                                    int, double, long, double, const T*, T*, cudaStream_t,  \
+                                    int, const int*, int);                                  \
+  template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
+                                    const int*, const int*, const int*, int, int, int, int, \
+                                    int, int, int, cudaStream_t, int, const int*);          \
+  template int block_weights_launch<T>(T*, const int*, const int*, const int*, const int*,  \
+                                       const int*, const int*, int, int, int, int, int,     \
+                                       int, int, cudaStream_t);
 INST(float)
 INST(double)
 

@@ -6,7 +6,14 @@
 // across mask changes of the same geometry.  A V-cycle is recorded once into
 // a CUDA graph and replayed; the only host synchronisation in a solve is the
 // read-back of the per-channel residual norms for the tolerance test
-// (solver.py:358-368), exactly one 8*C-byte copy per V-cycle.
+// (solver.py:358-368), one small copy per V-cycle.
+//
+// A hierarchy holds `ntile` independent problems of the same shape (each
+// with its own mask): ntile = 1 is the global image; the RAS tonal
+// optimizer solves all of its 64x64 block-local systems as one batch
+// (tonal.py:343-354, 120-131).  Each tile keeps its own stopping decision:
+// tiles that have converged are switched off through a device flag array
+// that every kernel of the (graph-captured) V-cycle reads.
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -15,17 +22,6 @@
 #include "solver.cuh"
 
 namespace sp {
-
-template <typename T>
-int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src,
-                      double tau_scale, const int* ys, const int* xs, int nby, int nbx,
-                      int bh, int bw, int H, int W, int C, double gamma, long cap,
-                      double inv_h2, T* corr, cudaStream_t s);
-template <typename T>
-int oras_blend_launch(T* u, const T* corr, const T* weights, const int* ys, const int* xs,
-                      const int* row_k0, const int* row_n, const int* col_k0,
-                      const int* col_n, int nby, int nbx, int bh, int bw, int H, int W,
-                      int C, int overlap, cudaStream_t s);
 
 // covering tables for sorted block starts (host)
 void cover_tables(const std::vector<int>& starts, int size, int dim, std::vector<int>& k0,
@@ -56,19 +52,26 @@ Hier::~Hier() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (cap_stream) cudaStreamDestroy(cap_stream);
   for (auto& L : lv) {
-    for (void* p : {(void*)L.mask, L.values, L.u, L.b, L.r, L.corr, (void*)L.partial,
+    for (void* p : {(void*)L.mask, L.values, L.u, L.b, L.r, L.corr, L.weights, (void*)L.partial,
                     (void*)L.counter, (void*)L.norms, (void*)L.ys, (void*)L.xs,
                     (void*)L.row_k0, (void*)L.row_n, (void*)L.col_k0, (void*)L.col_n})
       if (p) cudaFree(p);
   }
+  if (d_active) cudaFree(d_active);
+  if (d_scratch) cudaFree(d_scratch);
   if (h_norms) cudaFreeHost(h_norms);
+  if (h_active) cudaFreeHost(h_active);
 }
 
 int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
-                int with_values) {
+                int with_values, int ntile) {
   *out = nullptr;
-  if (H < 1 || W < 1 || C < 1) {
-    set_error("bad hierarchy shape (%d, %d, %d)", C, H, W);
+  if (H < 1 || W < 1 || C < 1 || ntile < 1) {
+    set_error("bad hierarchy shape (%d tiles, %d, %d, %d)", ntile, C, H, W);
+    return -2;
+  }
+  if ((long)ntile * C > 65535) {
+    set_error("at most 65535 tile-channels per hierarchy (got %d x %d)", ntile, C);
     return -2;
   }
   if (cfg.block < cfg.overlap + 2 || cfg.overlap < 1) {
@@ -78,9 +81,11 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
   Hier* h = new Hier();
   h->dtype = dtype;
   h->C = C;
+  h->ntile = ntile;
   h->cfg = cfg;
   h->gamma = (1.0 - cfg.alpha) / (1.0 + cfg.alpha);
   const size_t es = dtype == SP_F64 ? 8 : 4;
+  const size_t ntc = (size_t)ntile * C;
   int hh = H, ww = W, level = 0;
   while (true) {
     Level L{};
@@ -100,18 +105,19 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     // solver.py:262-264: tau_c = rho * (bh*bw / N) * ||r_c||^2, cap = bh*bw
     L.tau_scale = cfg.rho * ((double)(L.bh * L.bw) / (double)((long)hh * ww));
     size_t plane = (size_t)hh * ww, nb = (size_t)L.nby * L.nbx;
-    size_t vec = es * C * plane;
+    size_t vec = es * ntc * plane;
     int rc = 0;
-    rc |= dalloc((void**)&L.mask, plane);
+    rc |= dalloc((void**)&L.mask, plane * ntile);
     rc |= dalloc(&L.u, vec);
     rc |= dalloc(&L.b, vec);
     rc |= dalloc(&L.r, vec);
-    rc |= dalloc(&L.corr, es * C * nb * L.bh * L.bw);
+    rc |= dalloc(&L.corr, es * ntc * nb * L.bh * L.bw);
+    rc |= dalloc(&L.weights, es * nb * L.bh * L.bw);
     if (with_values) rc |= dalloc(&L.values, vec);
     L.npart = residual_partials(hh, ww);
-    rc |= dalloc((void**)&L.partial, sizeof(double) * std::max((size_t)C * L.npart, red_partials() * 4));
-    rc |= dalloc((void**)&L.counter, sizeof(unsigned));
-    rc |= dalloc((void**)&L.norms, sizeof(double) * C);
+    rc |= dalloc((void**)&L.partial, sizeof(double) * ntc * L.npart);
+    rc |= dalloc((void**)&L.counter, sizeof(unsigned) * ntc);
+    rc |= dalloc((void**)&L.norms, sizeof(double) * ntc);
     rc |= dalloc((void**)&L.ys, sizeof(int) * L.nby);
     rc |= dalloc((void**)&L.xs, sizeof(int) * L.nbx);
     rc |= dalloc((void**)&L.row_k0, sizeof(int) * hh);
@@ -121,7 +127,7 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     h->lv.push_back(L);
     if (rc) { delete h; return -1; }
     Level& B = h->lv.back();
-    if (cudaMemset(B.counter, 0, sizeof(unsigned)) != cudaSuccess ||
+    if (cudaMemset(B.counter, 0, sizeof(unsigned) * ntc) != cudaSuccess ||
         cudaMemcpy(B.ys, ys.data(), sizeof(int) * B.nby, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(B.xs, xs.data(), sizeof(int) * B.nbx, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(B.row_k0, rk0.data(), sizeof(int) * hh, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -129,6 +135,18 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
         cudaMemcpy(B.col_k0, ck0.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(B.col_n, cn.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess) {
       set_error("hierarchy upload failed");
+      delete h;
+      return -1;
+    }
+    int wrc = dtype == SP_F64
+                  ? block_weights_launch<double>((double*)B.weights, B.ys, B.xs, B.row_k0,
+                                                 B.row_n, B.col_k0, B.col_n, B.nby, B.nbx,
+                                                 B.bh, B.bw, hh, ww, cfg.overlap, 0)
+                  : block_weights_launch<float>((float*)B.weights, B.ys, B.xs, B.row_k0,
+                                                B.row_n, B.col_k0, B.col_n, B.nby, B.nbx,
+                                                B.bh, B.bw, hh, ww, cfg.overlap, 0);
+    if (wrc || cudaDeviceSynchronize() != cudaSuccess) {
+      set_error("partition-of-unity weights failed");
       delete h;
       return -1;
     }
@@ -142,8 +160,12 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     hh = (hh + 1) / 2;
     ww = (ww + 1) / 2;
   }
-  if (cudaMallocHost((void**)&h->h_norms, sizeof(double) * C) != cudaSuccess) {
-    set_error("pinned alloc failed");
+  size_t scratch = sizeof(double) * (1024 + 8) * (size_t)ntile + 256;
+  if (cudaMallocHost((void**)&h->h_norms, sizeof(double) * ntc) != cudaSuccess ||
+      cudaMallocHost((void**)&h->h_active, sizeof(int) * ntile) != cudaSuccess ||
+      cudaMalloc((void**)&h->d_active, sizeof(int) * ntile) != cudaSuccess ||
+      cudaMalloc(&h->d_scratch, scratch) != cudaSuccess) {
+    set_error("hierarchy bookkeeping alloc failed");
     delete h;
     return -1;
   }
@@ -156,7 +178,7 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
 template <typename T>
 static int set_mask_t(Hier* h, const uint8_t* mask, const T* values, cudaStream_t s) {
   Level& L0 = h->lv[0];
-  size_t plane = (size_t)L0.H * L0.W;
+  size_t plane = (size_t)L0.H * L0.W * h->ntile;
   SP_CUDA(cudaMemcpyAsync(L0.mask, mask, plane, cudaMemcpyDeviceToDevice, s));
   bool vals = values != nullptr && L0.values != nullptr;
   if (vals)
@@ -166,7 +188,7 @@ static int set_mask_t(Hier* h, const uint8_t* mask, const T* values, cudaStream_
     Level& F = h->lv[i - 1];
     Level& G = h->lv[i];
     SP_TRY(restrict_mask<T>(F.mask, vals ? (const T*)F.values : nullptr, G.mask,
-                            vals ? (T*)G.values : nullptr, h->C, F.H, F.W, s));
+                            vals ? (T*)G.values : nullptr, h->C, F.H, F.W, s, h->ntile));
   }
   h->has_values = vals;
   return 0;
@@ -183,7 +205,8 @@ template <typename T>
 static int residual_lv(Hier* h, int lv, bool with_norms, cudaStream_t s) {
   Level& L = h->lv[lv];
   return residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
-                     with_norms ? L.norms : nullptr, h->C, L.H, L.W, 1.0, s);
+                     with_norms ? L.norms : nullptr, h->C, L.H, L.W, 1.0, s, h->ntile,
+                     h->d_active);
 }
 
 template <typename T>
@@ -193,10 +216,11 @@ static int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t 
     if (!(sw == 0 && first_done)) SP_TRY(residual_lv<T>(h, lv, true, s));
     SP_TRY(oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
                                 L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
-                                (long)L.bh * L.bw, 1.0, (T*)L.corr, s));
-    SP_TRY(oras_blend_launch<T>((T*)L.u, (const T*)L.corr, nullptr, L.ys, L.xs, L.row_k0,
-                                L.row_n, L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw,
-                                L.H, L.W, h->C, h->cfg.overlap, s));
+                                (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
+                                h->ntile, h->d_active, h->cfg.block - h->cfg.overlap));
+    SP_TRY(oras_blend_launch<T>((T*)L.u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,
+                                L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
+                                s, h->ntile, h->d_active));
   }
   return 0;
 }
@@ -212,11 +236,12 @@ static int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
   Level& F = h->lv[lv];
   Level& G = h->lv[lv + 1];
   SP_TRY(residual_restrict<T>((const T*)F.u, (const T*)F.b, F.mask, (T*)G.r, h->C, F.H,
-                              F.W, 1.0, s));
-  SP_TRY(sym_rhs<T>((const T*)G.r, G.mask, (T*)G.b, (T*)G.u, h->C, G.H, G.W, 1.0, s));
+                              F.W, 1.0, s, h->ntile, h->d_active));
+  SP_TRY(sym_rhs<T>((const T*)G.r, G.mask, (T*)G.b, (T*)G.u, h->C, G.H, G.W, 1.0, s,
+                    h->ntile, h->d_active));
   SP_TRY(vcycle_lv<T>(h, lv + 1, false, s));
-  SP_TRY(prolong_add_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H,
-                                G.W, F.H, F.W, s));
+  SP_TRY(prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H, G.W,
+                            F.H, F.W, 1, s, h->ntile, h->d_active));
   SP_TRY(smooth_lv<T>(h, lv, cfg.post, false, s));
   return 0;
 }
@@ -246,31 +271,44 @@ static int run_vcycle(Hier* h, cudaStream_t s) {
 template <typename T>
 static int cascade_t(Hier* h, cudaStream_t s) {
   int last = (int)h->lv.size() - 1;
+  const int nt = h->ntile;
   Level& Lc = h->lv[last];
   // solver.py:302-317: coarsest: u = 0, b = level rhs, enforce, smooth 1
-  SP_TRY(masked_sym_rhs<T>((const T*)Lc.values, Lc.mask, (T*)Lc.b, h->C, Lc.H, Lc.W, s));
-  SP_TRY(enforce<T>((T*)Lc.u, (const T*)Lc.b, Lc.mask, h->C, Lc.H, Lc.W, 1, s));
+  SP_TRY(masked_sym_rhs<T>((const T*)Lc.values, Lc.mask, (T*)Lc.b, h->C, Lc.H, Lc.W, s, nt,
+                           h->d_active));
+  SP_TRY(enforce<T>((T*)Lc.u, (const T*)Lc.b, Lc.mask, h->C, Lc.H, Lc.W, 1, s, nt,
+                    h->d_active));
   SP_TRY(smooth_lv<T>(h, last, 1, false, s));
   for (int lv = last - 1; lv >= 0; --lv) {
     Level& F = h->lv[lv];
     Level& G = h->lv[lv + 1];
-    SP_TRY(masked_sym_rhs<T>((const T*)F.values, F.mask, (T*)F.b, h->C, F.H, F.W, s));
-    SP_TRY(prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H,
-                              G.W, F.H, F.W, s));
+    SP_TRY(masked_sym_rhs<T>((const T*)F.values, F.mask, (T*)F.b, h->C, F.H, F.W, s, nt,
+                             h->d_active));
+    SP_TRY(prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H, G.W,
+                              F.H, F.W, 0, s, nt, h->d_active));
     SP_TRY(smooth_lv<T>(h, lv, 1, false, s));
   }
   return 0;
 }
 
+static int upload_active(Hier* h, cudaStream_t s) {
+  SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * h->ntile,
+                          cudaMemcpyHostToDevice, s));
+  return 0;
+}
+
 template <typename T>
 static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, int cycles,
-                   int max_cycles, cudaStream_t s, SolveReport* rep) {
+                   int max_cycles, cudaStream_t s, const int* active_in, int* iters,
+                   int* conv, SolveReport* rep) {
   Level& L0 = h->lv[0];
-  const int C = h->C;
-  size_t n = (size_t)C * L0.H * L0.W;
-  rep->iterations = 0;
-  rep->nres = 0;
-  rep->converged = 0;
+  const int C = h->C, nt = h->ntile;
+  size_t per = (size_t)C * L0.H * L0.W, n = per * nt;
+  if (rep) { rep->iterations = 0; rep->nres = 0; rep->converged = 0; }
+  // the pinned flag buffer may still feed an earlier async upload
+  SP_CUDA(cudaStreamSynchronize(s));
+  for (int t = 0; t < nt; ++t) h->h_active[t] = active_in ? (active_in[t] != 0) : 1;
+  SP_TRY(upload_active(h, s));
   if (init_mode == 1) {
     SP_CUDA(cudaMemcpyAsync(L0.u, u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
   } else if (init_mode == 2 && h->lv.size() > 1) {
@@ -283,61 +321,79 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
     SP_CUDA(cudaMemsetAsync(L0.u, 0, sizeof(T) * n, s));
   }
   SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
-  SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s));
+  SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s, nt, h->d_active));
+  std::vector<int> done(nt, 0), cv(nt, 0);
   if (tol < 0) {
     // solver.py:345-350: exactly `cycles` V-cycles, converged = True
     for (int c = 0; c < cycles; ++c) {
       SP_TRY(residual_lv<T>(h, 0, true, s));
       SP_TRY(run_vcycle<T>(h, s));
     }
-    rep->iterations = cycles;
-    rep->converged = 1;
-  } else {
-    // solver.py:351-369
-    double bnorm = 0.0;
-    {
-      // solver.py:355-358: ||b~|| over all channels, double
-      SP_TRY(dot_self<T>((const T*)L0.b, n, L0.partial, L0.counter, L0.norms, s));
-      SP_CUDA(cudaMemcpyAsync(h->h_norms, L0.norms, sizeof(double), cudaMemcpyDeviceToHost, s));
-      SP_CUDA(cudaStreamSynchronize(s));
-      bnorm = std::sqrt(h->h_norms[0]);
+    for (int t = 0; t < nt; ++t) {
+      done[t] = h->h_active[t] ? cycles : 0;
+      cv[t] = 1;
     }
-    double scale = bnorm > 0 ? bnorm : 1.0;
-    int cap = max_cycles;
-    int done = 0;
+    if (rep) { rep->iterations = cycles; rep->converged = 1; }
+  } else {
+    // solver.py:351-369, per tile: ||b~|| over all channels of the tile
+    double* part = (double*)h->d_scratch;
+    double* bn = part + 1024 * (size_t)nt;
+    unsigned* counter = (unsigned*)(bn + nt);
+    SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
+    SP_TRY(chan_reduce<T>(0, (const T*)L0.b, nullptr, nullptr, per, nt, part, counter, bn, s));
+    std::vector<double> scale(nt);
+    SP_CUDA(cudaMemcpyAsync(h->h_norms, bn, sizeof(double) * nt, cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    for (int t = 0; t < nt; ++t) {
+      double bnorm = std::sqrt(h->h_norms[t]);
+      scale[t] = bnorm > 0 ? bnorm : 1.0;
+    }
     while (true) {
       SP_TRY(residual_lv<T>(h, 0, true, s));
-      SP_CUDA(cudaMemcpyAsync(h->h_norms, L0.norms, sizeof(double) * C,
+      SP_CUDA(cudaMemcpyAsync(h->h_norms, L0.norms, sizeof(double) * C * nt,
                               cudaMemcpyDeviceToHost, s));
       SP_CUDA(cudaStreamSynchronize(s));
-      double tot = 0.0;
-      for (int c = 0; c < C; ++c) tot += h->h_norms[c];
-      double rel = std::sqrt(tot) / scale;
-      if (rep->nres < SP_MAX_RES) rep->residuals[rep->nres++] = rel;
-      if (rel <= tol) { rep->converged = 1; break; }
-      if (done >= cap) break;
+      int live = 0;
+      for (int t = 0; t < nt; ++t) {
+        if (!h->h_active[t]) continue;
+        double tot = 0.0;
+        for (int c = 0; c < C; ++c) tot += h->h_norms[(size_t)t * C + c];
+        double rel = std::sqrt(tot) / scale[t];
+        if (t == 0 && rep && rep->nres < SP_MAX_RES) rep->residuals[rep->nres++] = rel;
+        if (rel <= tol) { cv[t] = 1; h->h_active[t] = 0; continue; }
+        if (done[t] >= max_cycles) { h->h_active[t] = 0; continue; }
+        ++live;
+      }
+      if (!live) break;
+      SP_TRY(upload_active(h, s));
       SP_TRY(run_vcycle<T>(h, s));
-      ++done;
+      for (int t = 0; t < nt; ++t) done[t] += h->h_active[t];
     }
-    rep->iterations = done;
+    if (rep) { rep->iterations = done[0]; rep->converged = cv[0]; }
   }
+  if (iters) for (int t = 0; t < nt; ++t) iters[t] = done[t];
+  if (conv) for (int t = 0; t < nt; ++t) conv[t] = cv[t];
   SP_CUDA(cudaMemcpyAsync(u_io, L0.u, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
   return 0;
 }
 
 int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
-               int cycles, int max_cycles, cudaStream_t s, SolveReport* rep) {
+               int cycles, int max_cycles, cudaStream_t s, const int* active_in, int* iters,
+               int* conv, SolveReport* rep) {
   if (h->dtype == SP_F64)
     return solve_t<double>(h, (const double*)bsym, (double*)u_io, init_mode, tol, cycles,
-                           max_cycles, s, rep);
+                           max_cycles, s, active_in, iters, conv, rep);
   return solve_t<float>(h, (const float*)bsym, (float*)u_io, init_mode, tol, cycles,
-                        max_cycles, s, rep);
+                        max_cycles, s, active_in, iters, conv, rep);
 }
 
 template <typename T>
 static int vcycle_once_t(Hier* h, const T* bsym, T* u_io, cudaStream_t s) {
   Level& L0 = h->lv[0];
-  size_t n = (size_t)h->C * L0.H * L0.W;
+  size_t n = (size_t)h->C * L0.H * L0.W * h->ntile;
+  SP_CUDA(cudaStreamSynchronize(s));
+  for (int t = 0; t < h->ntile; ++t) h->h_active[t] = 1;
+  SP_TRY(upload_active(h, s));
   SP_CUDA(cudaMemcpyAsync(L0.u, u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
   SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
   SP_TRY(residual_lv<T>(h, 0, true, s));

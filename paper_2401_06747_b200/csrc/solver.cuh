@@ -18,7 +18,7 @@ struct Level {
   int H, W, bh, bw, nby, nbx;
   double tau_scale;
   uint8_t* mask;
-  void *values, *u, *b, *r, *corr;
+  void *values, *u, *b, *r, *corr, *weights;
   double* partial;
   size_t npart;
   unsigned* counter;
@@ -27,7 +27,7 @@ struct Level {
 };
 
 struct Hier {
-  int dtype = 0, C = 1;
+  int dtype = 0, C = 1, ntile = 1;
   HierCfg cfg;
   double gamma = 0.0;
   bool has_values = false;
@@ -35,7 +35,10 @@ struct Hier {
   std::vector<Level> lv;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
-  double* h_norms = nullptr;
+  double* h_norms = nullptr;   // pinned [ntile][C]
+  int* h_active = nullptr;     // pinned [ntile]
+  int* d_active = nullptr;     // [ntile] read by every V-cycle kernel
+  void* d_scratch = nullptr;   // reduction partials
   ~Hier();
 };
 
@@ -49,10 +52,11 @@ struct SolveReport {
 };
 
 int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
-                int with_values);
+                int with_values, int ntile = 1);
 int hier_set_mask(Hier* h, const uint8_t* mask, const void* values, cudaStream_t s);
 int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
-               int cycles, int max_cycles, cudaStream_t s, SolveReport* rep);
+               int cycles, int max_cycles, cudaStream_t s, const int* active_in, int* iters,
+               int* conv, SolveReport* rep);
 int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s);
 
 // vec.cu: deterministic reductions (fixed CTA count per size)

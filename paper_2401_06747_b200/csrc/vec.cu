@@ -44,9 +44,10 @@ __global__ void __launch_bounds__(NT) k_reduce(const T* __restrict__ x,
     double s = cta_sum<NT>(acc, (c & 1) ? s1 : s0);
     if (threadIdx.x == 0) partial[(size_t)blockIdx.x * C + c] = s;
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) am_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    am_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
   if (!am_last) return;
   __threadfence();
