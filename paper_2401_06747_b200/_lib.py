@@ -61,6 +61,23 @@ _SIGS = {
     "sp_geo_fill_highest_error": [P, P, P, c_long, P],
     "sp_geo_load": [P, P, P, P, c_long, P],
     "sp_stats": [c_int, P],
+    "sp_cell_index": [P, c_int, c_int, c_long, P, P, P, P],
+    "sp_vi_weights": [P, P, P, P, P, P, c_int, c_int, c_long, c_int, P, P],
+    "sp_cell_sum": [P, P, P, P, c_long, P, P],
+    "sp_vi_step": [c_int, P, P, P, P, P, P, P, P, c_long, c_int, c_int, c_int, c_double, P, P],
+    "sp_plane_dot": [c_int, P, P, c_long, c_long, c_int, P, P, P],
+    "sp_plane_axpy": [c_int, P, P, P, P, c_double, c_long, c_long, c_int, P, P],
+    "sp_gather_tiles": [c_int, P, P, P, c_int, c_int, c_int, c_int, c_int, c_int, P, P],
+    "sp_gather_mask_tiles": [P, P, P, c_int, c_int, c_int, c_int, c_int, P, P],
+    "sp_ras_scatter": [c_int, P, P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_int,
+                       c_int, P],
+    "sp_where_mask": [c_int, P, P, P, c_int, c_int, c_int, P],
+    "sp_masked_sym_rhs_tiles": [c_int, P, P, P, c_int, c_int, c_int, c_int, P, P],
+    "sp_ct_apply_tiles": [c_int, P, P, P, c_int, c_int, c_int, c_int, P, P],
+    "sp_density_map": [P, c_int, c_int, c_int, c_double, P, c_int, P, P, P],
+    "sp_init_mask_random": [P, c_int, c_int, c_int, c_long, c_double, P, c_int, P, P, P, P],
+    "sp_pcg64_doubles": [P, ctypes.c_longlong, ctypes.c_longlong, P, P],
+    "sp_pairwise_sum": [P, ctypes.c_longlong, P, P],
     "sp_oras_variant": [c_int],
     "sp_geo_export": [P, P, P, P, P, P, P, P, c_long, P],
 }

@@ -453,3 +453,39 @@ int oras_variant(int v);
 // select the float ORAS kernel for blocks <= 32x32: 1 = warp per job
 // (default), 0 = CTA per job; v < 0 only queries.  Returns the current value.
 extern "C" int sp_oras_variant(int v) { return sp::oras_variant(v); }
+
+// ---- dithered initial mask (spatial.py:107-148) -------------------------------
+namespace sp {
+int density_map(const double* f, int C, int H, int W, double density, const double* gauss_h,
+                int radius, double* dens, double* total_out, cudaStream_t s);
+int init_mask_random(const double* f, int C, int H, int W, long target, double density,
+                     const double* gauss_h, int radius, const uint64_t* pcg_h, uint8_t* mask,
+                     int* degenerate, cudaStream_t s);
+int pcg_doubles(const uint64_t* pcg_h, long long start, long long count, double* out,
+                cudaStream_t s);
+int pairwise_sum(const double* a, long long n, double* out, cudaStream_t s);
+
+}
+
+extern "C" {
+int sp_density_map(const double* f, int C, int H, int W, double density, const double* gauss_h,
+                   int radius, double* dens, double* total_h, void* s) {
+  return sp::density_map(f, C, H, W, density, gauss_h, radius, dens, total_h, STREAM(s));
+}
+
+int sp_init_mask_random(const double* f, int C, int H, int W, long target, double density,
+                        const double* gauss_h, int radius, const uint64_t* pcg_h, uint8_t* mask,
+                        int* degenerate_h, void* s) {
+  return sp::init_mask_random(f, C, H, W, target, density, gauss_h, radius, pcg_h, mask,
+                              degenerate_h, STREAM(s));
+}
+
+int sp_pcg64_doubles(const uint64_t* pcg_h, long long start, long long count, double* out,
+                     void* s) {
+  return sp::pcg_doubles(pcg_h, start, count, out, STREAM(s));
+}
+
+int sp_pairwise_sum(const double* a, long long n, double* out_h, void* s) {
+  return sp::pairwise_sum(a, n, out_h, STREAM(s));
+}
+}  // extern "C"

@@ -324,11 +324,20 @@ __global__ void k_not_mask(const uint8_t* __restrict__ mask, size_t n,
   if (i < n) flags[i] = !mask[i];
 }
 
-// descending non-negative doubles: complement of the IEEE bit pattern
+// sort keys of non-negative doubles: the IEEE bit pattern orders them
+// ascending, its complement descending
 __global__ void k_desc_keys(const int* __restrict__ idx, long n, const double* __restrict__ v,
-                            unsigned long long* __restrict__ keys) {
+                            unsigned long long* __restrict__ keys, int descending) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = ~(unsigned long long)__double_as_longlong(v[idx[i]]);
+  if (i >= n) return;
+  unsigned long long b = (unsigned long long)__double_as_longlong(v[idx[i]]);
+  keys[i] = descending ? ~b : b;
+}
+
+__global__ void k_set_mask_val(const int* __restrict__ idx, long n, uint8_t* __restrict__ mask,
+                               uint8_t val) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) mask[idx[i]] = val;
 }
 
 __global__ void k_apply_picks(const int* __restrict__ order, long npick,
@@ -642,7 +651,8 @@ int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s) {
 // complemented key == np.lexsort((index, -value)).
 template <typename Apply>
 static int top_by_desc(const uint8_t* flags, const double* vals, long n, long want,
-                       int* nsel, long* taken, cudaStream_t s, Apply apply) {
+                       int* nsel, long* taken, cudaStream_t s, Apply apply,
+                       bool descending = true) {
   *taken = 0;
   if (want <= 0 || n <= 0) return 0;
   cub::CountingInputIterator<int> it(0);
@@ -666,7 +676,7 @@ static int top_by_desc(const uint8_t* flags, const double* vals, long n, long wa
   SP_CUDA(cudaStreamSynchronize(s));
   long nv = nv_h;
   if (nv == 0) return 0;
-  k_desc_keys<<<cdiv(nv, 256), 256, 0, s>>>(v_in, nv, vals, k_in);
+  k_desc_keys<<<cdiv(nv, 256), 256, 0, s>>>(v_in, nv, vals, k_in, descending ? 1 : 0);
   SP_CHECK_LAUNCH();
   SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, k_in, k_out, v_in, v_out, (int)nv,
                                           0, 64, s));
@@ -704,6 +714,30 @@ int fill_highest_error(Geo* g, const double* err, uint8_t* mask, long want, cuda
                        SP_CHECK_LAUNCH();
                        return 0;
                      });
+}
+
+// spatial.py:90-104 (_exact_count): among the flagged pixels (flags == NULL:
+// the pixels with mask_set == 0) take the `want` first of the order
+// (value descending or ascending, index ascending) and set them to
+// `set_value` in mask_set
+int top_select(const uint8_t* flags, const double* vals, long n, long want, bool descending,
+               int* nsel, cudaStream_t s, uint8_t* mask_set, uint8_t set_value) {
+  Scratch fl(s);
+  if (!flags) {
+    SP_TRY(fl.alloc((size_t)n));
+    k_not_mask<<<cdiv(n, 256), 256, 0, s>>>(mask_set, (size_t)n, (uint8_t*)fl.p);
+    SP_CHECK_LAUNCH();
+    flags = (const uint8_t*)fl.p;
+  }
+  long taken = 0;
+  return top_by_desc(flags, vals, n, want, nsel, &taken, s,
+                     [&](const int* order, long k) {
+                       k_set_mask_val<<<cdiv(k, 256), 256, 0, s>>>(order, k, mask_set,
+                                                                   set_value);
+                       SP_CHECK_LAUNCH();
+                       return 0;
+                     },
+                     descending);
 }
 
 }  // namespace sp
