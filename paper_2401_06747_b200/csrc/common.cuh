@@ -82,12 +82,18 @@ __host__ __device__ __forceinline__ int num_starts(int dim, int size, int stride
   return (dim - size + stride - 1) / stride + 1;
 }
 
+// keep freed stream-ordered memory in the device pool (the default release
+// threshold of 0 hands it back to the driver at every synchronization, which
+// makes every later scratch allocation pay a fresh mapping)
+void retain_pool_memory();
+
 // RAII stream-ordered scratch (cudaMallocAsync / cudaFreeAsync)
 struct Scratch {
   void* p = nullptr;
   cudaStream_t s;
   explicit Scratch(cudaStream_t st) : s(st) {}
   int alloc(size_t bytes) {
+    retain_pool_memory();
     if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) {
       set_error("cudaMallocAsync(%zu) failed", bytes);
       return -1;
