@@ -61,6 +61,7 @@ _SIGS = {
     "sp_geo_fill_highest_error": [P, P, P, c_long, P],
     "sp_geo_load": [P, P, P, P, c_long, P],
     "sp_stats": [c_int, P],
+    "sp_hier_bench": [P, c_int, c_int, P, P, P],
     "sp_cell_index": [P, c_int, c_int, c_long, P, P, P, P],
     "sp_vi_weights": [P, P, P, P, P, P, c_int, c_int, c_long, c_int, P, P],
     "sp_cell_sum": [P, P, P, P, c_long, P, P],
@@ -103,6 +104,8 @@ def load(require_cuda: bool = True):
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = c_int
+        lib.sp_launch_count.restype = ctypes.c_longlong
+        lib.sp_launch_count.argtypes = [c_int]
         lib.sp_last_error.restype = ctypes.c_char_p
         lib.sp_last_error.argtypes = []
         _lib = lib
@@ -113,7 +116,7 @@ def load(require_cuda: bool = True):
 
 
 def exported_symbols():
-    return list(_SIGS) + ["sp_last_error"]
+    return list(_SIGS) + ["sp_last_error", "sp_launch_count"]
 
 
 def call(name, *args):

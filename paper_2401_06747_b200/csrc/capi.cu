@@ -501,3 +501,27 @@ int sp_pairwise_sum(const double* a, long long n, double* out_h, void* s) {
   return sp::pairwise_sum(a, n, out_h, STREAM(s));
 }
 }  // extern "C"
+
+// ---- measurement hooks (bench.py) ---------------------------------------------
+#include <atomic>
+namespace sp {
+static std::atomic<long long> g_launches{0};
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int hier_bench(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes);
+}  // namespace sp
+
+extern "C" {
+// kernels launched by the library since the last reset (reset != 0 zeroes it)
+long long sp_launch_count(int reset) {
+  long long v = sp::g_launches.load();
+  if (reset) sp::g_launches.store(0);
+  return v;
+}
+
+// mean time (ms, CUDA events on `stream`) of `reps` launches of a finest-level
+// kernel of the hierarchy (0 residual, 1 ORAS local CG, 2 ORAS blend, 3
+// residual+restriction) and its algorithmic bytes per launch
+int sp_hier_bench(void* h, int which, int reps, double* ms_h, double* bytes_h, void* s) {
+  return sp::hier_bench((sp::Hier*)h, which, reps, (cudaStream_t)s, ms_h, bytes_h);
+}
+}  // extern "C"

@@ -26,8 +26,13 @@ const char* last_error();
     }                                                                          \
   } while (0)
 
+// kernels launched by this library (direct launches; graph replays add their
+// node count) -- reported by bench.py as gpu_launches
+void count_launches(long long n);
+
 #define SP_CHECK_LAUNCH()                                                      \
   do {                                                                         \
+    ::sp::count_launches(1);                                                   \
     cudaError_t _e = cudaGetLastError();                                       \
     if (_e != cudaSuccess) {                                                   \
       ::sp::set_error("%s:%d launch: %s", __FILE__, __LINE__,                  \

@@ -260,11 +260,15 @@ static int run_vcycle(Hier* h, cudaStream_t s) {
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) { if (e == cudaSuccess) cudaGraphDestroy(g); return rc; }
     SP_CUDA(e);
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    h->graph_nodes = (long long)nn;
     cudaError_t ie = cudaGraphInstantiate(&h->graph_exec, g, 0);
     cudaGraphDestroy(g);
     SP_CUDA(ie);
   }
   SP_CUDA(cudaGraphLaunch(h->graph_exec, s));
+  count_launches(h->graph_nodes);
   return 0;
 }
 
@@ -405,6 +409,81 @@ static int vcycle_once_t(Hier* h, const T* bsym, T* u_io, cudaStream_t s) {
 int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s) {
   if (h->dtype == SP_F64) return vcycle_once_t<double>(h, (const double*)bsym, (double*)u_io, s);
   return vcycle_once_t<float>(h, (const float*)bsym, (float*)u_io, s);
+}
+
+}  // namespace sp
+
+namespace sp {
+
+// ---- per-kernel timing on the finest level (bench.py roofline) ---------------
+// which: 0 = residual + norms sweep, 1 = ORAS local CG, 2 = ORAS blend,
+// 3 = fused residual + restriction.  Runs `reps` launches on the current
+// level-0 state (after a solve) between CUDA events on `s`; returns the mean
+// milliseconds per launch and the algorithmic bytes per launch.
+template <typename T>
+static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes) {
+  Level& L = h->lv[0];
+  const size_t es = sizeof(T), C = h->C, plane = (size_t)L.H * L.W, nt = h->ntile;
+  const size_t vec = C * plane * nt;
+  const size_t nb = (size_t)L.nby * L.nbx, npx = (size_t)L.bh * L.bw;
+  // algorithmic bytes (SURVEY.md section 8d conventions, mask shared by channels)
+  switch (which) {
+    case 0: *bytes = (double)(3 * es * vec + plane * nt); break;          // u, b, r + mask
+    case 1: *bytes = (double)(es * C * nb * npx * nt * 3 + nb * npx * nt); break;  // r, w, corr + mask
+    case 2: *bytes = (double)(es * C * nb * npx * nt + 2 * es * vec); break;       // corr + u rw
+    case 3: *bytes = (double)(2 * es * vec + plane * nt + es * vec / 4); break;    // u, b, mask, rc
+    default: set_error("unknown kernel id %d", which); return -2;
+  }
+  for (int t = 0; t < nt; ++t) h->h_active[t] = 1;
+  SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * nt, cudaMemcpyHostToDevice, s));
+  Level* G = h->lv.size() > 1 ? &h->lv[1] : nullptr;
+  auto launch = [&]() -> int {
+    switch (which) {
+      case 0:
+        return residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
+                           L.norms, h->C, L.H, L.W, 1.0, s, h->ntile, h->d_active);
+      case 1:
+        return oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
+                                    L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
+                                    (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
+                                    h->ntile, h->d_active, h->cfg.block - h->cfg.overlap);
+      case 2: {
+        // blend into a scratch copy so the solver state is not disturbed
+        return oras_blend_launch<T>((T*)L.r, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,
+                                    L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
+                                    s, h->ntile, h->d_active);
+      }
+      default:
+        if (!G) { set_error("single-level hierarchy"); return -2; }
+        return residual_restrict<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)G->r, h->C, L.H,
+                                    L.W, 1.0, s, h->ntile, h->d_active);
+    }
+  };
+  // the ORAS local kernel needs current r/norms
+  SP_TRY((residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
+                      L.norms, h->C, L.H, L.W, 1.0, s, h->ntile, h->d_active)));
+  SP_TRY(launch());  // warm-up
+  cudaEvent_t e0, e1;
+  SP_CUDA(cudaEventCreate(&e0));
+  SP_CUDA(cudaEventCreate(&e1));
+  SP_CUDA(cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i) SP_TRY(launch());
+  SP_CUDA(cudaEventRecord(e1, s));
+  SP_CUDA(cudaEventSynchronize(e1));
+  float t = 0.f;
+  SP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = (double)t / reps;
+  // leave r / norms consistent with u for the next solve
+  SP_TRY((residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
+                      L.norms, h->C, L.H, L.W, 1.0, s, h->ntile, h->d_active)));
+  return 0;
+}
+
+int hier_bench(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes) {
+  if (h->dtype == SP_F64) return bench_t<double>(h, which, reps, s, ms, bytes);
+  return bench_t<float>(h, which, reps, s, ms, bytes);
 }
 
 }  // namespace sp

@@ -35,6 +35,7 @@ struct Hier {
   std::vector<Level> lv;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
+  long long graph_nodes = 0;
   double* h_norms = nullptr;   // pinned [ntile][C]
   int* h_active = nullptr;     // pinned [ntile]
   int* d_active = nullptr;     // [ntile] read by every V-cycle kernel
