@@ -179,6 +179,77 @@ int sp_geo_export(void* geo, int32_t* labels, int32_t* sy, int32_t* sx, int32_t*
                   double* sums, int64_t* amax, double* amax_val, long nbuckets,
                   void* stream);
 
+/* ================ B2: dithered initial mask (spatial.py:107-148) ========== */
+/* dens (H,W) double = clip(sum_c |L(gauss_sigma f_c)| * density*n/total, 0, 1);
+ * gauss_h: 2r+1 HOST weights exactly as scipy's _gaussian_kernel1d; total_h
+ * (HOST) receives the numpy pairwise total (0 = constant image).  Syncs. */
+int sp_density_map(const double* f, int C, int H, int W, double density,
+                   const double* gauss_h, int radius, double* dens, double* total_h,
+                   void* stream);
+/* analytic_mask(dither="random") + _exact_count; pcg_h = HOST {state_lo,
+ * state_hi, inc_lo, inc_hi} of numpy default_rng(seed)'s PCG64.  Sets
+ * *degenerate_h = 1 (mask untouched) when the Laplacian vanishes. */
+int sp_init_mask_random(const double* f, int C, int H, int W, long target, double density,
+                        const double* gauss_h, int radius, const uint64_t* pcg_h,
+                        uint8_t* mask, int* degenerate_h, void* stream);
+/* doubles start..start+count-1 of numpy Generator(PCG64).random (tests) */
+int sp_pcg64_doubles(const uint64_t* pcg_h, long long start, long long count, double* out,
+                     void* stream);
+/* numpy pairwise sum of a device double array (result on the HOST) */
+int sp_pairwise_sum(const double* a, long long n, double* out_h, void* stream);
+
+/* ======================= B2: tonal optimizers (tonal.py) ================== */
+/* pixels stably sorted by label: perm (H*W), per-cell [start, end) */
+int sp_cell_index(const int32_t* labels, int H, int W, long m, int32_t* perm, int32_t* start,
+                  int32_t* end, void* stream);
+/* voronoi_weights (geometry.py:247-264): scheme 0 constant, 1 inverse-log */
+int sp_vi_weights(const int32_t* labels, const int32_t* sy, const int32_t* sx,
+                  const int32_t* perm, const int32_t* start, const int32_t* end, int H, int W,
+                  long m, int scheme, double* w, void* stream);
+/* per-cell sequential sums in pixel order (np.bincount) */
+int sp_cell_sum(const int32_t* perm, const int32_t* start, const int32_t* end, const double* v,
+                long m, double* out, void* stream);
+/* g[seed_t] += T(tau * sum_cell w (f - u)) per channel (tonal.py:459-464) */
+int sp_vi_step(int dtype, const int32_t* perm, const int32_t* start, const int32_t* end,
+               const double* w, const void* f, const void* u, const int32_t* sy,
+               const int32_t* sx, long m, int C, int H, int W, double tau, void* g,
+               void* stream);
+/* out[plane] = sum x*y (y NULL: x*x), planes of len elements, double */
+int sp_plane_dot(int dtype, const void* x, const void* y, long len, long nplanes, int C,
+                 const int32_t* active, double* out, void* stream);
+/* yout = x + sign * T(coef[plane]) * z, per plane (CG vector updates) */
+int sp_plane_axpy(int dtype, void* yout, const void* x, const void* z, const double* coef,
+                  double sign, long len, long nplanes, int C, const int32_t* active,
+                  void* stream);
+int sp_gather_tiles(int dtype, const void* img, const int32_t* oy, const int32_t* ox, int ntile,
+                    int C, int H, int W, int bh, int bw, void* out, void* stream);
+int sp_gather_mask_tiles(const uint8_t* mask, const int32_t* oy, const int32_t* ox, int ntile,
+                         int H, int W, int bh, int bw, uint8_t* out, void* stream);
+/* g += sum over covering RAS blocks of T(1/cover) * v_b (tonal.py:375-380) */
+int sp_ras_scatter(int dtype, void* g, const void* v, const int32_t* tile_of,
+                   const int32_t* ys, const int32_t* xs, const int32_t* row_k0,
+                   const int32_t* row_n, const int32_t* col_k0, const int32_t* col_n, int nbx,
+                   int bh, int bw, int C, int H, int W, void* stream);
+int sp_where_mask(int dtype, const void* x, const uint8_t* mask, void* out, int C, int H, int W,
+                  void* stream);
+int sp_masked_sym_rhs_tiles(int dtype, const void* x, const uint8_t* mask, void* out, int C,
+                            int H, int W, int ntile, const int32_t* active, void* stream);
+int sp_ct_apply_tiles(int dtype, const void* w, const uint8_t* mask, void* out, int C, int H,
+                      int W, int ntile, const int32_t* active, void* stream);
+
+/* ======================= tracing / measurement =========================== */
+/* ORAS local-CG statistics {jobs, iterations, converged-on-entry, max it};
+ * enable 1 = reset+start, 0 = reset+stop, -1 = read only */
+int sp_stats(int enable, uint64_t* out_h);
+/* float ORAS kernel for blocks <= 32x32: 1 warp/job, 0 CTA/job; v < 0 query */
+int sp_oras_variant(int v);
+/* kernels launched by the library since the last reset */
+long long sp_launch_count(int reset);
+/* CUDA-event timing of a finest-level kernel (0 residual, 1 ORAS local CG,
+ * 2 blend, 3 residual+restrict): mean ms and algorithmic bytes per launch */
+int sp_hier_bench(void* hier, int which, int reps, double* ms_h, double* bytes_h,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -184,7 +184,7 @@ def jfa_dist2(labels, seeds):
     labels = _c(labels, np.int32)
     seeds = _c(seeds, np.int64)
     out = np.empty(labels.shape, np.int64)
-    lib().ora_jfa_dist2(_p(labels), _p(seeds), _p(out),
+    lib().ora_jfa_dist2(_p(labels), _p(seeds), ctypes.c_long(seeds.shape[0]), _p(out),
                         *map(ctypes.c_int, labels.shape))
     return out
 

@@ -341,12 +341,13 @@ void ora_jfa_run(const int32_t *labels, int32_t *out, const int64_t *seeds, long
   free(a); free(b); free(sy); free(sx);
 }
 
-void ora_jfa_dist2(const int32_t *labels, const int64_t *seeds, int64_t *out, int H,
+void ora_jfa_dist2(const int32_t *labels, const int64_t *seeds, long m, int64_t *out, int H,
                    int W) {
 #pragma omp parallel for schedule(static)
   for (int y = 0; y < H; ++y)
     for (int x = 0; x < W; ++x) {
       int32_t s = labels[IDX2(y, x)];
+      if (s < 0) s += (int32_t)m;  /* numba wraparound indexing (seeds[-1]) */
       int64_t dy = (int64_t)y - seeds[2 * (int64_t)s];
       int64_t dx = (int64_t)x - seeds[2 * (int64_t)s + 1];
       out[IDX2(y, x)] = dy * dy + dx * dx;

@@ -349,7 +349,7 @@ int sp_jfa_dist2(const int32_t* labels, const int64_t* seeds, long m, int64_t* o
   int* sy = (int*)scr.p;
   int* sx = sy + (m > 0 ? m : 1);
   SP_TRY(seeds_to_soa((const long long*)seeds, m, sy, sx, st));
-  return dist2(labels, sy, sx, (long long*)out, (unsigned long long*)dmax, H, W, st);
+  return dist2(labels, sy, sx, (long long*)out, (unsigned long long*)dmax, H, W, (int)m, st);
 }
 
 int sp_fs_dither(const double* dens, uint8_t* out, int H, int W, void* s) {

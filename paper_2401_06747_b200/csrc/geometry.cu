@@ -69,12 +69,13 @@ __global__ void k_jfa_pass(const int* __restrict__ cur, int* __restrict__ nxt,
 
 __global__ void k_dist2(const int* __restrict__ lab, const int* __restrict__ sy,
                         const int* __restrict__ sx, long long* __restrict__ out,
-                        unsigned long long* __restrict__ dmax, int H, int W) {
+                        unsigned long long* __restrict__ dmax, int H, int W, int m) {
   int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
   long long d = 0;
   bool live = x < W && y < H;
   if (live) {
     int s = lab[(size_t)y * W + x];
+    if (s < 0) s += m;  // unlabelled pixel: numba's wraparound seeds[-1]
     long long dy = (long long)y - sy[s], dx = (long long)x - sx[s];
     d = dy * dy + dx * dx;
     if (out) out[(size_t)y * W + x] = d;
@@ -386,9 +387,9 @@ int jfa_passes(int* a, int* b, const int* sy, const int* sx, const long long* st
 }
 
 int dist2(const int* lab, const int* sy, const int* sx, long long* out,
-          unsigned long long* dmax, int H, int W, cudaStream_t s) {
+          unsigned long long* dmax, int H, int W, int m, cudaStream_t s) {
   if (dmax) SP_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
-  k_dist2<<<grid2(W, H), dim3(BX, BY), 0, s>>>(lab, sy, sx, out, dmax, H, W);
+  k_dist2<<<grid2(W, H), dim3(BX, BY), 0, s>>>(lab, sy, sx, out, dmax, H, W, m);
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -580,7 +581,7 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
   SP_TRY(jfa_passes(g->lab_a, g->lab_b, g->sy, g->sx, steps.data(), (int)steps.size(), H, W,
                     &res, s));
   if (res != g->lab_a) std::swap(g->lab_a, g->lab_b);  // labels live in lab_a
-  SP_TRY(dist2(g->lab_a, g->sy, g->sx, nullptr, g->dmax, H, W, s));
+  SP_TRY(dist2(g->lab_a, g->sy, g->sx, nullptr, g->dmax, H, W, (int)g->m, s));
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   unsigned long long d2 = ((unsigned long long*)g->h_small)[0];

@@ -39,7 +39,7 @@ int fill_highest_error(Geo* g, const double* err, uint8_t* mask, long want, cuda
 int jfa_passes(int* a, int* b, const int* sy, const int* sx, const long long* steps,
                int nsteps, int H, int W, int** result, cudaStream_t s);
 int dist2(const int* lab, const int* sy, const int* sx, long long* out,
-          unsigned long long* dmax, int H, int W, cudaStream_t s);
+          unsigned long long* dmax, int H, int W, int m, cudaStream_t s);
 int seeds_to_soa(const long long* seeds, long m, int* sy, int* sx, cudaStream_t s);
 int fs_dither(const double* dens, uint8_t* out, int H, int W, cudaStream_t s);
 template <typename V>

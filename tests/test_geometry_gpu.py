@@ -1,0 +1,199 @@
+"""Densification geometry on the GPU: bit-exact against the reference
+fixtures and the oracle.  The north_star contract: Voronoi labels, dithered
+masks and triangulation indices bit-exact for the same error map and seed
+(checked in lockstep, feeding the reference's own per-iteration
+mask + error map)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+G = np.load(os.path.join(HERE, "golden", "reference_vectors.npz"))
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import paper_2401_06747_b200 as sp
+    return sp
+
+
+@pytest.mark.parametrize("hh,ww,cc,seed", [(64, 64, 3, 0), (96, 80, 1, 7), (128, 128, 3, 2)])
+def test_dithered_initial_mask_matches_reference(sp, hh, ww, cc, seed):
+    from paper_2401_06747_b200 import spatial
+    f = O.synth(hh, ww, cc, seed)
+    n = hh * ww
+    init, _ = spatial._schedule(int(0.05 * n), 20, 1.0, None)
+    m = sp.analytic_mask(sp.Image(f), init / n, dither="random", sigma=1.0, seed=seed,
+                         count=init)
+    assert np.array_equal(m.indicator, G[f"initmask_{hh}x{ww}x{cc}_s{seed}"])
+
+
+def test_dithered_masks_textured_and_fs(sp, textured64):
+    img = sp.Image(textured64)
+    assert np.array_equal(sp.analytic_mask(img, 0.07, dither="random", seed=5).indicator,
+                          G["initmask_textured64_d007_s5"])
+    assert np.array_equal(sp.analytic_mask(img, 0.05).indicator, G["aamask_textured64_d005"])
+
+
+@pytest.mark.parametrize("shape,seed", [((1, 512, 384), 3), ((3, 300, 301), 11)])
+def test_dithered_mask_vs_oracle_larger(sp, shape, seed):
+    f = O.synth(shape[1], shape[2], shape[0], seed)
+    n = shape[1] * shape[2]
+    init = max(1, int(0.05 * n) // 21)
+    got = sp.analytic_mask(sp.Image(f), init / n, dither="random", seed=seed,
+                           count=init).indicator
+    assert np.array_equal(got, O.analytic_mask(f, init / n, dither="random", seed=seed,
+                                               count=init))
+
+
+def test_constant_image_falls_back_to_uniform(sp):
+    m = sp.analytic_mask(sp.Image(np.full((1, 16, 16), 9.0)), 0.1, seed=3)
+    assert m.count == 25
+    assert np.array_equal(m.indicator, O.uniform_random_mask(16, 16, 25, 3))
+
+
+def test_pcg64_stream_and_pairwise_sum(sp):
+    import ctypes
+    from paper_2401_06747_b200 import _lib, spatial
+    st = spatial._pcg_state(42)
+    out = torch.empty(5000, dtype=torch.float64, device="cuda")
+    _lib.call("sp_pcg64_doubles", _lib.ptr(st), 1234, 5000, _lib.ptr(out), _lib.stream())
+    ref = np.random.default_rng(42).random(6234)[1234:]
+    assert np.array_equal(out.cpu().numpy(), ref)
+    for n in (7, 128, 129, 1000, 4321, 2160 * 3840):
+        a = np.abs(np.random.default_rng(n).standard_normal(n)) * 1e3
+        tot = ctypes.c_double()
+        _lib.call("sp_pairwise_sum", _lib.ptr(torch.from_numpy(a).cuda()), n,
+                  ctypes.byref(tot), _lib.stream())
+        assert tot.value == float(a.sum()), n
+
+
+_TRACE = {}
+
+
+def _oracle_trace():
+    """Per-iteration (mask, error map, labels, triangles, picks) of the
+    oracle densification -- bit-exact with the reference (the CPU test
+    test_oracle_golden.py pins iterations 0/4/9 against the fixtures)."""
+    if not _TRACE:
+        trace = []
+        O.delaunay_densify(O.synth(64, 64, 3, 0), 0.05, 10, seed=0, trace=trace)
+        _TRACE.update(enumerate(trace))
+    return _TRACE
+
+
+def test_lockstep_picks_match_oracle(sp):
+    """Every densification iteration: same error map in -> same picks out."""
+    from paper_2401_06747_b200.geometry import workspace
+    t = _oracle_trace()
+    ws = workspace(64, 64)
+    hint = None
+    for i in sorted(t):
+        mask_t = torch.from_numpy(t[i]["mask"].astype(np.uint8)).cuda()
+        ws.voronoi(mask_t, hint)
+        hint = ws.max_radius
+        assert np.array_equal(ws.labels_tensor().cpu().numpy(), t[i]["labels"])
+        nb = ws.delaunay()
+        assert np.array_equal(ws.triangles_tensor().cpu().numpy(), t[i]["tris"])
+        ws.accumulate(torch.from_numpy(t[i]["err"]).cuda())
+        sums, amax, _ = ws.buckets(nb)
+        assert np.array_equal(sums.cpu().numpy(), t[i]["sums"])
+        assert np.array_equal(amax.cpu().numpy(), t[i]["amax"])
+        if i in (0, 4, 9):  # the reference's own arrays
+            assert np.array_equal(ws.triangles_tensor().cpu().numpy(), G[f"dd_it{i}_tris"])
+            assert np.array_equal(sums.cpu().numpy(), G[f"dd_it{i}_sums"])
+        picked = ws.select(mask_t, nb, t[i]["want"])
+        assert picked == len(t[i]["picked"])
+        expect = t[i]["mask"].copy().ravel()
+        expect[t[i]["picked"]] = 1
+        assert np.array_equal(mask_t.cpu().numpy().ravel(), expect)
+
+
+def test_jfa_against_oracle_with_hints(sp):
+    rng = np.random.default_rng(11)
+    for (h, w, d) in ((300, 257, 0.01), (128, 128, 0.002), (1, 40, 0.1), (64, 64, 0.3)):
+        m = (rng.random((h, w)) < d).astype(np.uint8)
+        m.ravel()[rng.integers(0, h * w)] = 1
+        for hint in (None, 3.0, 40.0):
+            lab = sp.jump_flood_voronoi(sp.Mask(m), hint)
+            lo, seeds, rad = O.jump_flood_voronoi(m, hint)
+            assert np.array_equal(lab.labels, lo) and lab.max_radius == rad
+            if (lo < 0).any():
+                # a too-small hint leaves pixels unlabelled (-1); the densify
+                # loop never triangulates such a map (its hint is the
+                # previous, larger radius), so only the labels are pinned
+                continue
+            mesh = sp.delaunay_from_voronoi(lab)
+            to, eo = O.delaunay_from_voronoi(lo, seeds.shape[0])
+            assert np.array_equal(mesh.triangles, to)
+            assert np.array_equal(mesh.edges, eo)
+
+
+def test_reference_geometry_kats(sp):
+    """test_geometry.py:24-103 known answers."""
+    def mask_from(h, w, pts):
+        m = np.zeros((h, w), np.uint8)
+        for y, x in pts:
+            m[y, x] = 1
+        return sp.Mask(m)
+    lab = sp.jump_flood_voronoi(mask_from(1, 8, [(0, 0), (0, 7)]))
+    assert lab.labels[0].tolist() == [0, 0, 0, 0, 1, 1, 1, 1]
+    mesh = sp.delaunay_from_voronoi(sp.jump_flood_voronoi(
+        mask_from(16, 16, [(2, 2), (3, 13), (12, 6)])))
+    assert mesh.triangles.tolist() == [[0, 1, 2]] and not mesh.degenerate
+    mesh = sp.delaunay_from_voronoi(sp.jump_flood_voronoi(
+        mask_from(8, 8, [(1, 1), (1, 6), (6, 1), (6, 6)])))
+    assert mesh.triangles.tolist() == [[0, 1, 3], [0, 2, 3]]
+    mesh = sp.delaunay_from_voronoi(sp.jump_flood_voronoi(mask_from(8, 8, [(1, 1), (6, 6)])))
+    assert mesh.degenerate and mesh.edges.tolist() == [[0, 1]]
+    with pytest.raises(ValueError):
+        sp.jump_flood_voronoi(sp.Mask(np.zeros((4, 4))))
+
+
+def test_accumulate_errors_partition_and_kat(sp):
+    """test_geometry.py:169-184: sums partition the error; unit-error argmax."""
+    rng = np.random.default_rng(2)
+    m = (rng.random((48, 48)) < 0.05).astype(np.uint8)
+    lab = sp.jump_flood_voronoi(sp.Mask(m))
+    mesh = sp.delaunay_from_voronoi(lab)
+    err = rng.uniform(0, 1, (48, 48))
+    ce = sp.accumulate_errors(mesh, err, lab)
+    lo, seeds, _ = O.jump_flood_voronoi(m)
+    so, ao, vo, _ = O.accumulate_errors(mesh.triangles, err, lo, seeds)
+    assert np.array_equal(ce.sums, so) and np.array_equal(ce.argmax_flat, ao)
+    assert abs(ce.total - err.sum()) <= 1e-9 * err.sum()
+    s2, a2, _ = sp.voronoi_cell_errors(lab, err)
+    s3, a3, _ = O.voronoi_cell_errors(lo, seeds.shape[0], err)
+    assert np.array_equal(s2, s3) and np.array_equal(a2, a3)
+
+
+def test_voronoi_weights_and_cell_average(sp):
+    rng = np.random.default_rng(4)
+    m = (rng.random((40, 56)) < 0.06).astype(np.uint8)
+    lab = sp.jump_flood_voronoi(sp.Mask(m))
+    lo, seeds, _ = O.jump_flood_voronoi(m)
+    for scheme in ("inverse-log", "constant"):
+        w = sp.voronoi_weights(lab, scheme)
+        wo = O.voronoi_weights(lo, seeds, scheme)
+        assert np.allclose(w, wo, rtol=1e-15, atol=0)
+    plane = rng.standard_normal((40, 56))
+    a = sp.geometry.cell_weighted_average(lab, wo, plane)
+    assert np.array_equal(a, O.cell_weighted_average(lo, seeds.shape[0], wo, plane))
+
+
+def test_densify_64_matches_reference_end_to_end(sp):
+    """At 64x64 RGB the GPU densification reproduces the reference mask."""
+    f = O.synth(64, 64, 3, 0)
+    mask, u, hist = sp.delaunay_densify(sp.Image(f), sp.DensificationConfig(
+        density=0.05, iterations=10, seed=0))
+    assert np.array_equal(mask.indicator, G["dd_final_mask"])
+    S = json.load(open(os.path.join(HERE, "golden", "reference_scalars.json")))
+    assert np.allclose([h[2] for h in hist], S["dd_history_mse"], rtol=1e-4)
