@@ -60,6 +60,26 @@ __global__ void __launch_bounds__(NT) k_reduce(const T* __restrict__ x,
   }
   if (threadIdx.x == 0) *counter = 0u;
 }
+// many short segments (the batched RAS tiles: thousands of (tile) planes of
+// a few thousand elements): one CTA per segment, fixed per-thread strides and
+// a fixed-order CTA sum, so results are still run-to-run bit-identical
+template <typename T, int MODE>
+__global__ void __launch_bounds__(NT) k_reduce_seg(const T* __restrict__ x,
+                                                   const T* __restrict__ y,
+                                                   const double* __restrict__ z, size_t n,
+                                                   double* __restrict__ out) {
+  __shared__ double s0[NT / 32];
+  const size_t off = (size_t)blockIdx.x * n;
+  double acc = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += NT) {
+    double a = (double)x[off + i];
+    if (MODE == 0) acc += a * a;
+    else if (MODE == 1) acc += a * (double)y[off + i];
+    else { double d = a - z[off + i]; acc += d * d; }
+  }
+  double s = cta_sum<NT>(acc, s0);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
 }  // namespace
 
 size_t red_partials() { return MAXB; }
@@ -78,6 +98,13 @@ template <typename T>
 int chan_reduce(int mode, const T* x, const T* y, const double* z, size_t n, int C,
                 double* partial, unsigned* counter, double* out, cudaStream_t s) {
   int nb = nblocks_for(n);
+  if (C >= 2 * num_sms() && n <= (size_t)NT * 64) {
+    if (mode == 0) k_reduce_seg<T, 0><<<C, NT, 0, s>>>(x, y, z, n, out);
+    else if (mode == 1) k_reduce_seg<T, 1><<<C, NT, 0, s>>>(x, y, z, n, out);
+    else k_reduce_seg<T, 2><<<C, NT, 0, s>>>(x, y, z, n, out);
+    SP_CHECK_LAUNCH();
+    return 0;
+  }
   if (mode == 0) k_reduce<T, 0><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
   else if (mode == 1) k_reduce<T, 1><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
   else k_reduce<T, 2><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
