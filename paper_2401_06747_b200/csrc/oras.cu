@@ -32,12 +32,13 @@ namespace sp {
 __device__ unsigned long long g_oras_stats[4];
 __device__ int g_stats_on;
 
-// kernel choice for float blocks <= 32x32: warp-per-job (default) or the
-// 256-thread CTA kernel (sp_oras_variant, for A/B measurements)
-static int oras_use_warp = 0;
+// kernel choice for float blocks <= 32x32: 0 = register-resident 4-warp job
+// kernel (k_oras_rows, default), 1 = the 256-thread CTA kernel with the
+// reference's double-precision stencil (sp_oras_variant, A/B measurements)
+static int oras_kernel = 0;
 int oras_variant(int v) {
-  if (v >= 0) oras_use_warp = v;
-  return oras_use_warp;
+  if (v >= 0) oras_kernel = v;
+  return oras_kernel;
 }
 
 int oras_stats(int enable, unsigned long long* out) {
@@ -238,133 +239,181 @@ __global__ void __launch_bounds__(NT, 4) k_oras_local32(
 }
 
 // ---------------------------------------------------------------------------
-// Barrier-free variant for float blocks up to 32 x 32 (the default ORAS
-// configuration): ONE WARP per (block, channel, tile) job.  Lane j owns
-// column j; the 32 rows of p, res and A p live in registers (fully unrolled),
-// up/down neighbours are the adjacent registers, left/right come from one
-// shuffle each, and the column masks are 32-bit words so every neighbour
-// test is a bit test.  Both CG dots are exact float products accumulated in
-// double per lane and reduced with warp shuffles: no __syncthreads at all.
-// v and the local diagonal live in shared memory (4 KB each per warp).
+// Default float kernel for blocks up to 32 x 32 (the ORAS 32/6 configuration
+// on every level): 4 warps per (block, channel, tile) job.  Warp w owns the 8
+// consecutive block rows 8w..8w+7 and lane j owns column j, so the whole
+// local CG lives in registers: up/down neighbours are the adjacent registers,
+// left/right come from one shuffle each, the mask is a per-thread bit word.
+// Only the two edge rows of each warp cross warps, through shared memory.
+//
+// Two barriers per CG step instead of three: after the r-update each warp
+// publishes its NEW edge residual rows together with its rs partial; after
+// the barrier a neighbour rebuilds the new edge search direction itself as
+// r_edge + beta * p_edge_old -- the same operation, operands and rounding the
+// owning warp uses for its own p -- so p never has to be staged again.
+//
+// Arithmetic: stencil and vector updates in float (fused multiply-adds), the
+// per-thread dot partials in float over 8 pixels, warp and cross-warp sums in
+// double, alpha/beta rounded to float (numba_impl.py:234-247).  The local CG
+// is an inexact smoother whose dot order already differs from the
+// reference's, so solver parity is tolerance based (tests/test_solver_gpu.py)
+// -- the bit-exact B1 kernel-table path keeps the CTA kernels below.
 // ---------------------------------------------------------------------------
-constexpr int WJ = 4;  // jobs (warps) per CTA
+constexpr int RW = 8;           // rows per warp
+constexpr int NWJ = 4;          // warps per job
+constexpr int NTJ = NWJ * 32;   // threads per job
 
-__global__ void __launch_bounds__(WJ * 32) k_oras_warp(
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(NTJ, 6) k_oras_rows(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
-    const int* __restrict__ xs, int nby, int nbx, int bh, int bw, int H, int W, int C,
-    int ntile, int stride, double gamma, long cap, float inv_h2,
-    const float* __restrict__ weights, float* __restrict__ corr,
-    const int* __restrict__ active) {
-  __shared__ float vs_all[WJ][32][33];
-  __shared__ float dg_all[WJ][32][33];
-  const int warp = threadIdx.x >> 5, j = threadIdx.x & 31;
-  const int nb = nby * nbx;
-  const long job = (long)blockIdx.x * WJ + warp;
-  if (job >= (long)nb * C * ntile) return;
-  const int bi = (int)(job % nb);
-  const long rest = job / nb;
-  const int ch = (int)(rest % C), tile = (int)(rest / C);
+    const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W, int stride,
+    float closure, long cap, float inv_h2, const float* __restrict__ weights,
+    float* __restrict__ corr, const int* __restrict__ active) {
+  __shared__ float er_top[NWJ][32], er_bot[NWJ][32];  // edge rows of r (new)
+  __shared__ double red_a[NWJ], red_b[NWJ];
+  const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y, nb = gridDim.x;
+  const int tile = blockIdx.z;
   if (active && !active[tile]) return;
-  float(*vs)[33] = vs_all[warp];
-  float(*dg)[33] = dg_all[warp];
+  const int j = threadIdx.x & 31, w = threadIdx.x >> 5, i0 = w * RW;
   const int kyb = bi / nbx, kxb = bi - kyb * nbx;
   const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
   const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
   const size_t plane = (size_t)H * W;
   const float* rc = r + ((size_t)tile * C + ch) * plane;
   const uint8_t* mt = m + (size_t)tile * plane;
-  const float* wb = weights + (size_t)bi * bh * bw;
   const bool lane_ok = j < bw;
   const int gx = x0 + j;
-  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
 
-  float p[32], res[32], ap[32], wgt[32];
-  uint32_t mcol = 0;
+  // ---- load the job: residual rows, mask bits (own rows + the row above
+  // and below the warp's band), validity
+  float res[RW];
+  uint32_t mb = 0, vb = 0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    res[i] = 0.0f;
-    wgt[i] = 0.0f;
+  for (int s = 0; s < RW; ++s) {
+    const int i = i0 + s;
+    res[s] = 0.0f;
     if (i < bh && lane_ok) {
       const size_t g = (size_t)(y0 + i) * W + gx;
-      if (mt[g]) mcol |= 1u << i;
-      res[i] = rc[g];
-      wgt[i] = wb[i * bw + j];
+      res[s] = rc[g];
+      if (mt[g]) mb |= 1u << s;
+      vb |= 1u << s;
     }
   }
-  const uint32_t valid = lane_ok ? (bh >= 32 ? 0xFFFFFFFFu : ((1u << bh) - 1u)) : 0u;
-  const uint32_t nm = ~mcol & valid;                    // unmasked rows
-  const uint32_t ml = __shfl_up_sync(0xFFFFFFFFu, nm, 1);
-  const uint32_t mr = __shfl_down_sync(0xFFFFFFFFu, nm, 1);
-  const uint32_t upok = (nm << 1) & valid;              // row i-1 unmasked
-  const uint32_t dnok = (nm >> 1) & valid;              // row i+1 unmasked
-  const uint32_t lfok = (j > 0 && lane_ok) ? (ml & valid) : 0u;
-  const uint32_t rtok = (j < bw - 1) ? (mr & valid) : 0u;
-  // Robin-closed diagonal (numba_impl.py:196-226), double in reference order
-  double rs = 0.0;
+  const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
+  const bool has_dn = i0 + RW < bh && lane_ok;
+  const bool m_up = has_up ? mt[(size_t)(y0 + i0 - 1) * W + gx] != 0 : true;
+  const bool m_dn = has_dn ? mt[(size_t)(y0 + i0 + RW) * W + gx] != 0 : true;
+  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
+  // in-block unmasked neighbour bits (bit s = pixel of row i0 + s)
+  const uint32_t um = ~mb & vb;                          // unmasked, valid
+  const uint32_t upok = ((um << 1) | (m_up ? 0u : 1u)) & vb;
+  const uint32_t dnok = ((um >> 1) | (m_dn ? 0u : (1u << (RW - 1)))) & vb;
+  const uint32_t uml = __shfl_up_sync(0xFFFFFFFFu, um, 1);
+  const uint32_t umr = __shfl_down_sync(0xFFFFFFFFu, um, 1);
+  const uint32_t lfok = j > 0 ? (uml & vb) : 0u;
+  const uint32_t rtok = j < bw - 1 ? (umr & vb) : 0u;
+  // Robin-closed local diagonal (numba_impl.py:196-226): in-block neighbours
+  // count 1, block sides inside the image count 1 - gamma
+  float dg[RW];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double d = 0.0;
-    if (i < bh && lane_ok) {
-      const int gy = y0 + i;
-      if (gy > 0) d += (i > 0) ? 1.0 : 1.0 - gamma;
-      if (gy < H - 1) d += (i < bh - 1) ? 1.0 : 1.0 - gamma;
-      if (gx > 0) d += (j > 0) ? 1.0 : 1.0 - gamma;
-      if (gx < W - 1) d += (j < bw - 1) ? 1.0 : 1.0 - gamma;
-    }
-    dg[i][j] = (float)d;
-    vs[i][j] = 0.0f;
-    p[i] = res[i];
-    rs += (double)res[i] * (double)res[i];
+  for (int s = 0; s < RW; ++s) {
+    const int i = i0 + s, gy = y0 + i;
+    float d = 0.0f;
+    if (gy > 0) d += i > 0 ? 1.0f : closure;
+    if (gy < H - 1) d += i < bh - 1 ? 1.0f : closure;
+    if (gx > 0) d += j > 0 ? 1.0f : closure;
+    if (gx < W - 1) d += j < bw - 1 ? 1.0f : closure;
+    dg[s] = d;
   }
+  float p[RW], v[RW], ap[RW];
+  float rs_f = 0.0f;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xFFFFFFFFu, rs, o);
-  __syncwarp();
+  for (int s = 0; s < RW; ++s) {
+    p[s] = res[s];
+    v[s] = 0.0f;
+    rs_f = __fmaf_rn(res[s], res[s], rs_f);
+  }
+  er_top[w][j] = res[0];
+  er_bot[w][j] = res[RW - 1];
+  double rs = warp_sum_d((double)rs_f);
+  if (j == 0) red_a[w] = rs;
+  __syncthreads();
+  rs = 0.0;
+#pragma unroll
+  for (int q = 0; q < NWJ; ++q) rs += red_a[q];
+  // p of the row above / below this warp's band (owned by warps w-1 / w+1)
+  float pu = w > 0 ? er_bot[w - 1][j] : 0.0f;
+  float pd = w < NWJ - 1 ? er_top[w + 1][j] : 0.0f;
   long it = 0;
+  const bool unit_h = inv_h2 == 1.0f;
   while (rs > tau && it < cap) {
+    float pap_f = 0.0f;
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+      const float pl = __shfl_up_sync(0xFFFFFFFFu, p[s], 1);
+      const float pr = __shfl_down_sync(0xFFFFFFFFu, p[s], 1);
+      const float up = s > 0 ? p[s - 1] : pu;
+      const float dn = s < RW - 1 ? p[s + 1] : pd;
+      float acc = ((upok >> s) & 1u) ? up : 0.0f;
+      acc += ((dnok >> s) & 1u) ? dn : 0.0f;
+      acc += ((lfok >> s) & 1u) ? pl : 0.0f;
+      acc += ((rtok >> s) & 1u) ? pr : 0.0f;
+      float a = __fmaf_rn(dg[s], p[s], -acc);
+      if (!unit_h) a *= inv_h2;
+      a = ((mb >> s) & 1u) ? p[s] : a;
+      a = ((vb >> s) & 1u) ? a : 0.0f;
+      ap[s] = a;
+      pap_f = __fmaf_rn(p[s], a, pap_f);
+    }
+    const double pw = warp_sum_d((double)pap_f);
+    if (j == 0) red_b[w] = pw;
+    __syncthreads();
     double pap = 0.0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float pl = __shfl_up_sync(0xFFFFFFFFu, p[i], 1);
-      const float pr = __shfl_down_sync(0xFFFFFFFFu, p[i], 1);
-      float acc = 0.0f;
-      if (i > 0) acc += (upok >> i) & 1u ? p[i - 1] : 0.0f;
-      if (i < 31) acc += (dnok >> i) & 1u ? p[i + 1] : 0.0f;
-      acc += (lfok >> i) & 1u ? pl : 0.0f;
-      acc += (rtok >> i) & 1u ? pr : 0.0f;
-      float a = ((mcol >> i) & 1u) ? p[i] : (dg[i][j] * p[i] - acc) * inv_h2;
-      a = ((valid >> i) & 1u) ? a : 0.0f;
-      ap[i] = a;
-      pap += (double)p[i] * (double)a;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pap += __shfl_xor_sync(0xFFFFFFFFu, pap, o);
+    for (int q = 0; q < NWJ; ++q) pap += red_b[q];
     if (pap <= 0.0) break;
     const float alpha = (float)(rs / pap);
+    float rsn_f = 0.0f;
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+      if ((vb >> s) & 1u) {
+        v[s] = __fmaf_rn(alpha, p[s], v[s]);
+        res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
+      }
+      rsn_f = __fmaf_rn(res[s], res[s], rsn_f);
+    }
+    er_top[w][j] = res[0];
+    er_bot[w][j] = res[RW - 1];
+    const double rw = warp_sum_d((double)rsn_f);
+    if (j == 0) red_a[w] = rw;
+    __syncthreads();
     double rsn = 0.0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if ((valid >> i) & 1u) {
-        vs[i][j] = vs[i][j] + alpha * p[i];
-        res[i] = res[i] - alpha * ap[i];
-      }
-      rsn += (double)res[i] * (double)res[i];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rsn += __shfl_xor_sync(0xFFFFFFFFu, rsn, o);
+    for (int q = 0; q < NWJ; ++q) rsn += red_a[q];
     const float beta = (float)(rsn / rs);
     rs = rsn;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if ((valid >> i) & 1u) p[i] = res[i] + beta * p[i];
+    for (int s = 0; s < RW; ++s)
+      if ((vb >> s) & 1u) p[s] = __fmaf_rn(beta, p[s], res[s]);
+    // the neighbours' new edge directions, rebuilt bit-identically
+    if (w > 0) pu = __fmaf_rn(beta, pu, er_bot[w - 1][j]);
+    if (w < NWJ - 1) pd = __fmaf_rn(beta, pd, er_top[w + 1][j]);
     ++it;
   }
-  __syncwarp();
   float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
+  const float* wb = weights + (size_t)bi * bh * bw;
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if ((valid >> i) & 1u) out[i * bw + j] = wgt[i] * vs[i][j];
-  if (j == 0 && g_stats_on) {
+  for (int s = 0; s < RW; ++s) {
+    const int i = i0 + s;
+    if ((vb >> s) & 1u) out[i * bw + j] = wb[i * bw + j] * v[s];
+  }
+  if (threadIdx.x == 0 && g_stats_on) {
     atomicAdd(&g_oras_stats[0], 1ull);
     atomicAdd(&g_oras_stats[1], (unsigned long long)it);
     if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
@@ -612,11 +661,11 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   const int npx = bh * bw;
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
-  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_use_warp) {
-    const long njobs = (long)nby * nbx * C * ntile;
-    k_oras_warp<<<(unsigned)((njobs + WJ - 1) / WJ), WJ * 32, 0, s>>>(
-        (const float*)r, m, tau_src, tau_scale, ys, xs, nby, nbx, bh, bw, H, W, C, ntile,
-        stride, gamma, cap, (float)inv_h2, (const float*)weights, (float*)corr, active);
+  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 0) {
+    k_oras_rows<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh,
+                                     bw, H, W, stride, (float)(1.0 - gamma), cap,
+                                     (float)inv_h2, (const float*)weights, (float*)corr,
+                                     active);
   } else if (bw == 32 && bh <= 32) {
     k_oras_local32<T><<<grid, NT, 0, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, H, W,
                                           stride, gamma, cap, inv_h2, weights, corr, active);
