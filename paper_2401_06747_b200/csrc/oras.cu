@@ -252,9 +252,15 @@ __global__ void __launch_bounds__(NT, 4) k_oras_local32(
 // r_edge + beta * p_edge_old -- the same operation, operands and rounding the
 // owning warp uses for its own p -- so p never has to be staged again.
 //
+// The operator is applied branch-free: (A p)_i = dgp_i p_i - fm_i * sum of the
+// in-block neighbours' q = fm * p, with fm the valid-and-unmasked indicator
+// and dgp the Robin-closed diagonal (1 on masked identity rows, 0 outside the
+// block), so no per-pixel mask bit tests remain in the loop.
+//
 // Arithmetic: stencil and vector updates in float (fused multiply-adds), the
-// per-thread dot partials in float over 8 pixels, warp and cross-warp sums in
-// double, alpha/beta rounded to float (numba_impl.py:234-247).  The local CG
+// dot partials in float per warp, the cross-warp sums in double, alpha/beta
+// as float quotients (the reference rounds them to the solve dtype,
+// numba_impl.py:234-247).  The local CG
 // is an inexact smoother whose dot order already differs from the
 // reference's, so solver parity is tolerance based (tests/test_solver_gpu.py)
 // -- the bit-exact B1 kernel-table path keeps the CTA kernels below.
@@ -263,12 +269,13 @@ constexpr int RW = 8;           // rows per warp
 constexpr int NWJ = 4;          // warps per job
 constexpr int NTJ = NWJ * 32;   // threads per job
 
-__device__ __forceinline__ double warp_sum_d(double v) {
+__device__ __forceinline__ float warp_sum_f(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
   return v;
 }
 
+template <bool UNIT_H>
 __global__ void __launch_bounds__(NTJ, 6) k_oras_rows(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
@@ -307,29 +314,32 @@ __global__ void __launch_bounds__(NTJ, 6) k_oras_rows(
   }
   const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
   const bool has_dn = i0 + RW < bh && lane_ok;
-  const bool m_up = has_up ? mt[(size_t)(y0 + i0 - 1) * W + gx] != 0 : true;
-  const bool m_dn = has_dn ? mt[(size_t)(y0 + i0 + RW) * W + gx] != 0 : true;
+  // neighbour rows outside the warp's band: 1 if they exist in the block and
+  // are unmasked (their q = p * fm feeds this band's stencil)
+  const float fm_up =
+      has_up && !mt[(size_t)(y0 + i0 - 1) * W + gx] ? 1.0f : 0.0f;
+  const float fm_dn =
+      has_dn && !mt[(size_t)(y0 + i0 + RW) * W + gx] ? 1.0f : 0.0f;
   const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
-  // in-block unmasked neighbour bits (bit s = pixel of row i0 + s)
-  const uint32_t um = ~mb & vb;                          // unmasked, valid
-  const uint32_t upok = ((um << 1) | (m_up ? 0u : 1u)) & vb;
-  const uint32_t dnok = ((um >> 1) | (m_dn ? 0u : (1u << (RW - 1)))) & vb;
-  const uint32_t uml = __shfl_up_sync(0xFFFFFFFFu, um, 1);
-  const uint32_t umr = __shfl_down_sync(0xFFFFFFFFu, um, 1);
-  const uint32_t lfok = j > 0 ? (uml & vb) : 0u;
-  const uint32_t rtok = j < bw - 1 ? (umr & vb) : 0u;
-  // Robin-closed local diagonal (numba_impl.py:196-226): in-block neighbours
-  // count 1, block sides inside the image count 1 - gamma
-  float dg[RW];
+  const bool lf_in = j > 0, rt_in = j < bw - 1;
+  // Branch-free operator (numba_impl.py:196-226 semantics):
+  //   (A p)_i = dgp_i * p_i - fm_i * sum_{in-block nbrs k} fm_k p_k
+  // fm = 1 on valid unmasked pixels, else 0.  dgp = the Robin-closed local
+  // diagonal (in-block neighbours count 1, block sides inside the image
+  // 1 - gamma) on unmasked pixels, 1 on masked pixels (identity rows),
+  // 0 outside the block; invalid pixels keep p = r = 0 throughout.
+  float fm[RW], dgp[RW];
 #pragma unroll
   for (int s = 0; s < RW; ++s) {
     const int i = i0 + s, gy = y0 + i;
     float d = 0.0f;
     if (gy > 0) d += i > 0 ? 1.0f : closure;
     if (gy < H - 1) d += i < bh - 1 ? 1.0f : closure;
-    if (gx > 0) d += j > 0 ? 1.0f : closure;
-    if (gx < W - 1) d += j < bw - 1 ? 1.0f : closure;
-    dg[s] = d;
+    if (gx > 0) d += lf_in ? 1.0f : closure;
+    if (gx < W - 1) d += rt_in ? 1.0f : closure;
+    const bool valid = (vb >> s) & 1u, masked = (mb >> s) & 1u;
+    fm[s] = valid && !masked ? 1.0f : 0.0f;
+    dgp[s] = !valid ? 0.0f : (masked ? 1.0f : d * inv_h2);
   }
   float p[RW], v[RW], ap[RW];
   float rs_f = 0.0f;
@@ -341,66 +351,63 @@ __global__ void __launch_bounds__(NTJ, 6) k_oras_rows(
   }
   er_top[w][j] = res[0];
   er_bot[w][j] = res[RW - 1];
-  double rs = warp_sum_d((double)rs_f);
-  if (j == 0) red_a[w] = rs;
+  const float rsw = warp_sum_f(rs_f);
+  if (j == 0) red_a[w] = (double)rsw;
   __syncthreads();
-  rs = 0.0;
+  double rs = 0.0;
 #pragma unroll
   for (int q = 0; q < NWJ; ++q) rs += red_a[q];
   // p of the row above / below this warp's band (owned by warps w-1 / w+1)
   float pu = w > 0 ? er_bot[w - 1][j] : 0.0f;
   float pd = w < NWJ - 1 ? er_top[w + 1][j] : 0.0f;
   long it = 0;
-  const bool unit_h = inv_h2 == 1.0f;
   while (rs > tau && it < cap) {
+    float q[RW];
+#pragma unroll
+    for (int s = 0; s < RW; ++s) q[s] = p[s] * fm[s];
+    const float qu = pu * fm_up, qd = pd * fm_dn;
     float pap_f = 0.0f;
 #pragma unroll
     for (int s = 0; s < RW; ++s) {
-      const float pl = __shfl_up_sync(0xFFFFFFFFu, p[s], 1);
-      const float pr = __shfl_down_sync(0xFFFFFFFFu, p[s], 1);
-      const float up = s > 0 ? p[s - 1] : pu;
-      const float dn = s < RW - 1 ? p[s + 1] : pd;
-      float acc = ((upok >> s) & 1u) ? up : 0.0f;
-      acc += ((dnok >> s) & 1u) ? dn : 0.0f;
-      acc += ((lfok >> s) & 1u) ? pl : 0.0f;
-      acc += ((rtok >> s) & 1u) ? pr : 0.0f;
-      float a = __fmaf_rn(dg[s], p[s], -acc);
-      if (!unit_h) a *= inv_h2;
-      a = ((mb >> s) & 1u) ? p[s] : a;
-      a = ((vb >> s) & 1u) ? a : 0.0f;
+      float ql = __shfl_up_sync(0xFFFFFFFFu, q[s], 1);
+      float qr = __shfl_down_sync(0xFFFFFFFFu, q[s], 1);
+      ql = lf_in ? ql : 0.0f;
+      qr = rt_in ? qr : 0.0f;
+      const float up = s > 0 ? q[s - 1] : qu;
+      const float dn = s < RW - 1 ? q[s + 1] : qd;
+      const float acc = (up + dn) + (ql + qr);
+      const float fa = fm[s] * acc;
+      const float a = __fmaf_rn(dgp[s], p[s], UNIT_H ? -fa : -(fa * inv_h2));
       ap[s] = a;
       pap_f = __fmaf_rn(p[s], a, pap_f);
     }
-    const double pw = warp_sum_d((double)pap_f);
-    if (j == 0) red_b[w] = pw;
+    const float pw = warp_sum_f(pap_f);
+    if (j == 0) red_b[w] = (double)pw;
     __syncthreads();
     double pap = 0.0;
 #pragma unroll
-    for (int q = 0; q < NWJ; ++q) pap += red_b[q];
+    for (int q2 = 0; q2 < NWJ; ++q2) pap += red_b[q2];
     if (pap <= 0.0) break;
-    const float alpha = (float)(rs / pap);
+    const float alpha = (float)rs / (float)pap;
     float rsn_f = 0.0f;
 #pragma unroll
     for (int s = 0; s < RW; ++s) {
-      if ((vb >> s) & 1u) {
-        v[s] = __fmaf_rn(alpha, p[s], v[s]);
-        res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
-      }
+      v[s] = __fmaf_rn(alpha, p[s], v[s]);
+      res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
       rsn_f = __fmaf_rn(res[s], res[s], rsn_f);
     }
     er_top[w][j] = res[0];
     er_bot[w][j] = res[RW - 1];
-    const double rw = warp_sum_d((double)rsn_f);
-    if (j == 0) red_a[w] = rw;
+    const float rw = warp_sum_f(rsn_f);
+    if (j == 0) red_a[w] = (double)rw;
     __syncthreads();
     double rsn = 0.0;
 #pragma unroll
-    for (int q = 0; q < NWJ; ++q) rsn += red_a[q];
-    const float beta = (float)(rsn / rs);
+    for (int q2 = 0; q2 < NWJ; ++q2) rsn += red_a[q2];
+    const float beta = (float)rsn / (float)rs;
     rs = rsn;
 #pragma unroll
-    for (int s = 0; s < RW; ++s)
-      if ((vb >> s) & 1u) p[s] = __fmaf_rn(beta, p[s], res[s]);
+    for (int s = 0; s < RW; ++s) p[s] = __fmaf_rn(beta, p[s], res[s]);
     // the neighbours' new edge directions, rebuilt bit-identically
     if (w > 0) pu = __fmaf_rn(beta, pu, er_bot[w - 1][j]);
     if (w < NWJ - 1) pd = __fmaf_rn(beta, pd, er_top[w + 1][j]);
@@ -611,9 +618,55 @@ __global__ void k_block_weights(T* __restrict__ weights, const int* __restrict__
 }
 
 // u += sum over covering blocks (block order) of the weighted corrections.
-// grid (nbx_cta, ntile * C): CTA walks the plane's 32x8 pixel tiles.
-template <typename T>
+// grid (nbx_cta, ntile): a thread owns one pixel of the tile's plane and
+// ALL C channels, so the covering-block lookup (<= 3 x 3 blocks, normally
+// 1-4) and the per-block offsets are computed once per pixel, not per
+// channel.  The blocks are visited in ascending block index (row-major
+// ky, kx), exactly the reference's sequential blend order.
+template <typename T, int CM>
 __global__ void __launch_bounds__(256) k_oras_blend(
+    T* __restrict__ u, const T* __restrict__ corr, const int* __restrict__ ys,
+    const int* __restrict__ xs, const int* __restrict__ row_k0,
+    const int* __restrict__ row_n, const int* __restrict__ col_k0,
+    const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int Cdyn,
+    const int* __restrict__ active) {
+  const int C = CM > 0 ? CM : Cdyn;
+  const int tile = blockIdx.y;
+  if (active && !active[tile]) return;
+  const int nb = nby * nbx;
+  const size_t plane = (size_t)H * W, npx = (size_t)bh * bw, cplane = (size_t)nb * npx;
+  T* ut = u + (size_t)tile * C * plane;
+  const T* ct = corr + (size_t)tile * C * cplane;
+  const int ntx = (W + 31) / 32, nty = (H + 7) / 8, per = ntx * nty;
+  for (int t = blockIdx.x; t < per; t += gridDim.x) {
+    const int x = (t % ntx) * 32 + threadIdx.x, y = (t / ntx) * 8 + threadIdx.y;
+    if (x >= W || y >= H) continue;
+    const int ky0 = row_k0[y], nky = row_n[y], kx0 = col_k0[x], nkx = col_n[x];
+    const size_t k = (size_t)y * W + x;
+    T acc[CM > 0 ? CM : 4];
+#pragma unroll
+    for (int c = 0; c < (CM > 0 ? CM : 4); ++c)
+      if (c < C) acc[c] = ut[(size_t)c * plane + k];
+    for (int a = 0; a < nky; ++a) {
+      const int ky = ky0 + a;
+      const size_t rowoff = (size_t)ky * nbx * npx + (size_t)(y - ys[ky]) * bw;
+      for (int b2 = 0; b2 < nkx; ++b2) {
+        const int kx = kx0 + b2;
+        const size_t off = rowoff + (size_t)kx * npx + (size_t)(x - xs[kx]);
+#pragma unroll
+        for (int c = 0; c < (CM > 0 ? CM : 4); ++c)
+          if (c < C) acc[c] = acc[c] + ct[(size_t)c * cplane + off];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < (CM > 0 ? CM : 4); ++c)
+      if (c < C) ut[(size_t)c * plane + k] = acc[c];
+  }
+}
+
+// generic channel count (C > 4): one channel plane per grid row
+template <typename T>
+__global__ void __launch_bounds__(256) k_oras_blend_plane(
     T* __restrict__ u, const T* __restrict__ corr, const int* __restrict__ ys,
     const int* __restrict__ xs, const int* __restrict__ row_k0,
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
@@ -630,22 +683,14 @@ __global__ void __launch_bounds__(256) k_oras_blend(
     const int x = (t % ntx) * 32 + threadIdx.x, y = (t / ntx) * 8 + threadIdx.y;
     if (x >= W || y >= H) continue;
     const int ky0 = row_k0[y], nky = row_n[y], kx0 = col_k0[x], nkx = col_n[x];
-    T cv[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      const int a = q / 3, b = q % 3;
-      cv[q] = (T)0;
-      if (a < nky && b < nkx) {
-        const int ky = ky0 + a, kx = kx0 + b;
-        cv[q] = cc[(size_t)(ky * nbx + kx) * npx + (size_t)(y - ys[ky]) * bw + (x - xs[kx])];
-      }
-    }
     const size_t k = (size_t)y * W + x;
     T uv = uc[k];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      const int a = q / 3, b = q % 3;
-      if (a < nky && b < nkx) uv = uv + cv[q];
+    for (int a = 0; a < nky; ++a) {
+      const int ky = ky0 + a;
+      for (int b2 = 0; b2 < nkx; ++b2) {
+        const int kx = kx0 + b2;
+        uv = uv + cc[(size_t)(ky * nbx + kx) * npx + (size_t)(y - ys[ky]) * bw + (x - xs[kx])];
+      }
     }
     uc[k] = uv;
   }
@@ -662,10 +707,10 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
   if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 0) {
-    k_oras_rows<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh,
-                                     bw, H, W, stride, (float)(1.0 - gamma), cap,
-                                     (float)inv_h2, (const float*)weights, (float*)corr,
-                                     active);
+    auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
+    kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
+                              W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
+                              (const float*)weights, (float*)corr, active);
   } else if (bw == 32 && bh <= 32) {
     k_oras_local32<T><<<grid, NT, 0, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, H, W,
                                           stride, gamma, cap, inv_h2, weights, corr, active);
@@ -692,12 +737,21 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile,
                       const int* active) {
   long per = (long)cdiv(W, 32) * cdiv(H, 8);
-  long nz = (long)ntile * C;
+  long nz = C <= 4 ? (long)ntile : (long)ntile * C;
   long nbx_cta = (2L * 148 * 8 + nz - 1) / nz;
   if (nbx_cta > per) nbx_cta = per;
   if (nbx_cta < 1) nbx_cta = 1;
-  k_oras_blend<T><<<dim3((unsigned)nbx_cta, (unsigned)nz), dim3(32, 8), 0, s>>>(
-      u, corr, ys, xs, row_k0, row_n, col_k0, col_n, nby, nbx, bh, bw, H, W, C, active);
+  dim3 grid((unsigned)nbx_cta, (unsigned)nz), blk(32, 8);
+#define SP_BLEND(CM)                                                                      \
+  k_oras_blend<T, CM><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n, \
+                                          nby, nbx, bh, bw, H, W, C, active)
+  if (C == 1) SP_BLEND(1);
+  else if (C == 3) SP_BLEND(3);
+  else if (C <= 4) SP_BLEND(0);
+  else
+    k_oras_blend_plane<T><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n,
+                                               nby, nbx, bh, bw, H, W, C, active);
+#undef SP_BLEND
   SP_CHECK_LAUNCH();
   return 0;
 }

@@ -259,12 +259,14 @@ def cgnr_tonal(f: Image, mask: Mask, init: TonalState | None = None,
 # ---------------------------------------------------------------------------
 
 def _cover_tables(starts, size, dim):
-    k0 = np.zeros(dim, np.int32)
-    nn = np.zeros(dim, np.int32)
-    for y in range(dim):
-        ks = [k for k, s in enumerate(starts) if s <= y < s + size]
-        k0[y] = ks[0] if ks else 0
-        nn[y] = len(ks)
+    """First covering block and number of covering blocks per row/column
+    (sorted starts; vectorised)."""
+    st = np.asarray(starts, np.int64)
+    y = np.arange(dim)
+    first = np.searchsorted(st + size, y, side="right")
+    last = np.searchsorted(st, y, side="right") - 1
+    nn = np.maximum(last - first + 1, 0).astype(np.int32)
+    k0 = np.where(nn > 0, first, 0).astype(np.int32)
     return k0, nn
 
 

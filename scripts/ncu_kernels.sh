@@ -1,11 +1,12 @@
 #!/bin/bash
-# ncu --set full of the finest-level ORAS local CG, blend and residual sweeps
-# (warm 4K RGB V-cycle); run under gpurun from the repo root.
-TAG=${1:-r01}
+# ncu --set full of finest-level V-cycle kernels (warm 4K RGB V-cycle,
+# scripts/probe_vcycle.py); run under gpurun from the repo root.
+#   bash scripts/ncu_kernels.sh TAG kernel_regex...
+TAG=${1:-r01}; shift
+KS=${@:-k_oras_rows k4_residual k_oras_blend}
 mkdir -p gpurun_out
-for K in k_oras_local32 k4_residual k_oras_blend; do
+for K in $KS; do
   timeout 300 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "warm/" \
     -k regex:$K -c 1 -o gpurun_out/prof_${K}_$TAG -f \
     python scripts/probe_vcycle.py 1 > gpurun_out/ncu_${K}_$TAG.log 2>&1
 done
-ls -la gpurun_out
