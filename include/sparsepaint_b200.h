@@ -152,6 +152,32 @@ int sp_hier_solve_tiles(void* hier, const void* bsym, void* u, int init_mode, do
                         int cycles, int max_cycles, const int* active_h, int* iters_h,
                         int* conv_h, void* stream);
 
+/* ============ B2: row-strip partitioned solve ============== */
+/* The north_star's multi-GPU layout for large images: the finest `La`
+ * levels of the inpainting hierarchy are cut into P row strips (owned rows
+ * o0/o1, int[La][P], multiples of 16 except the image end), each computed
+ * on its owned rows widened by `halo` (>= 33, multiple of 16) rows; the
+ * coarser levels are replicated.  Per smoothing sweep: halo exchange, ORAS
+ * on the view, and the residual norms combined across strips as
+ * partition-independent row-band partials, so the solve is bit-identical for
+ * every P.  This process holds strips [first, first + nloc); strips on other
+ * ranks are reached through the NCCL communicator `comm` (one strip per
+ * rank, rank = strip index), strips in this process through device copies.
+ * Same semantics as sp_hier_solve (solver.py:328-372) on a float32 image;
+ * bsym / u are full-size, u returns the gathered solution on every rank.
+ * No reference counterpart: the reference is single-process CPU code. */
+int sp_nccl_unique_id(uint8_t* out128);
+int sp_nccl_comm_create(void** comm, const uint8_t* id128, int nranks, int rank);
+int sp_nccl_comm_destroy(void* comm);
+int sp_strip_create(void** out, int C, int H, int W, int block, int overlap, int levels,
+                    int pre, int post, double alpha, double rho, int P, int nloc, int first,
+                    int La, int halo, const int* o0_h, const int* o1_h, void* comm);
+int sp_strip_destroy(void* group);
+int sp_strip_set_mask(void* group, const uint8_t* mask, const void* values, void* stream);
+int sp_strip_solve(void* group, const void* bsym, void* u, int init_mode, double tol,
+                   int cycles, int max_cycles, sp_solve_report* rep, void* stream);
+int sp_strip_levels(void* group, int* nlev, int* dims, int cap);
+
 /* ================ B2: densification geometry workspace ================== */
 /* One workspace per (H, W).  Replaces, per densification iteration,
  * jump_flood_voronoi (geometry.py:92-110), delaunay_from_voronoi (:113-185),
@@ -241,8 +267,14 @@ int sp_ct_apply_tiles(int dtype, const void* w, const uint8_t* mask, void* out, 
 /* ORAS local-CG statistics {jobs, iterations, converged-on-entry, max it};
  * enable 1 = reset+start, 0 = reset+stop, -1 = read only */
 int sp_stats(int enable, uint64_t* out_h);
-/* float ORAS kernel for blocks <= 32x32: 1 warp/job, 0 CTA/job; v < 0 query */
+/* float ORAS kernel for blocks <= 32x32: 0 = register-resident 4-warp job
+ * kernel (default), 1 = 256-thread CTA kernel; v < 0 query */
 int sp_oras_variant(int v);
+/* Default sweep kernels of hierarchies created afterwards: 1 = row-marching
+ * float kernels on wide float levels (mgfast.cu), 0 = the reference-exact
+ * double-accumulating kernels everywhere; v < 0 queries.  A/B measurement
+ * aid, no reference counterpart. */
+int sp_march_variant(int v);
 /* kernels launched by the library since the last reset */
 long long sp_launch_count(int reset);
 /* CUDA-event timing of a finest-level kernel (0 residual, 1 ORAS local CG,

@@ -52,6 +52,15 @@ _SIGS = {
     "sp_hier_solve": [P, P, P, c_int, c_double, c_int, c_int, P, P],
     "sp_hier_vcycle": [P, P, P, P],
     "sp_hier_solve_tiles": [P, P, P, c_int, c_double, c_int, c_int, P, P, P, P],
+    "sp_nccl_unique_id": [P],
+    "sp_nccl_comm_create": [P, P, c_int, c_int],
+    "sp_nccl_comm_destroy": [P],
+    "sp_strip_create": [P, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_double,
+                        c_double, c_int, c_int, c_int, c_int, c_int, P, P, P],
+    "sp_strip_destroy": [P],
+    "sp_strip_set_mask": [P, P, P, P],
+    "sp_strip_solve": [P, P, P, c_int, c_double, c_int, c_int, P, P],
+    "sp_strip_levels": [P, P, P, c_int],
     "sp_geo_create": [P, c_int, c_int],
     "sp_geo_destroy": [P],
     "sp_geo_voronoi": [P, P, c_double, P, P, P, P],
@@ -80,6 +89,7 @@ _SIGS = {
     "sp_pcg64_doubles": [P, ctypes.c_longlong, ctypes.c_longlong, P, P],
     "sp_pairwise_sum": [P, ctypes.c_longlong, P, P],
     "sp_oras_variant": [c_int],
+    "sp_march_variant": [c_int],
     "sp_geo_export": [P, P, P, P, P, P, P, P, c_long, P],
 }
 

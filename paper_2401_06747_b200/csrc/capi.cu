@@ -466,6 +466,11 @@ int oras_variant(int v);
 // (default), 0 = CTA per job; v < 0 only queries.  Returns the current value.
 extern "C" int sp_oras_variant(int v) { return sp::oras_variant(v); }
 
+namespace sp {
+int march_default(int v);
+}
+extern "C" int sp_march_variant(int v) { return sp::march_default(v); }
+
 // ---- dithered initial mask (spatial.py:107-148) -------------------------------
 namespace sp {
 int density_map(const double* f, int C, int H, int W, double density, const double* gauss_h,
@@ -499,6 +504,59 @@ int sp_pcg64_doubles(const uint64_t* pcg_h, long long start, long long count, do
 
 int sp_pairwise_sum(const double* a, long long n, double* out_h, void* s) {
   return sp::pairwise_sum(a, n, out_h, STREAM(s));
+}
+}  // extern "C"
+
+// ---- B2: row-strip partitioned solve (strips.cu) -----------------
+namespace sp {
+struct StripGroup;
+int strip_create(StripGroup** out, int C, int H, int W, const HierCfg& cfg, int P, int nloc,
+                 int first, int La, int halo, const int* o0, const int* o1, void* comm);
+void strip_destroy(StripGroup* g);
+int strip_set_mask(StripGroup* g, const uint8_t* mask, const float* values, cudaStream_t s);
+int strip_solve(StripGroup* g, const float* bsym, float* u_io, int init_mode, double tol,
+                int cycles, int max_cycles, cudaStream_t s, SolveReport* rep);
+int strip_levels(StripGroup* g, int* nlev, int* dims, int cap);
+int nccl_unique_id(uint8_t* out);
+int nccl_comm_create(void** comm, const uint8_t* id_bytes, int nranks, int rank);
+int nccl_comm_destroy(void* comm);
+}  // namespace sp
+
+extern "C" {
+int sp_nccl_unique_id(uint8_t* out128) { return sp::nccl_unique_id(out128); }
+int sp_nccl_comm_create(void** comm, const uint8_t* id128, int nranks, int rank) {
+  return sp::nccl_comm_create(comm, id128, nranks, rank);
+}
+int sp_nccl_comm_destroy(void* comm) { return sp::nccl_comm_destroy(comm); }
+
+int sp_strip_create(void** out, int C, int H, int W, int block, int overlap, int levels,
+                    int pre, int post, double alpha, double rho, int P, int nloc, int first,
+                    int La, int halo, const int* o0_h, const int* o1_h, void* comm) {
+  HierCfg cfg;
+  cfg.block = block;
+  cfg.overlap = overlap;
+  cfg.levels = levels;
+  cfg.pre = pre;
+  cfg.post = post;
+  cfg.alpha = alpha;
+  cfg.rho = rho;
+  return sp::strip_create((sp::StripGroup**)out, C, H, W, cfg, P, nloc, first, La, halo, o0_h,
+                          o1_h, comm);
+}
+int sp_strip_destroy(void* g) {
+  sp::strip_destroy((sp::StripGroup*)g);
+  return 0;
+}
+int sp_strip_set_mask(void* g, const uint8_t* mask, const void* values, void* s) {
+  return sp::strip_set_mask((sp::StripGroup*)g, mask, (const float*)values, STREAM(s));
+}
+int sp_strip_solve(void* g, const void* bsym, void* u, int init_mode, double tol, int cycles,
+                   int max_cycles, sp_solve_report* rep, void* s) {
+  return sp::strip_solve((sp::StripGroup*)g, (const float*)bsym, (float*)u, init_mode, tol,
+                         cycles, max_cycles, STREAM(s), (sp::SolveReport*)rep);
+}
+int sp_strip_levels(void* g, int* nlev, int* dims, int cap) {
+  return sp::strip_levels((sp::StripGroup*)g, nlev, dims, cap);
 }
 }  // extern "C"
 

@@ -27,18 +27,31 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile = 1, const int* active = nullptr,
-                      int stride = 0);
+                      int stride = 0, int corr_nb = 0);
 // u += weighted corrections of the covering blocks, in block order
 template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile = 1,
-                      const int* active = nullptr);
+                      const int* active = nullptr, int corr_nb = 0);
 // partition-of-unity weights [nb][bh][bw] (solver.py:142-197)
 template <typename T>
 int block_weights_launch(T* weights, const int* ys, const int* xs, const int* row_k0,
                          const int* row_n, const int* col_k0, const int* col_n, int nby,
                          int nbx, int bh, int bw, int H, int W, int overlap, cudaStream_t s);
+
+// ---- mgfast.cu: row-marching float sweeps (W % 4 == 0, W >= 128, inv_h2 = 1) --
+bool march_ok(int H, int W, size_t npart);
+int resid_march(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
+                unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s,
+                int ntile, const int* active, double* bandcol = nullptr, int band0 = 0,
+                int nbt = 0);
+int march_band_rows();  // rows per norm band (bandcol mode)
+int resid_restrict_march(const float* u, const float* b, const uint8_t* m, float* rc, int C,
+                         int H, int W, cudaStream_t s, int ntile, const int* active);
+int prolong_march(const float* e, float* u, const float* b, const uint8_t* m, int C, int chh,
+                  int cww, int H, int W, int add, cudaStream_t s, int ntile,
+                  const int* active);
 
 // ---- vec.cu ------------------------------------------------------------------
 template <typename T>

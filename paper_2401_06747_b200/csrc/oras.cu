@@ -276,15 +276,18 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 }
 
 template <bool UNIT_H>
-__global__ void __launch_bounds__(NTJ, 6) k_oras_rows(
+__global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
     const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W, int stride,
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
-    float* __restrict__ corr, const int* __restrict__ active) {
+    float* __restrict__ corr, const int* __restrict__ active, int corr_nb) {
   __shared__ float er_top[NWJ][32], er_bot[NWJ][32];  // edge rows of r (new)
   __shared__ double red_a[NWJ], red_b[NWJ];
-  const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y, nb = gridDim.x;
+  // corr_nb: blocks per channel plane of `corr` (a row-strip view launches a
+  // sub-range of the level's blocks, `weights` / `corr` offset to its first)
+  const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y;
+  const int nb = corr_nb > 0 ? corr_nb : (int)gridDim.x;
   const int tile = blockIdx.z;
   if (active && !active[tile]) return;
   const int j = threadIdx.x & 31, w = threadIdx.x >> 5, i0 = w * RW;
@@ -629,38 +632,73 @@ __global__ void __launch_bounds__(256) k_oras_blend(
     const int* __restrict__ xs, const int* __restrict__ row_k0,
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
     const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int Cdyn,
-    const int* __restrict__ active) {
+    const int* __restrict__ active, int corr_nb) {
   const int C = CM > 0 ? CM : Cdyn;
   const int tile = blockIdx.y;
   if (active && !active[tile]) return;
-  const int nb = nby * nbx;
+  const int nb = corr_nb > 0 ? corr_nb : nby * nbx;
   const size_t plane = (size_t)H * W, npx = (size_t)bh * bw, cplane = (size_t)nb * npx;
   T* ut = u + (size_t)tile * C * plane;
   const T* ct = corr + (size_t)tile * C * cplane;
-  const int ntx = (W + 31) / 32, nty = (H + 7) / 8, per = ntx * nty;
+  constexpr int CC = CM > 0 ? CM : 4;
+  // a CTA tile is 32 x 16 pixels: each thread blends rows y and y + 8, and
+  // issues all corrections of both pixels (<= 2 x 2 covering blocks each, the
+  // regular case) before adding them, for memory-level parallelism
+  const int ntx = (W + 31) / 32, nty = (H + 15) / 16, per = ntx * nty;
   for (int t = blockIdx.x; t < per; t += gridDim.x) {
-    const int x = (t % ntx) * 32 + threadIdx.x, y = (t / ntx) * 8 + threadIdx.y;
-    if (x >= W || y >= H) continue;
-    const int ky0 = row_k0[y], nky = row_n[y], kx0 = col_k0[x], nkx = col_n[x];
-    const size_t k = (size_t)y * W + x;
-    T acc[CM > 0 ? CM : 4];
+    const int x = (t % ntx) * 32 + threadIdx.x;
+    if (x >= W) continue;
+    const int kx0 = col_k0[x], nkx = col_n[x];
+    const int xo0 = x - xs[kx0], xo1 = nkx > 1 ? x - xs[kx0 + 1] : 0;
 #pragma unroll
-    for (int c = 0; c < (CM > 0 ? CM : 4); ++c)
-      if (c < C) acc[c] = ut[(size_t)c * plane + k];
-    for (int a = 0; a < nky; ++a) {
-      const int ky = ky0 + a;
-      const size_t rowoff = (size_t)ky * nbx * npx + (size_t)(y - ys[ky]) * bw;
-      for (int b2 = 0; b2 < nkx; ++b2) {
-        const int kx = kx0 + b2;
-        const size_t off = rowoff + (size_t)kx * npx + (size_t)(x - xs[kx]);
+    for (int half = 0; half < 2; ++half) {
+      const int y = (t / ntx) * 16 + threadIdx.y + 8 * half;
+      if (y >= H) continue;
+      const int ky0 = row_k0[y], nky = row_n[y];
+      const size_t k = (size_t)y * W + x;
+      T acc[CC];
 #pragma unroll
-        for (int c = 0; c < (CM > 0 ? CM : 4); ++c)
-          if (c < C) acc[c] = acc[c] + ct[(size_t)c * cplane + off];
+      for (int c = 0; c < CC; ++c)
+        if (c < C) acc[c] = ut[(size_t)c * plane + k];
+      if (nky <= 2 && nkx <= 2) {
+        // offsets of the (ky0 + a, kx0 + b) corrections, block order
+        size_t off[4];
+        bool on[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = q >> 1, b2 = q & 1;
+          on[q] = a < nky && b2 < nkx;
+          const int ky = ky0 + (on[q] ? a : 0), kx = kx0 + (on[q] ? b2 : 0);
+          off[q] = ((size_t)ky * nbx + kx) * npx + (size_t)(y - ys[ky]) * bw + (b2 ? xo1 : xo0);
+        }
+        T v[4][CC];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < CC; ++c)
+            v[q][c] = (on[q] && c < C) ? ct[(size_t)c * cplane + off[q]] : (T)0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < CC; ++c)
+            if (on[q] && c < C) acc[c] = acc[c] + v[q][c];
+      } else {
+        for (int a = 0; a < nky; ++a) {
+          const int ky = ky0 + a;
+          const size_t rowoff = (size_t)ky * nbx * npx + (size_t)(y - ys[ky]) * bw;
+          for (int b2 = 0; b2 < nkx; ++b2) {
+            const int kx = kx0 + b2;
+            const size_t off = rowoff + (size_t)kx * npx + (size_t)(x - xs[kx]);
+#pragma unroll
+            for (int c = 0; c < CC; ++c)
+              if (c < C) acc[c] = acc[c] + ct[(size_t)c * cplane + off];
+          }
+        }
       }
-    }
 #pragma unroll
-    for (int c = 0; c < (CM > 0 ? CM : 4); ++c)
-      if (c < C) ut[(size_t)c * plane + k] = acc[c];
+      for (int c = 0; c < CC; ++c)
+        if (c < C) ut[(size_t)c * plane + k] = acc[c];
+    }
   }
 }
 
@@ -671,10 +709,10 @@ __global__ void __launch_bounds__(256) k_oras_blend_plane(
     const int* __restrict__ xs, const int* __restrict__ row_k0,
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
     const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int C,
-    const int* __restrict__ active) {
+    const int* __restrict__ active, int corr_nb) {
   const int z = blockIdx.y, tile = z / C;
   if (active && !active[tile]) return;
-  const int nb = nby * nbx;
+  const int nb = corr_nb > 0 ? corr_nb : nby * nbx;
   const size_t plane = (size_t)H * W, npx = (size_t)bh * bw;
   T* uc = u + (size_t)z * plane;
   const T* cc = corr + (size_t)z * nb * npx;
@@ -702,15 +740,20 @@ template <typename T>
 int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, double tau_scale,
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
-                      T* corr, cudaStream_t s, int ntile, const int* active, int stride) {
+                      T* corr, cudaStream_t s, int ntile, const int* active, int stride,
+                      int corr_nb) {
   const int npx = bh * bw;
+  if (corr_nb > 0 && !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 0)) {
+    set_error("block sub-range launches need the float 32x32 ORAS kernel");
+    return -2;
+  }
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
   if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 0) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
     kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
                               W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
-                              (const float*)weights, (float*)corr, active);
+                              (const float*)weights, (float*)corr, active, corr_nb);
   } else if (bw == 32 && bh <= 32) {
     k_oras_local32<T><<<grid, NT, 0, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, H, W,
                                           stride, gamma, cap, inv_h2, weights, corr, active);
@@ -735,8 +778,8 @@ template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile,
-                      const int* active) {
-  long per = (long)cdiv(W, 32) * cdiv(H, 8);
+                      const int* active, int corr_nb) {
+  long per = (long)cdiv(W, 32) * cdiv(H, C <= 4 ? 16 : 8);
   long nz = C <= 4 ? (long)ntile : (long)ntile * C;
   long nbx_cta = (2L * 148 * 8 + nz - 1) / nz;
   if (nbx_cta > per) nbx_cta = per;
@@ -744,13 +787,13 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   dim3 grid((unsigned)nbx_cta, (unsigned)nz), blk(32, 8);
 #define SP_BLEND(CM)                                                                      \
   k_oras_blend<T, CM><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n, \
-                                          nby, nbx, bh, bw, H, W, C, active)
+                                          nby, nbx, bh, bw, H, W, C, active, corr_nb)
   if (C == 1) SP_BLEND(1);
   else if (C == 3) SP_BLEND(3);
   else if (C <= 4) SP_BLEND(0);
   else
     k_oras_blend_plane<T><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n,
-                                               nby, nbx, bh, bw, H, W, C, active);
+                                               nby, nbx, bh, bw, H, W, C, active, corr_nb);
 #undef SP_BLEND
   SP_CHECK_LAUNCH();
   return 0;
@@ -772,10 +815,10 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
   template int oras_local_launch<T>(const T*, const uint8_t*, const double*, double,        \
                                     const int*, const int*, int, int, int, int, int, int,   \
                                     int, double, long, double, const T*, T*, cudaStream_t,  \
-                                    int, const int*, int);                                  \
+                                    int, const int*, int, int);                             \
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
-                                    int, int, int, cudaStream_t, int, const int*);          \
+                                    int, int, int, cudaStream_t, int, const int*, int);     \
   template int block_weights_launch<T>(T*, const int*, const int*, const int*, const int*,  \
                                        const int*, const int*, int, int, int, int, int,     \
                                        int, int, cudaStream_t);

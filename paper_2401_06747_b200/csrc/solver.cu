@@ -23,6 +23,16 @@
 
 namespace sp {
 
+// default for new hierarchies: row-marching sweeps on the wide float levels
+// (1) or the per-pixel kernels everywhere (0, measured faster on B200 for
+// the single-image solve: profiles/oras_ab_r01*.txt); sp_march_variant.
+// The row-strip solver always uses the row-marching kernels.
+int march_default(int v) {
+  static int on = 0;
+  if (v >= 0) on = v;
+  return on;
+}
+
 // covering tables for sorted block starts (host)
 void cover_tables(const std::vector<int>& starts, int size, int dim, std::vector<int>& k0,
                   std::vector<int>& n) {
@@ -79,6 +89,7 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     return -2;
   }
   Hier* h = new Hier();
+  h->march = march_default(-1) != 0;
   h->dtype = dtype;
   h->C = C;
   h->ntile = ntile;
@@ -201,16 +212,50 @@ int hier_set_mask(Hier* h, const uint8_t* mask, const void* values, cudaStream_t
 
 // ---- V-cycle ----------------------------------------------------------------
 
+// the level sweeps: row-marching float kernels on wide float levels
+// (mgfast.cu), the reference-exact double-accumulating kernels otherwise
+template <typename T>
+static bool use_march(const Hier* h, const Level& L) {
+  return sizeof(T) == 4 && h->march && march_ok(L.H, L.W, L.npart) &&
+         (((uintptr_t)L.u | (uintptr_t)L.b | (uintptr_t)L.r | (uintptr_t)L.mask) & 15u) == 0;
+}
+
 template <typename T>
 static int residual_lv(Hier* h, int lv, bool with_norms, cudaStream_t s) {
   Level& L = h->lv[lv];
+  if (use_march<T>(h, L))
+    return resid_march((const float*)L.u, (const float*)L.b, L.mask, (float*)L.r, L.partial,
+                       L.counter, with_norms ? L.norms : nullptr, h->C, L.H, L.W, s, h->ntile,
+                       h->d_active);
   return residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
                      with_norms ? L.norms : nullptr, h->C, L.H, L.W, 1.0, s, h->ntile,
                      h->d_active);
 }
 
 template <typename T>
-static int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
+static int residual_restrict_lv(Hier* h, int lv, cudaStream_t s) {
+  Level& F = h->lv[lv];
+  Level& G = h->lv[lv + 1];
+  if (use_march<T>(h, F))
+    return resid_restrict_march((const float*)F.u, (const float*)F.b, F.mask, (float*)G.r,
+                                h->C, F.H, F.W, s, h->ntile, h->d_active);
+  return residual_restrict<T>((const T*)F.u, (const T*)F.b, F.mask, (T*)G.r, h->C, F.H, F.W,
+                              1.0, s, h->ntile, h->d_active);
+}
+
+template <typename T>
+int prolong_lv(Hier* h, int lv, int add, cudaStream_t s) {
+  Level& F = h->lv[lv];
+  Level& G = h->lv[lv + 1];
+  if (use_march<T>(h, F))
+    return prolong_march((const float*)G.u, (float*)F.u, (const float*)F.b, F.mask, h->C, G.H,
+                         G.W, F.H, F.W, add, s, h->ntile, h->d_active);
+  return prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H, G.W, F.H,
+                            F.W, add, s, h->ntile, h->d_active);
+}
+
+template <typename T>
+int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
   Level& L = h->lv[lv];
   for (int sw = 0; sw < sweeps; ++sw) {
     if (!(sw == 0 && first_done)) SP_TRY(residual_lv<T>(h, lv, true, s));
@@ -228,20 +273,18 @@ static int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t 
 // solver.py:283-300; `first_done`: level lv's residual r/norms for the
 // current u are already in place (computed by the caller's tolerance check)
 template <typename T>
-static int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
+int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
   const HierCfg& cfg = h->cfg;
   int last = (int)h->lv.size() - 1;
   if (lv == last) return smooth_lv<T>(h, lv, cfg.pre + cfg.post, first_done, s);
   SP_TRY(smooth_lv<T>(h, lv, cfg.pre, first_done, s));
   Level& F = h->lv[lv];
   Level& G = h->lv[lv + 1];
-  SP_TRY(residual_restrict<T>((const T*)F.u, (const T*)F.b, F.mask, (T*)G.r, h->C, F.H,
-                              F.W, 1.0, s, h->ntile, h->d_active));
+  SP_TRY(residual_restrict_lv<T>(h, lv, s));
   SP_TRY(sym_rhs<T>((const T*)G.r, G.mask, (T*)G.b, (T*)G.u, h->C, G.H, G.W, 1.0, s,
                     h->ntile, h->d_active));
   SP_TRY(vcycle_lv<T>(h, lv + 1, false, s));
-  SP_TRY(prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H, G.W,
-                            F.H, F.W, 1, s, h->ntile, h->d_active));
+  SP_TRY(prolong_lv<T>(h, lv, 1, s));
   SP_TRY(smooth_lv<T>(h, lv, cfg.post, false, s));
   return 0;
 }
@@ -288,8 +331,7 @@ static int cascade_t(Hier* h, cudaStream_t s) {
     Level& G = h->lv[lv + 1];
     SP_TRY(masked_sym_rhs<T>((const T*)F.values, F.mask, (T*)F.b, h->C, F.H, F.W, s, nt,
                              h->d_active));
-    SP_TRY(prolong_enforce<T>((const T*)G.u, (T*)F.u, (const T*)F.b, F.mask, h->C, G.H, G.W,
-                              F.H, F.W, 0, s, nt, h->d_active));
+    SP_TRY(prolong_lv<T>(h, lv, 0, s));
     SP_TRY(smooth_lv<T>(h, lv, 1, false, s));
   }
   return 0;
@@ -440,8 +482,7 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
   auto launch = [&]() -> int {
     switch (which) {
       case 0:
-        return residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
-                           L.norms, h->C, L.H, L.W, 1.0, s, h->ntile, h->d_active);
+        return residual_lv<T>(h, 0, true, s);
       case 1:
         return oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
                                     L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
@@ -455,13 +496,11 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
       }
       default:
         if (!G) { set_error("single-level hierarchy"); return -2; }
-        return residual_restrict<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)G->r, h->C, L.H,
-                                    L.W, 1.0, s, h->ntile, h->d_active);
+        return residual_restrict_lv<T>(h, 0, s);
     }
   };
   // the ORAS local kernel needs current r/norms
-  SP_TRY((residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
-                      L.norms, h->C, L.H, L.W, 1.0, s, h->ntile, h->d_active)));
+  SP_TRY(residual_lv<T>(h, 0, true, s));
   SP_TRY(launch());  // warm-up
   cudaEvent_t e0, e1;
   SP_CUDA(cudaEventCreate(&e0));
@@ -476,8 +515,7 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
   cudaEventDestroy(e1);
   *ms = (double)t / reps;
   // leave r / norms consistent with u for the next solve
-  SP_TRY((residual<T>((const T*)L.u, (const T*)L.b, L.mask, (T*)L.r, L.partial, L.counter,
-                      L.norms, h->C, L.H, L.W, 1.0, s, h->ntile, h->d_active)));
+  SP_TRY(residual_lv<T>(h, 0, true, s));
   return 0;
 }
 
@@ -485,5 +523,10 @@ int hier_bench(Hier* h, int which, int reps, cudaStream_t s, double* ms, double*
   if (h->dtype == SP_F64) return bench_t<double>(h, which, reps, s, ms, bytes);
   return bench_t<float>(h, which, reps, s, ms, bytes);
 }
+
+// level operations shared with the row-strip solver (strips.cu)
+template int prolong_lv<float>(Hier*, int, int, cudaStream_t);
+template int smooth_lv<float>(Hier*, int, int, bool, cudaStream_t);
+template int vcycle_lv<float>(Hier*, int, bool, cudaStream_t);
 
 }  // namespace sp

@@ -32,6 +32,7 @@ struct Hier {
   double gamma = 0.0;
   bool has_values = false;
   bool use_graphs = true;
+  bool march = true;           // row-marching float sweeps (mgfast.cu)
   std::vector<Level> lv;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
@@ -59,6 +60,14 @@ int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
                int cycles, int max_cycles, cudaStream_t s, const int* active_in, int* iters,
                int* conv, SolveReport* rep);
 int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s);
+
+// level operations (solver.cu), used by the row-strip solver (strips.cu)
+template <typename T>
+int prolong_lv(Hier* h, int lv, int add, cudaStream_t s);
+template <typename T>
+int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s);
+template <typename T>
+int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s);
 
 // vec.cu: deterministic reductions (fixed CTA count per size)
 size_t red_partials();  // doubles needed in `partial` per reduced channel

@@ -1,0 +1,242 @@
+"""Row-strip partitioned inpainting solve.
+
+The north_star's layout for large images on several B200s: the finest
+``La`` levels of the multigrid-ORAS hierarchy (solver.py:200-372) are cut
+into P horizontal strips; each strip computes its owned rows widened by a
+48-row halo, exchanges halos every smoothing sweep and combines residual
+norms as partition-independent row-band partials (so every P gives the
+bit-identical solve); the coarse levels are agglomerated (replicated).  See
+csrc/strips.cu for the kernels and the transport.
+
+Transports:
+* one process holding all P strips on one GPU (``StripSolver(..., strips=P)``)
+  -- device copies; the single-GPU harness that proves P-independence;
+* one strip per rank over NCCL (``StripSolver.distributed(...)`` inside a
+  ``torch.distributed`` job, one process per GPU): point-to-point halo
+  sends/receives, an all-reduce of zero-padded band sums, broadcasts for the
+  agglomeration gather -- NVLink / NVSwitch on a B200 box.
+
+The plan (which rows each strip owns at each level) is pure host arithmetic
+(``strip_plan``) and is what the multi-process CPU tests exercise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import SolveReport as _CReport
+from ._lib import call, ptr, stream
+from .grid import Image, Mask
+from .solver import MultigridConfig, SolverReport, _enforce, _masked_rhs
+
+HALO = 48   # rows: >= ORAS block (32) + stencil (1), a multiple of BAND
+BAND = 16   # rows per residual-norm band (csrc/mgfast.cu MRB)
+
+
+def level_dims(height, width, cfg: MultigridConfig | None = None):
+    """Level sizes of the hierarchy (solver.py:238-243): halve (ceil) until
+    max(h, w) <= block, or `levels` levels."""
+    cfg = cfg or MultigridConfig()
+    dims, h, w = [], height, width
+    while True:
+        dims.append((h, w))
+        if cfg.levels > 0:
+            if len(dims) >= cfg.levels or max(h, w) <= 2:
+                break
+        elif max(h, w) <= cfg.oras.block:
+            break
+        h, w = (h + 1) // 2, (w + 1) // 2
+    return dims
+
+
+def _feasible(dims, P, La, halo):
+    if La >= len(dims):
+        return False
+    for lv in range(La):
+        h, w = dims[lv]
+        if w % 4 or w < 128:
+            return False
+    if La == 0 or P == 1:
+        return True
+    align = BAND << (La - 1)
+    H = dims[0][0]
+    bounds = [0] + [int(round(p * H / P / align)) * align for p in range(1, P)] + [H]
+    for lv in range(La):
+        hl = dims[lv][0]
+        for p in range(P):
+            a = bounds[p] >> lv
+            b = hl if p == P - 1 else bounds[p + 1] >> lv
+            if b - a < halo:
+                return False
+    return True
+
+
+def max_partitioned_levels(height, width, P, cfg=None, halo=HALO):
+    dims = level_dims(height, width, cfg)
+    best = 0
+    for La in range(1, len(dims)):
+        if _feasible(dims, P, La, halo):
+            best = La
+    return best
+
+
+def strip_plan(height, width, P, La=None, cfg=None, halo=HALO):
+    """Owned rows of every strip at every partitioned level.
+
+    Returns ``(La, o0, o1)`` with ``o0[lv][p]`` / ``o1[lv][p]``.  Strip
+    boundaries are multiples of ``16 * 2**(La-1)`` rows, so every partitioned
+    level cuts on a 16-row norm band; every strip owns >= ``halo`` rows at
+    every partitioned level (a halo then comes from the adjacent strip only).
+    """
+    dims = level_dims(height, width, cfg)
+    if La is None:
+        La = max_partitioned_levels(height, width, P, cfg, halo)
+    if La > 0 and not _feasible(dims, P, La, halo):
+        raise ValueError(f"{P} strips of {height}x{width} cannot partition {La} levels")
+    o0 = [[0] * P for _ in range(La)]
+    o1 = [[0] * P for _ in range(La)]
+    if La == 0:
+        return 0, o0, o1
+    align = BAND << (La - 1)
+    bounds = [0] + [int(round(p * height / P / align)) * align for p in range(1, P)] + [height]
+    for lv in range(La):
+        hl = dims[lv][0]
+        for p in range(P):
+            o0[lv][p] = bounds[p] >> lv
+            o1[lv][p] = hl if p == P - 1 else bounds[p + 1] >> lv
+    return La, o0, o1
+
+
+def halo_ranges(o0, o1, lv, p, level_height, halo=HALO):
+    """(recv, send) row ranges of strip p at level lv: recv = {q: (r0, r1)}
+    rows it takes from neighbour q, send = {q: (s0, s1)} rows q takes from
+    it (the same rule as csrc/strips.cu exchange())."""
+    P = len(o0[lv])
+    a, b = o0[lv][p], o1[lv][p]
+    e0, e1 = max(0, a - halo), min(level_height, b + halo)
+    recv, send = {}, {}
+    if p > 0:
+        recv[p - 1] = (e0, a)
+        send[p - 1] = (b_prev := o1[lv][p - 1], min(level_height, b_prev + halo))
+    if p < P - 1:
+        recv[p + 1] = (b, e1)
+        send[p + 1] = (max(0, o0[lv][p + 1] - halo), o0[lv][p + 1])
+    return recv, send
+
+
+class NcclComm:
+    """An NCCL communicator of the library (csrc/strips.cu), bootstrapped over
+    an initialised ``torch.distributed`` group (rank 0's unique id is
+    broadcast as a Python object)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            raise RuntimeError("NcclComm needs torch.distributed to be initialised")
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            call("sp_nccl_unique_id", uid)
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        self._c = ctypes.c_void_p()
+        call("sp_nccl_comm_create", ctypes.byref(self._c), uid, self.world, self.rank)
+
+    @property
+    def handle(self):
+        return self._c
+
+    def close(self):
+        if self._c:
+            _lib.load().sp_nccl_comm_destroy(self._c)
+            self._c = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class StripSolver:
+    """`InpaintSolver` semantics (solver.py:514-536) on a row-strip partition.
+
+    ``StripSolver(h, w, c, strips=P)``: all P strips in this process (one
+    GPU).  ``StripSolver.distributed(h, w, c)``: one strip per rank of the
+    current ``torch.distributed`` job, NCCL transport.  float32 only.
+    """
+
+    def __init__(self, height, width, channels, strips=1, cfg: MultigridConfig | None = None,
+                 La=None, _rank=None, _comm=None):
+        self.cfg = cfg if cfg is not None else MultigridConfig()
+        if self.cfg.dtype != "float32":
+            raise ValueError("the strip solver runs float32")
+        self.height, self.width, self.channels = height, width, channels
+        self.P = strips
+        self.La, o0, o1 = strip_plan(height, width, strips, La, self.cfg)
+        self.o0, self.o1 = o0, o1
+        flat0 = np.array([v for row in o0 for v in row] or [0], np.int32)
+        flat1 = np.array([v for row in o1 for v in row] or [0], np.int32)
+        nloc, first = (strips, 0) if _rank is None else (1, _rank)
+        self._comm = _comm
+        o = self.cfg.oras
+        self._g = ctypes.c_void_p()
+        call("sp_strip_create", ctypes.byref(self._g), channels, height, width, o.block,
+             o.overlap, self.cfg.levels, self.cfg.pre, self.cfg.post, float(o.alpha),
+             float(o.rho), strips, nloc, first, self.La, HALO, ptr(flat0), ptr(flat1),
+             _comm.handle if _comm is not None else None)
+        self._rep = _CReport()
+
+    @classmethod
+    def distributed(cls, height, width, channels, cfg=None, La=None):
+        import torch.distributed as dist
+        comm = NcclComm()
+        return cls(height, width, channels, strips=dist.get_world_size(), cfg=cfg, La=La,
+                   _rank=dist.get_rank(), _comm=comm)
+
+    def __del__(self):
+        g = getattr(self, "_g", None)
+        if g:
+            try:
+                _lib.load().sp_strip_destroy(g)
+            except Exception:
+                pass
+            self._g = None
+
+    def inpaint(self, f: Image, mask: Mask, init: Image | None = None, tol=-1.0, cycles=None):
+        """solver.py:485-511 on the strips: FMG cascade unless `init`; the
+        result interpolates f exactly on the mask (gathered on every rank)."""
+        cfg = self.cfg
+        tol = cfg.tol if tol == -1.0 else tol
+        if mask.count == 0:
+            raise ValueError("singular system: empty mask")
+        t0 = time.perf_counter()
+        f_t = f.tensor(torch.float32)
+        m_t = mask.tensor()
+        if tuple(f_t.shape) != (self.channels, self.height, self.width):
+            raise ValueError("image does not match the strip solver's geometry")
+        call("sp_strip_set_mask", self._g, ptr(m_t), ptr(f_t), stream())
+        bsym = _masked_rhs(f_t, m_t)
+        if init is not None:
+            u = init.tensor(torch.float32).clone()
+            mode = 1
+        else:
+            u = torch.empty_like(bsym)
+            mode = 2 if cfg.mode == "fmg" else 0
+        n_cycles = cfg.cycles if cycles is None else cycles
+        rep = self._rep
+        call("sp_strip_solve", self._g, ptr(bsym), ptr(u), mode,
+             -1.0 if tol is None else float(tol), int(n_cycles), int(cfg.max_cycles),
+             ctypes.byref(rep), stream())
+        _enforce(u, f_t, m_t)
+        out = SolverReport(iterations=rep.iterations, converged=bool(rep.converged),
+                           residuals=[rep.residuals[i] for i in range(rep.nres)])
+        out.seconds = time.perf_counter() - t0
+        return Image(u), out

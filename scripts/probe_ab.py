@@ -13,8 +13,9 @@ for dens in (0.05, 0.0024):
     mask = (np.random.default_rng(2).random((H, W)) < dens).astype(np.uint8)
     fi, mi = sp.Image(torch.from_numpy(f).cuda()), sp.Mask(torch.from_numpy(mask).cuda())
     u, rep = sp.inpaint(fi, mi)
-    for var in (0, 1, 0, 1):
+    for var, mv in ((0, 1), (0, 0), (1, 0), (0, 1)):
         lib.sp_oras_variant(var)
+        lib.sp_march_variant(mv)
         sp.solver._POOL.clear()
         cfg = sp.MultigridConfig(tol=None, cycles=10)
         u2, rep = sp.inpaint(fi, mi, cfg, init=u)
@@ -26,7 +27,8 @@ for dens in (0.05, 0.0024):
         sp.inpaint(fi, mi, sp.MultigridConfig(tol=None, cycles=1), init=u)
         torch.cuda.synchronize()
         call("sp_stats", 0, st)
-        print(f"dens {dens} variant {var}: {dt*1e2:.3f} ms/V-cycle; jobs={st[0]} "
+        print(f"dens {dens} oras {var} march {mv}: {dt*1e2:.3f} ms/V-cycle; jobs={st[0]} "
               f"mean iters={st[1]/max(1,st[0]):.2f} zero={st[2]/max(1,st[0]):.2%} max={st[3]}",
               flush=True)
     lib.sp_oras_variant(0)
+    lib.sp_march_variant(0)

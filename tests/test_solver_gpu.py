@@ -58,3 +58,30 @@ def test_empty_mask_raises():
     import paper_2401_06747_b200 as sp
     with pytest.raises(ValueError):
         sp.inpaint(sp.Image(np.ones((1, 8, 8))), sp.Mask(np.zeros((8, 8))))
+
+
+@pytest.mark.parametrize("shape", [(3, 301, 512), (1, 260, 384)])
+def test_row_marching_sweeps_match_per_pixel_kernels(shape):
+    """mgfast.cu's row-marching sweeps (wide float levels) use the reference
+    arithmetic of mg.cu's per-pixel kernels: the same V-cycles from the same
+    start agree to the last bits (only the norm summation order differs)."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 3)
+    mask = (np.random.default_rng(4).random((h, w)) < 0.05).astype(np.uint8)
+    outs = []
+    prev = lib.sp_march_variant(-1)
+    try:
+        for mv in (1, 0):
+            lib.sp_march_variant(mv)
+            _POOL.clear()
+            u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
+            outs.append(u.data)
+    finally:
+        lib.sp_march_variant(prev)
+        _POOL.clear()
+    rel = np.abs(outs[0] - outs[1]).max() / np.abs(outs[1]).max()
+    assert rel <= 1e-6
