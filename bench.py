@@ -13,6 +13,11 @@ the result (mask + stored values) read back inside the timed region.  Under
 torchrun each rank optimizes its own image (replicas: the path has no data
 exchange across images), so `scaling` is "weak".
 
+`strips` (BASELINE.json configs[4]) is the north_star's multi-GPU layout for
+one large image: a 7680x4320 RGB inpainting solve cut into one row strip
+per rank, halo exchange / norm all-reduce over NCCL (csrc/strips.cu),
+strong scaling, Mpixel-iterations/s.
+
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port under oracle/: C kernel table + numpy orchestration, bit-exact
 with the reference) on the host cores, on a bounded sample of the workload,
@@ -189,6 +194,54 @@ def _cpu_baseline_sample():
                       f"runtime slope, test_output.txt:35) to 3840x2160"}
 
 
+S5 = (4320, 7680, 3)  # BASELINE.json configs[4]: 8K RGB, row strips over the ranks
+
+
+def run_strips(world, rank, steps=3):
+    """configs[4]: a 7680x4320 RGB inpainting solve (cold FMG to the default
+    1e-4, 5% random mask) cut into one row strip per rank (csrc/strips.cu:
+    halo exchange + band-norm all-reduce + agglomeration broadcasts over
+    NCCL; at N = 1 a single strip).  Strong scaling: the image is fixed.
+    Time = CUDA events around each solve, max over ranks; Mpixel-iterations
+    = pixels x finest-level V-cycles."""
+    import numpy as np
+    import torch
+
+    import paper_2401_06747_b200 as sp
+    from oracle.oracle import synth  # input generator only
+    from paper_2401_06747_b200.strips import StripSolver
+
+    H5, W5, C5 = S5
+    f = torch.from_numpy(synth(H5, W5, C5, seed=0)).cuda()
+    m = torch.from_numpy((np.random.default_rng(5).random((H5, W5)) < 0.05)
+                         .astype(np.uint8)).cuda()
+    cfg = sp.MultigridConfig()
+    solver = (StripSolver.distributed(H5, W5, C5, cfg=cfg) if world > 1
+              else StripSolver(H5, W5, C5, strips=1, cfg=cfg))
+    fi, mi = sp.Image(f), sp.Mask(m)
+    u, rep = solver.inpaint(fi, mi)  # warm-up (allocations, NCCL channels)
+    torch.cuda.synchronize()
+    times, cycles = [], rep.iterations
+    stream = torch.cuda.current_stream()
+    for _ in range(steps):
+        _barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        u, rep = solver.inpaint(fi, mi)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(_max_over_ranks(e0.elapsed_time(e1), world))
+    ms = sorted(times)[len(times) // 2]
+    # the gathered solution is the same on every rank
+    chk = float(u.tensor()[:, ::97, ::89].double().sum())
+    return {"workload": f"{W5}x{H5} RGB inpaint (cold FMG to 1e-4, 5% random mask)",
+            "n_strips": world, "partitioned_levels": solver.La, "halo_rows": 48,
+            "ms_per_solve": ms, "vcycles": int(cycles),
+            "mpix_iter_per_s": H5 * W5 * cycles / (ms * 1e-3) / 1e6,
+            "converged": bool(rep.converged), "checksum": chk,
+            "scaling": "strong (fixed image, one strip per GPU)"}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -255,7 +308,7 @@ def run_ours(args):
     bsym = _masked_rhs(f_dev.float().contiguous(), mask.tensor())
     hier.solve_sym(bsym, tol=1e-4, cascade=True)
     import ctypes
-    names = {0: "k4_residual (sym_residual sweep)", 1: "k_oras_local32 (ORAS local CG)",
+    names = {0: "k4_residual (sym_residual sweep)", 1: "k_oras_rows (ORAS local CG)",
              2: "k_oras_blend", 3: "k4_residual_restrict"}
     for which in (0, 1, 2, 3):
         t_ms, nbytes = ctypes.c_double(), ctypes.c_double()
@@ -274,6 +327,8 @@ def run_ours(args):
     stencil_roofline = {"bound": "hbm", "kernel": sten, "achieved": kern[sten]["gbs"],
                         "peak": peak, "unit": "GB/s", "frac": kern[sten]["frac"]}
 
+    strips = None if args.no_strips else run_strips(world, rank)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline_sample()
@@ -291,6 +346,7 @@ def run_ours(args):
                        "final_mse": st.mse, "dd_mse": hist[-1][2], "mask_count": mask.count,
                        "images_per_s": world / (ms / 1e3)},
             "roofline": roof, "stencil_roofline": stencil_roofline, "kernels": kern,
+            "strips": strips,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -311,6 +367,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strips", action="store_true",
+                    help="skip the 8K row-strip solve (configs[4])")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)

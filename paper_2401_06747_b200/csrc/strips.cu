@@ -468,7 +468,7 @@ int strip_create(StripGroup** out, int C, int H, int W, const HierCfg& cfg, int 
   g->bands.assign(nloc, std::vector<double*>(La, nullptr));
   for (int lv = 0; lv < La; ++lv) {
     const Level& L = g->h[0]->lv[lv];
-    if (!march_ok(L.H, L.W, L.npart)) {
+    if (L.W % 4 != 0 || L.W < 128) {  // row-marching sweeps (band-norm mode)
       set_error("partitioned level %d (%d x %d) needs W %% 4 == 0 and W >= 128", lv, L.H, L.W);
       delete g;
       return -2;
