@@ -270,11 +270,17 @@ int sp_stats(int enable, uint64_t* out_h);
 /* float ORAS kernel for blocks <= 32x32: 0 = register-resident 4-warp job
  * kernel (default), 1 = 256-thread CTA kernel; v < 0 query */
 int sp_oras_variant(int v);
-/* Default sweep kernels of hierarchies created afterwards: 1 = row-marching
- * float kernels on wide float levels (mgfast.cu), 0 = the reference-exact
- * double-accumulating kernels everywhere; v < 0 queries.  A/B measurement
- * aid, no reference counterpart. */
+/* Default sweep kernels of hierarchies created afterwards (all bit-identical
+ * per element): 2 = TMA-staged residual sweeps on wide float levels
+ * (mgtma.cu, default), 1 = row-marching register kernels (mgfast.cu), 0 =
+ * the per-pixel kernels everywhere; v < 0 queries.  A/B measurement aid, no
+ * reference counterpart. */
 int sp_march_variant(int v);
+/* residual r = b~ - A~ u and per-plane sum r^2 of level lv's current iterate
+ * (after a solve), computed by the hierarchy's sweep kernel, into device
+ * buffers r_out [ntile][C][h][w], norms_out [ntile][C] (kernel-variant
+ * checks; the residual of solver.py:256-258) */
+int sp_hier_residual(void* hier, int lv, void* r_out, double* norms_out, void* stream);
 /* kernels launched by the library since the last reset */
 long long sp_launch_count(int reset);
 /* CUDA-event timing of a finest-level kernel (0 residual, 1 ORAS local CG,

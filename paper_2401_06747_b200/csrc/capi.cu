@@ -566,6 +566,7 @@ namespace sp {
 static std::atomic<long long> g_launches{0};
 void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int hier_bench(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes);
+int hier_residual_out(Hier* h, int lv, void* r_out, double* norms_out, cudaStream_t s);
 }  // namespace sp
 
 extern "C" {
@@ -581,5 +582,11 @@ long long sp_launch_count(int reset) {
 // residual+restriction) and its algorithmic bytes per launch
 int sp_hier_bench(void* h, int which, int reps, double* ms_h, double* bytes_h, void* s) {
   return sp::hier_bench((sp::Hier*)h, which, reps, (cudaStream_t)s, ms_h, bytes_h);
+}
+
+// residual (r, per-plane sum r^2) of level lv's current iterate with the
+// hierarchy's sweep kernel, into device buffers
+int sp_hier_residual(void* h, int lv, void* r_out, double* norms_out, void* s) {
+  return sp::hier_residual_out((sp::Hier*)h, lv, r_out, norms_out, (cudaStream_t)s);
 }
 }  // extern "C"

@@ -53,6 +53,14 @@ int prolong_march(const float* e, float* u, const float* b, const uint8_t* m, in
                   int cww, int H, int W, int add, cudaStream_t s, int ntile,
                   const int* active);
 
+// ---- mgtma.cu: TMA-staged float sweeps (W % 16 == 0, W >= 128, inv_h2 = 1) -----
+bool tma_ok(int H, int W, size_t npart);
+int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
+              unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
+              const int* active);
+int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
+                       int H, int W, cudaStream_t s, int ntile, const int* active);
+
 // ---- vec.cu ------------------------------------------------------------------
 template <typename T>
 int chan_reduce(int mode, const T* x, const T* y, const double* z, size_t n, int C,

@@ -1,0 +1,336 @@
+// mgtma.cu -- TMA-staged stencil sweeps of the multigrid hierarchy (sm_100a).
+//
+// The two HBM-bound sweeps of every V-cycle on the wide float levels:
+//   residual           r = b~ - A~ u, per-plane sum r^2     (numba_impl.py:147-158)
+//   residual+restrict  r_H = restrict(b~ - A~ u)          (solver.py:289-291)
+//
+// Data movement: a CTA owns a 128-column x 64-row tile of one plane and
+// streams it in 8-row chunks through a 4-stage shared-memory ring filled by
+// the Tensor Memory Accelerator (cp.async.bulk.tensor.3d, one elected
+// thread, completion on an mbarrier with expect_tx).  Each chunk brings the
+// u rows y-1 .. y+8 with a 4-column halo (136 x 10 floats), the mask rows
+// with a 16-byte halo (160 x 10 bytes) and the b rows (128 x 8 floats); the
+// tensor maps are 3-D ([plane][H][W]) so the image border is the TMA
+// out-of-bounds zero fill -- no edge special cases in the load path.  While
+// the 8 warps compute chunk k, chunks k+1..k+3 are in flight: the memory
+// level parallelism comes from the TMA engine, not from registers.
+//
+// Arithmetic is the reference's bit for bit (the same as mg.cu's per-pixel
+// kernels): the neighbour sum in double in the order up, down, left, right,
+// (d u - sum) rounded once to float, r = b - A u in float; the restriction
+// averages ((a + b) + c) + d in double.  Norms: per-thread float sums, then
+// double warp / CTA trees in fixed order and the last CTA of a plane adds
+// the CTA partials in index order (deterministic).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr int TC = 128;              // tile columns
+constexpr int TR = 64;               // tile rows
+constexpr int CR = 8;                // rows per chunk (= warps)
+constexpr int NCH = TR / CR;         // chunks per tile
+constexpr int NS = 4;                // pipeline stages
+constexpr int UW = TC + 8;           // u row: 4-column halo each side
+constexpr int MW = TC + 32;          // mask row: 16-byte halo each side (TMA
+                                     // x coordinates must be 16-byte aligned)
+constexpr int U_BYTES = UW * (CR + 2) * 4;
+constexpr int M_BYTES = MW * (CR + 2);
+constexpr int B_BYTES = TC * CR * 4;
+constexpr int U_OFF = 0;
+constexpr int M_OFF = (U_BYTES + 127) / 128 * 128;
+constexpr int B_OFF = M_OFF + (M_BYTES + 127) / 128 * 128;
+constexpr int STAGE = B_OFF + (B_BYTES + 127) / 128 * 128;
+constexpr int SMEM = NS * STAGE + 128;
+constexpr int TX_BYTES = U_BYTES + M_BYTES + B_BYTES;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y,
+                                            int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Maps {
+  CUtensorMap u, b, m;
+};
+
+// issue the three TMA loads of chunk `ck` of the tile into stage `st`
+__device__ __forceinline__ void issue_chunk(const Maps& mp, unsigned char* sm, uint64_t* bars,
+                                            int st, int x0, int ychunk, int z, int tile) {
+  unsigned char* base = sm + st * STAGE;
+  mbar_expect_tx(&bars[st], TX_BYTES);
+  tma_load_3d(base + U_OFF, &mp.u, x0 - 4, ychunk - 1, z, &bars[st]);
+  tma_load_3d(base + M_OFF, &mp.m, x0 - 16, ychunk - 1, tile, &bars[st]);
+  tma_load_3d(base + B_OFF, &mp.b, x0, ychunk, z, &bars[st]);
+}
+
+__device__ __forceinline__ float f4g(const float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// r = b - A~ u for the lane's quad of chunk row `w` (stage buffers)
+__device__ __forceinline__ float4 resid_smem(const float* us, const unsigned char* ms,
+                                             const float* bs, int w, int lane, int y, int H,
+                                             int xq, int W) {
+  const float* uc = us + (w + 1) * UW + 4 + 4 * lane;
+  const float4 c = *reinterpret_cast<const float4*>(uc);
+  const float4 up = *reinterpret_cast<const float4*>(uc - UW);
+  const float4 dn = *reinterpret_cast<const float4*>(uc + UW);
+  const float ul = uc[-1], ur = uc[4];
+  const unsigned char* mc = ms + (w + 1) * MW + 16 + 4 * lane;
+  const uint32_t m = *reinterpret_cast<const uint32_t*>(mc);
+  const uint32_t mu = *reinterpret_cast<const uint32_t*>(mc - MW);
+  const uint32_t md = *reinterpret_cast<const uint32_t*>(mc + MW);
+  const bool ml = mc[-1] != 0, mr = mc[4] != 0;
+  const float4 bb = *reinterpret_cast<const float4*>(bs + w * TC + 4 * lane);
+  const bool hu = y > 0, hd = y < H - 1, hl = xq > 0, hr = xq + 4 < W;
+  // q: the value as it enters a neighbour's sum (0 where masked)
+  auto q = [](float v, uint32_t mw, int i) { return ((mw >> (8 * i)) & 0xFFu) ? 0.0 : (double)v; };
+  const double dv = (hu ? 1.0 : 0.0) + (hd ? 1.0 : 0.0);  // vertical neighbours
+  float out[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float uv = f4g(c, i);
+    float ax;
+    if ((m >> (8 * i)) & 0xFFu) {
+      ax = uv;
+    } else {
+      // absent neighbours (outside the image) are TMA zero fill: +0.0 exactly
+      const double qu = q(f4g(up, i), mu, i), qd = q(f4g(dn, i), md, i);
+      const double ql = i > 0 ? q(f4g(c, i - 1), m, i - 1) : (ml ? 0.0 : (double)ul);
+      const double qr = i < 3 ? q(f4g(c, i + 1), m, i + 1) : (mr ? 0.0 : (double)ur);
+      const double a = ((qu + qd) + ql) + qr;
+      const double d = dv + (i > 0 || hl ? 1.0 : 0.0) + (i < 3 || hr ? 1.0 : 0.0);
+      ax = (float)(d * (double)uv - a);
+    }
+    out[i] = f4g(bb, i) - ax;
+  }
+  return make_float4(out[0], out[1], out[2], out[3]);
+}
+
+// MODE 0: residual (+ norms); MODE 1: residual + 2x2 restriction
+template <int MODE, bool NORMS>
+__global__ void __launch_bounds__(CR * 32) k_resid_tma(
+    const __grid_constant__ Maps mp, float* __restrict__ r, double* __restrict__ partial,
+    unsigned* __restrict__ counter, double* __restrict__ norms, float* __restrict__ rcoarse,
+    int C, int H, int W, const int* __restrict__ active) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
+  __shared__ uint64_t bars[NS];
+  __shared__ double wsum[CR];
+  __shared__ bool am_last;
+  __shared__ float rrow[MODE == 1 ? CR : 1][MODE == 1 ? TC + 4 : 1];
+  const int z = blockIdx.z, tile = z / C;
+  if (active && !active[tile]) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * TC, y0 = blockIdx.y * TR;
+  const int nck = min(NCH, (H - y0 + CR - 1) / CR);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NS && k < nck; ++k) issue_chunk(mp, sm, bars, k, x0, y0 + k * CR, z, tile);
+  const int xq = x0 + 4 * lane;
+  const size_t plane = (size_t)H * W;
+  float sq = 0.0f;
+  for (int k = 0; k < nck; ++k) {
+    const int st = k % NS;
+    mbar_wait(&bars[st], (uint32_t)((k / NS) & 1));
+    const unsigned char* base = sm + st * STAGE;
+    const int y = y0 + k * CR + w;
+    float4 rr = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (y < H && xq < W) {
+      rr = resid_smem((const float*)(base + U_OFF), base + M_OFF, (const float*)(base + B_OFF),
+                      w, lane, y, H, xq, W);
+      if (MODE == 0) {
+        *reinterpret_cast<float4*>(r + (size_t)z * plane + (size_t)y * W + xq) = rr;
+        if (NORMS) {
+          sq = __fmaf_rn(rr.x, rr.x, sq);
+          sq = __fmaf_rn(rr.y, rr.y, sq);
+          sq = __fmaf_rn(rr.z, rr.z, sq);
+          sq = __fmaf_rn(rr.w, rr.w, sq);
+        }
+      }
+    }
+    if (MODE == 1) *reinterpret_cast<float4*>(&rrow[w][4 * lane]) = rr;
+    __syncthreads();  // stage st fully consumed (and the chunk's r rows staged)
+    if (threadIdx.x == 0 && k + NS < nck)
+      issue_chunk(mp, sm, bars, st, x0, y0 + (k + NS) * CR, z, tile);
+    if (MODE == 1) {
+      // restrict_values (numba_impl.py:266-284): warps 0..3 combine the row
+      // pairs of the chunk, 2 coarse pixels per lane, ((a + b) + c) + d
+      if (w < CR / 2) {
+        const int yf = y0 + k * CR + 2 * w;
+        if (yf < H && xq < W) {
+          const float4 a = *reinterpret_cast<const float4*>(&rrow[2 * w][4 * lane]);
+          float2 o;
+          if (yf + 1 < H) {
+            const float4 b2 = *reinterpret_cast<const float4*>(&rrow[2 * w + 1][4 * lane]);
+            o.x = (float)(((((double)a.x + (double)a.y) + (double)b2.x) + (double)b2.y) / 4.0);
+            o.y = (float)(((((double)a.z + (double)a.w) + (double)b2.z) + (double)b2.w) / 4.0);
+          } else {
+            o.x = (float)(((double)a.x + (double)a.y) / 2.0);
+            o.y = (float)(((double)a.z + (double)a.w) / 2.0);
+          }
+          const int cw = W / 2, chh = (H + 1) / 2;
+          *reinterpret_cast<float2*>(rcoarse + (size_t)z * chh * cw + (size_t)(yf >> 1) * cw +
+                                     (xq >> 1)) = o;
+        }
+      }
+      __syncthreads();  // rrow reused by the next chunk
+    }
+  }
+  if (MODE != 0 || !NORMS) return;
+  double sqd = (double)sq;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sqd += __shfl_xor_sync(0xFFFFFFFFu, sqd, o);
+  if (lane == 0) wsum[w] = sqd;
+  __syncthreads();
+  const unsigned ncta = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < CR; ++q) s += wsum[q];
+    if (ncta == 1) {
+      norms[z] = s;
+      am_last = false;
+    } else {
+      partial[(size_t)z * ncta + cta] = s;
+      __threadfence();
+      am_last = atomicAdd(counter + z, 1u) == ncta - 1;
+    }
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned i = threadIdx.x; i < ncta; i += CR * 32)
+    t += ((volatile double*)partial)[(size_t)z * ncta + i];
+  t = cta_sum<CR * 32>(t, wsum);
+  if (threadIdx.x == 0) {
+    norms[z] = t;
+    counter[z] = 0u;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, size_t esize, int W,
+              int H, int nz, int box_w, int box_h) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)W * esize, (cuuint64_t)W * H * esize};
+  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_maps(Maps& mp, const float* u, const float* b, const uint8_t* m, int C, int H, int W,
+               int ntile) {
+  const int nz = C * ntile;
+  return make_map(&mp.u, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, UW, CR + 2) &&
+         make_map(&mp.b, b, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, TC, CR) &&
+         make_map(&mp.m, m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, W, H, ntile, MW, CR + 2);
+}
+
+template <int MODE, bool NORMS>
+int launch(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
+           unsigned* counter, double* norms, float* rc, int C, int H, int W, cudaStream_t s,
+           int ntile, const int* active) {
+  Maps mp;
+  if (!make_maps(mp, u, b, m, C, H, W, ntile)) {
+    set_error("cuTensorMapEncodeTiled failed (%d x %d x %d)", C * ntile, H, W);
+    return -1;
+  }
+  static bool attr = false;
+  if (!attr) {
+    SP_CUDA(cudaFuncSetAttribute(k_resid_tma<MODE, NORMS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr = true;
+  }
+  dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)((long)C * ntile));
+  k_resid_tma<MODE, NORMS><<<grid, CR * 32, SMEM, s>>>(mp, r, partial, counter, norms, rc, C, H,
+                                                       W, active);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace
+
+// TMA path: float levels with W % 16 == 0 (16-byte mask row pitch for the
+// tensor map), W >= 128, 16-byte aligned buffers, and few enough CTAs per
+// plane for the partial-sum slots
+bool tma_ok(int H, int W, size_t npart) {
+  if (W % 16 != 0 || W < TC || !encode_fn()) return false;
+  return (size_t)cdiv(W, TC) * cdiv(H, TR) <= npart;
+}
+
+int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
+              unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
+              const int* active) {
+  if (norms)
+    return launch<0, true>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
+                           active);
+  return launch<0, false>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
+                          active);
+}
+
+int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
+                       int H, int W, cudaStream_t s, int ntile, const int* active) {
+  return launch<1, false>(u, b, m, nullptr, nullptr, nullptr, nullptr, rc, C, H, W, s, ntile,
+                          active);
+}
+
+}  // namespace sp

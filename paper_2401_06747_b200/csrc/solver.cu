@@ -23,12 +23,12 @@
 
 namespace sp {
 
-// default for new hierarchies: row-marching sweeps on the wide float levels
-// (1) or the per-pixel kernels everywhere (0, measured faster on B200 for
-// the single-image solve: profiles/oras_ab_r01*.txt); sp_march_variant.
-// The row-strip solver always uses the row-marching kernels.
+// sweep kernels of new hierarchies (sp_march_variant): 2 = TMA-staged
+// residual sweeps (default), 1 = row-marching register kernels, 0 = the
+// per-pixel kernels everywhere.  The row-strip solver always uses the
+// row-marching kernels (their band-norm mode).
 int march_default(int v) {
-  static int on = 0;
+  static int on = 2;
   if (v >= 0) on = v;
   return on;
 }
@@ -89,7 +89,7 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     return -2;
   }
   Hier* h = new Hier();
-  h->march = march_default(-1) != 0;
+  h->sweep = march_default(-1);
   h->dtype = dtype;
   h->C = C;
   h->ntile = ntile;
@@ -212,17 +212,30 @@ int hier_set_mask(Hier* h, const uint8_t* mask, const void* values, cudaStream_t
 
 // ---- V-cycle ----------------------------------------------------------------
 
-// the level sweeps: row-marching float kernels on wide float levels
-// (mgfast.cu), the reference-exact double-accumulating kernels otherwise
+// the level sweeps on wide float levels: TMA-staged kernels (mgtma.cu,
+// sweep variant 2, default), row-marching register kernels (mgfast.cu, 1),
+// or the per-pixel reference-exact kernels (mg.cu, 0 -- also every narrow or
+// double level).  All three are bit-identical per element.
+template <typename T>
+static bool aligned_level(const Level& L) {
+  return (((uintptr_t)L.u | (uintptr_t)L.b | (uintptr_t)L.r | (uintptr_t)L.mask) & 15u) == 0;
+}
+template <typename T>
+static bool use_tma(const Hier* h, const Level& L) {
+  return sizeof(T) == 4 && h->sweep == 2 && tma_ok(L.H, L.W, L.npart) && aligned_level<T>(L);
+}
 template <typename T>
 static bool use_march(const Hier* h, const Level& L) {
-  return sizeof(T) == 4 && h->march && march_ok(L.H, L.W, L.npart) &&
-         (((uintptr_t)L.u | (uintptr_t)L.b | (uintptr_t)L.r | (uintptr_t)L.mask) & 15u) == 0;
+  return sizeof(T) == 4 && h->sweep == 1 && march_ok(L.H, L.W, L.npart) && aligned_level<T>(L);
 }
 
 template <typename T>
 static int residual_lv(Hier* h, int lv, bool with_norms, cudaStream_t s) {
   Level& L = h->lv[lv];
+  if (use_tma<T>(h, L))
+    return resid_tma((const float*)L.u, (const float*)L.b, L.mask, (float*)L.r, L.partial,
+                     L.counter, with_norms ? L.norms : nullptr, h->C, L.H, L.W, s, h->ntile,
+                     h->d_active);
   if (use_march<T>(h, L))
     return resid_march((const float*)L.u, (const float*)L.b, L.mask, (float*)L.r, L.partial,
                        L.counter, with_norms ? L.norms : nullptr, h->C, L.H, L.W, s, h->ntile,
@@ -236,6 +249,9 @@ template <typename T>
 static int residual_restrict_lv(Hier* h, int lv, cudaStream_t s) {
   Level& F = h->lv[lv];
   Level& G = h->lv[lv + 1];
+  if (use_tma<T>(h, F))
+    return resid_restrict_tma((const float*)F.u, (const float*)F.b, F.mask, (float*)G.r, h->C,
+                              F.H, F.W, s, h->ntile, h->d_active);
   if (use_march<T>(h, F))
     return resid_restrict_march((const float*)F.u, (const float*)F.b, F.mask, (float*)G.r,
                                 h->C, F.H, F.W, s, h->ntile, h->d_active);
@@ -517,6 +533,28 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
   // leave r / norms consistent with u for the next solve
   SP_TRY(residual_lv<T>(h, 0, true, s));
   return 0;
+}
+
+// residual of level lv's current state (u, b) into r_out / norms_out, with
+// the sweep kernel the hierarchy uses (kernel-variant tests)
+template <typename T>
+static int residual_out_t(Hier* h, int lv, void* r_out, double* norms_out, cudaStream_t s) {
+  if (lv < 0 || lv >= (int)h->lv.size()) { set_error("no level %d", lv); return -2; }
+  Level& L = h->lv[lv];
+  for (int t = 0; t < h->ntile; ++t) h->h_active[t] = 1;
+  SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * h->ntile,
+                          cudaMemcpyHostToDevice, s));
+  SP_TRY(residual_lv<T>(h, lv, true, s));
+  const size_t n = (size_t)h->C * L.H * L.W * h->ntile;
+  SP_CUDA(cudaMemcpyAsync(r_out, L.r, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  SP_CUDA(cudaMemcpyAsync(norms_out, L.norms, sizeof(double) * h->C * h->ntile,
+                          cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int hier_residual_out(Hier* h, int lv, void* r_out, double* norms_out, cudaStream_t s) {
+  if (h->dtype == SP_F64) return residual_out_t<double>(h, lv, r_out, norms_out, s);
+  return residual_out_t<float>(h, lv, r_out, norms_out, s);
 }
 
 int hier_bench(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes) {

@@ -32,7 +32,7 @@ struct Hier {
   double gamma = 0.0;
   bool has_values = false;
   bool use_graphs = true;
-  bool march = true;           // row-marching float sweeps (mgfast.cu)
+  int sweep = 2;               // 2 TMA, 1 row-marching, 0 per-pixel (solver.cu)
   std::vector<Level> lv;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cap_stream = nullptr;

@@ -85,7 +85,9 @@ class Image:
         if self._dev is not None:
             t = self._dev
             if not t.is_cuda:
-                t = t.to(_lib.device())
+                # host (e.g. pinned) tensor: upload once, keep the device copy
+                t = t.to(_lib.device(), non_blocking=t.is_pinned())
+                self._dev = t
         else:
             t = _lib.to_dev(self._host)
         if dtype is not None and t.dtype != dtype:

@@ -61,10 +61,11 @@ def test_empty_mask_raises():
 
 
 @pytest.mark.parametrize("shape", [(3, 301, 512), (1, 260, 384)])
-def test_row_marching_sweeps_match_per_pixel_kernels(shape):
-    """mgfast.cu's row-marching sweeps (wide float levels) use the reference
-    arithmetic of mg.cu's per-pixel kernels: the same V-cycles from the same
-    start agree to the last bits (only the norm summation order differs)."""
+def test_sweep_kernel_variants_agree(shape):
+    """The TMA-staged (mgtma.cu) and row-marching (mgfast.cu) sweeps of the
+    wide float levels use the reference arithmetic of mg.cu's per-pixel
+    kernels: the same V-cycles from the same start agree to the last bits
+    (only the norm summation order differs)."""
     import paper_2401_06747_b200 as sp
     from paper_2401_06747_b200 import _lib
     from paper_2401_06747_b200.solver import _POOL
@@ -75,7 +76,7 @@ def test_row_marching_sweeps_match_per_pixel_kernels(shape):
     outs = []
     prev = lib.sp_march_variant(-1)
     try:
-        for mv in (1, 0):
+        for mv in (2, 1, 0):
             lib.sp_march_variant(mv)
             _POOL.clear()
             u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
@@ -83,5 +84,43 @@ def test_row_marching_sweeps_match_per_pixel_kernels(shape):
     finally:
         lib.sp_march_variant(prev)
         _POOL.clear()
-    rel = np.abs(outs[0] - outs[1]).max() / np.abs(outs[1]).max()
-    assert rel <= 1e-6
+    for o in outs[:2]:
+        rel = np.abs(o - outs[2]).max() / np.abs(outs[2]).max()
+        assert rel <= 1e-6
+
+
+@pytest.mark.parametrize("shape", [(1, 128, 128), (1, 200, 256), (3, 130, 384), (3, 67, 512)])
+def test_sweep_kernel_residuals_bit_identical(shape):
+    """The residual r = b~ - A~ u of one iterate computed by the TMA-staged,
+    row-marching and per-pixel sweep kernels: bit-identical (numba_impl.py
+    147-158 arithmetic in all three); norms equal to summation order."""
+    import torch
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import GridHierarchy, _POOL, _masked_rhs
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 0)
+    mask = (np.random.default_rng(7).random((h, w)) < 0.05).astype(np.uint8)
+    ft = torch.from_numpy(f).float().cuda()
+    mt = torch.from_numpy(mask).cuda()
+    u0 = ft + torch.from_numpy(np.random.default_rng(8).standard_normal(f.shape)).float().cuda()
+    bsym = _masked_rhs(ft, mt)
+    prev = lib.sp_march_variant(-1)
+    res = {}
+    try:
+        for v in (0, 1, 2):
+            lib.sp_march_variant(v)
+            _POOL.clear()
+            hier = GridHierarchy.build(sp.Mask(mt), sp.Image(ft), sp.MultigridConfig())
+            hier.solve_sym(bsym, init=u0, tol=1e9)      # u = u0 (enforced), no cycle
+            r = torch.empty_like(ft)
+            nrm = torch.empty(c, dtype=torch.float64, device="cuda")
+            _lib.call("sp_hier_residual", hier._h, 0, _lib.ptr(r), _lib.ptr(nrm), _lib.stream())
+            res[v] = (r.cpu().numpy(), nrm.cpu().numpy())
+    finally:
+        lib.sp_march_variant(prev)
+        _POOL.clear()
+    for v in (1, 2):
+        assert np.array_equal(res[v][0], res[0][0])
+        assert np.allclose(res[v][1], res[0][1], rtol=1e-6, atol=0)
