@@ -268,7 +268,8 @@ int sp_ct_apply_tiles(int dtype, const void* w, const uint8_t* mask, void* out, 
  * enable 1 = reset+start, 0 = reset+stop, -1 = read only */
 int sp_stats(int enable, uint64_t* out_h);
 /* float ORAS kernel for blocks <= 32x32: 0 = register-resident 4-warp job
- * kernel (default), 1 = 256-thread CTA kernel; v < 0 query */
+ * kernel, one job per CTA (default), 1 = 256-thread CTA kernel, 3 = the
+ * 4-warp kernel persistent with cp.async prefetch; v < 0 query */
 int sp_oras_variant(int v);
 /* Default sweep kernels of hierarchies created afterwards (all bit-identical
  * per element): 2 = TMA-staged residual sweeps on wide float levels

@@ -60,6 +60,9 @@ int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double
               const int* active);
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
                        int H, int W, cudaStream_t s, int ntile, const int* active);
+bool tma_prolong_ok(int H, int W);
+int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int C, int chh,
+                int cww, int H, int W, int add, cudaStream_t s, int ntile, const int* active);
 
 // ---- vec.cu ------------------------------------------------------------------
 template <typename T>

@@ -307,11 +307,124 @@ int launch(const float* u, const float* b, const uint8_t* m, float* r, double* p
   return 0;
 }
 
+// ---- prolongation + enforce (solver.py:294-296, numba_impl.py:316-348) -------
+// u = (add ? u : 0) + P e on unmasked pixels, u = b~ on masked pixels.  A
+// chunk is 8 fine rows x 128 columns: TMA brings the u rows (add only), the
+// mask rows and the 6 x 72 coarse rows / columns the bilinear stencil of
+// the chunk touches; b~ is read directly, and only for quads holding a
+// stored pixel (5% density).  The interpolation is the reference's double
+// expression with its clamped, cell-centred indices, one rounding.
+constexpr int EW = TC / 2 + 8;     // coarse columns per chunk (4-column halo)
+constexpr int EH = CR / 2 + 2;     // coarse rows per chunk
+constexpr int PU_BYTES = TC * CR * 4;
+constexpr int PM_BYTES = TC * CR;
+constexpr int PE_BYTES = EW * EH * 4;
+constexpr int PU_OFF = 0;
+constexpr int PM_OFF = PU_BYTES;
+constexpr int PE_OFF = PM_OFF + (PM_BYTES + 127) / 128 * 128;
+constexpr int PSTAGE = PE_OFF + (PE_BYTES + 127) / 128 * 128;
+constexpr int PSMEM = NS * PSTAGE + 128;
+
+struct PMaps {
+  CUtensorMap u, m, e;
+};
+
+__device__ __forceinline__ void paxis_d(int y, int n, int& y0, int& y1, double& wy) {
+  double fy = ((double)y + 0.5) / 2.0 - 0.5;
+  y0 = (int)floor(fy);
+  wy = fy - (double)y0;
+  if (y0 < 0) { y0 = 0; wy = 0.0; }
+  if (y0 > n - 1) { y0 = n - 1; wy = 0.0; }
+  y1 = min(y0 + 1, n - 1);
+}
+
+template <bool ADD>
+__global__ void __launch_bounds__(CR * 32) k_prolong_tma(
+    const __grid_constant__ PMaps mp, float* __restrict__ u, const float* __restrict__ b,
+    const uint8_t* __restrict__ m, int C, int chh, int cww, int H, int W,
+    const int* __restrict__ active) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
+  __shared__ uint64_t bars[NS];
+  const int z = blockIdx.z, tile = z / C;
+  if (active && !active[tile]) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * TC, y0 = blockIdx.y * TR;
+  const int nck = min(NCH, (H - y0 + CR - 1) / CR);
+  const uint32_t tx = (ADD ? PU_BYTES : 0) + PM_BYTES + PE_BYTES;
+  auto issue = [&](int st, int yc) {
+    unsigned char* base = sm + st * PSTAGE;
+    mbar_expect_tx(&bars[st], tx);
+    if (ADD) tma_load_3d(base + PU_OFF, &mp.u, x0, yc, z, &bars[st]);
+    tma_load_3d(base + PM_OFF, &mp.m, x0, yc, tile, &bars[st]);
+    tma_load_3d(base + PE_OFF, &mp.e, x0 / 2 - 4, yc / 2 - 1, z, &bars[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NS && k < nck; ++k) issue(k, y0 + k * CR);
+  const int xq = x0 + 4 * lane;
+  const size_t plane = (size_t)H * W;
+  // x interpolation of the lane's 4 pixels (chunk-independent)
+  int xa[4], xb[4];
+  double wx[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    paxis_d(xq + i, cww, xa[i], xb[i], wx[i]);
+    xa[i] -= x0 / 2 - 4;
+    xb[i] -= x0 / 2 - 4;
+  }
+  for (int k = 0; k < nck; ++k) {
+    const int st = k % NS;
+    mbar_wait(&bars[st], (uint32_t)((k / NS) & 1));
+    const unsigned char* base = sm + st * PSTAGE;
+    const int yc = y0 + k * CR, y = yc + w;
+    if (y < H && xq < W) {
+      const uint32_t mw = *reinterpret_cast<const uint32_t*>(base + PM_OFF + w * TC + 4 * lane);
+      const float4 uu = ADD ? *reinterpret_cast<const float4*>(base + PU_OFF + (w * TC + 4 * lane) * 4)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 bb = mw ? *reinterpret_cast<const float4*>(b + (size_t)z * plane +
+                                                               (size_t)y * W + xq)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      int ya, yb;
+      double wy;
+      paxis_d(y, chh, ya, yb, wy);
+      const float* es = (const float*)(base + PE_OFF);
+      const float* e0 = es + (ya - (yc / 2 - 1)) * EW;
+      const float* e1 = es + (yb - (yc / 2 - 1)) * EW;
+      float o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if ((mw >> (8 * i)) & 0xFFu) {
+          o[i] = f4g(bb, i);
+          continue;
+        }
+        const double v = (1.0 - wy) * ((1.0 - wx[i]) * (double)e0[xa[i]] + wx[i] * (double)e0[xb[i]]) +
+                         wy * ((1.0 - wx[i]) * (double)e1[xa[i]] + wx[i] * (double)e1[xb[i]]);
+        const float p = (float)v;
+        o[i] = ADD ? f4g(uu, i) + p : p;
+      }
+      *reinterpret_cast<float4*>(u + (size_t)z * plane + (size_t)y * W + xq) =
+          make_float4(o[0], o[1], o[2], o[3]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && k + NS < nck) issue(st, y0 + (k + NS) * CR);
+  }
+}
+
 }  // namespace
 
 // TMA path: float levels with W % 16 == 0 (16-byte mask row pitch for the
 // tensor map), W >= 128, 16-byte aligned buffers, and few enough CTAs per
 // plane for the partial-sum slots
+bool tma_prolong_ok(int H, int W) {
+  // the coarse map's row pitch (W/2 floats) must be a multiple of 16 bytes
+  return W % 16 == 0 && W >= TC && (W / 2) % 4 == 0 && encode_fn() != nullptr;
+}
+
 bool tma_ok(int H, int W, size_t npart) {
   if (W % 16 != 0 || W < TC || !encode_fn()) return false;
   return (size_t)cdiv(W, TC) * cdiv(H, TR) <= npart;
@@ -325,6 +438,36 @@ int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double
                            active);
   return launch<0, false>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
                           active);
+}
+
+int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int C, int chh,
+                int cww, int H, int W, int add, cudaStream_t s, int ntile, const int* active) {
+  PMaps mp;
+  const int nz = C * ntile;
+  if ((add && !make_map(&mp.u, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, TC, CR)) ||
+      !make_map(&mp.m, m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, W, H, ntile, TC, CR) ||
+      !make_map(&mp.e, e, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cww, chh, nz, EW, EH)) {
+    set_error("cuTensorMapEncodeTiled failed (prolongation %d x %d x %d)", nz, H, W);
+    return -1;
+  }
+  if (!add) mp.u = mp.m;  // unused
+  static bool attr[2] = {false, false};
+  if (!attr[add ? 1 : 0]) {
+    if (add)
+      SP_CUDA(cudaFuncSetAttribute(k_prolong_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   PSMEM));
+    else
+      SP_CUDA(cudaFuncSetAttribute(k_prolong_tma<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM));
+    attr[add ? 1 : 0] = true;
+  }
+  dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)nz);
+  if (add)
+    k_prolong_tma<true><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active);
+  else
+    k_prolong_tma<false><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active);
+  SP_CHECK_LAUNCH();
+  return 0;
 }
 
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,

@@ -23,6 +23,10 @@
 // (solver.py:142-197), recomputed on the device in double with the exact
 // operation order (pointwise total over covering blocks in block order,
 // last covering block takes 1 - sum of the others), cast to T.
+#include <cuda_pipeline.h>
+
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace sp {
@@ -32,9 +36,12 @@ namespace sp {
 __device__ unsigned long long g_oras_stats[4];
 __device__ int g_stats_on;
 
-// kernel choice for float blocks <= 32x32: 0 = register-resident 4-warp job
-// kernel (k_oras_rows, default), 1 = the 256-thread CTA kernel with the
-// reference's double-precision stencil (sp_oras_variant, A/B measurements)
+// kernel choice for float blocks <= 32x32 (sp_oras_variant, A/B runs):
+// 0 = register-resident 4-warp job kernel, one job per CTA (k_oras_rows,
+// default), 1 = the 256-thread CTA kernel with the reference's double
+// stencil, 3 = persistent k_oras_rows_p with cp.async prefetch of the next
+// job (it removes the load stalls but issues 32% more instructions and
+// loses: 1.80 vs 1.58 ms per 4K V-cycle, profiles/oras_ab_r01j.txt)
 static int oras_kernel = 0;
 int oras_variant(int v) {
   if (v >= 0) oras_kernel = v;
@@ -275,56 +282,20 @@ __device__ __forceinline__ float warp_sum_f(float v) {
   return v;
 }
 
+// The local CG of one (block, channel) job (numba_impl.py:188-251) on
+// registers: res[] (in: r, out: final residual), v[] (out: correction), the
+// mask / validity bit words of the warp's 8 rows and the unmasked flags of
+// the rows just above / below the band.  Returns the iteration count.
 template <bool UNIT_H>
-__global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
-    const float* __restrict__ r, const uint8_t* __restrict__ m,
-    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
-    const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W, int stride,
-    float closure, long cap, float inv_h2, const float* __restrict__ weights,
-    float* __restrict__ corr, const int* __restrict__ active, int corr_nb) {
-  __shared__ float er_top[NWJ][32], er_bot[NWJ][32];  // edge rows of r (new)
-  __shared__ double red_a[NWJ], red_b[NWJ];
-  // corr_nb: blocks per channel plane of `corr` (a row-strip view launches a
-  // sub-range of the level's blocks, `weights` / `corr` offset to its first)
-  const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y;
-  const int nb = corr_nb > 0 ? corr_nb : (int)gridDim.x;
-  const int tile = blockIdx.z;
-  if (active && !active[tile]) return;
-  const int j = threadIdx.x & 31, w = threadIdx.x >> 5, i0 = w * RW;
-  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
-  const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
-  const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
-  const size_t plane = (size_t)H * W;
-  const float* rc = r + ((size_t)tile * C + ch) * plane;
-  const uint8_t* mt = m + (size_t)tile * plane;
-  const bool lane_ok = j < bw;
-  const int gx = x0 + j;
-
-  // ---- load the job: residual rows, mask bits (own rows + the row above
-  // and below the warp's band), validity
-  float res[RW];
-  uint32_t mb = 0, vb = 0;
-#pragma unroll
-  for (int s = 0; s < RW; ++s) {
-    const int i = i0 + s;
-    res[s] = 0.0f;
-    if (i < bh && lane_ok) {
-      const size_t g = (size_t)(y0 + i) * W + gx;
-      res[s] = rc[g];
-      if (mt[g]) mb |= 1u << s;
-      vb |= 1u << s;
-    }
-  }
-  const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
-  const bool has_dn = i0 + RW < bh && lane_ok;
-  // neighbour rows outside the warp's band: 1 if they exist in the block and
-  // are unmasked (their q = p * fm feeds this band's stencil)
-  const float fm_up =
-      has_up && !mt[(size_t)(y0 + i0 - 1) * W + gx] ? 1.0f : 0.0f;
-  const float fm_dn =
-      has_dn && !mt[(size_t)(y0 + i0 + RW) * W + gx] ? 1.0f : 0.0f;
-  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
+__device__ __forceinline__ long cg_rows(float (&res)[RW], float (&v)[RW], uint32_t mb,
+                                        uint32_t vb, float fm_up, float fm_dn, int y0, int x0,
+                                        int bh, int bw, int H, int W, float closure,
+                                        float inv_h2, double tau, long cap, int j, int w,
+                                        float (*er_top)[32], float (*er_bot)[32],
+                                        double* red_a, double* red_b) {
+  long it;
   const bool lf_in = j > 0, rt_in = j < bw - 1;
+  const int gx = x0 + j;
   // Branch-free operator (numba_impl.py:196-226 semantics):
   //   (A p)_i = dgp_i * p_i - fm_i * sum_{in-block nbrs k} fm_k p_k
   // fm = 1 on valid unmasked pixels, else 0.  dgp = the Robin-closed local
@@ -334,7 +305,7 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
   float fm[RW], dgp[RW];
 #pragma unroll
   for (int s = 0; s < RW; ++s) {
-    const int i = i0 + s, gy = y0 + i;
+    const int i = w * RW + s, gy = y0 + i;
     float d = 0.0f;
     if (gy > 0) d += i > 0 ? 1.0f : closure;
     if (gy < H - 1) d += i < bh - 1 ? 1.0f : closure;
@@ -344,7 +315,7 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
     fm[s] = valid && !masked ? 1.0f : 0.0f;
     dgp[s] = !valid ? 0.0f : (masked ? 1.0f : d * inv_h2);
   }
-  float p[RW], v[RW], ap[RW];
+  float p[RW], ap[RW];
   float rs_f = 0.0f;
 #pragma unroll
   for (int s = 0; s < RW; ++s) {
@@ -363,7 +334,7 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
   // p of the row above / below this warp's band (owned by warps w-1 / w+1)
   float pu = w > 0 ? er_bot[w - 1][j] : 0.0f;
   float pd = w < NWJ - 1 ? er_top[w + 1][j] : 0.0f;
-  long it = 0;
+  it = 0;
   while (rs > tau && it < cap) {
     float q[RW];
 #pragma unroll
@@ -416,6 +387,61 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
     if (w < NWJ - 1) pd = __fmaf_rn(beta, pd, er_top[w + 1][j]);
     ++it;
   }
+  return it;
+}
+
+template <bool UNIT_H>
+__global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
+    const float* __restrict__ r, const uint8_t* __restrict__ m,
+    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
+    const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W, int stride,
+    float closure, long cap, float inv_h2, const float* __restrict__ weights,
+    float* __restrict__ corr, const int* __restrict__ active, int corr_nb) {
+  __shared__ float er_top[NWJ][32], er_bot[NWJ][32];  // edge rows of r (new)
+  __shared__ double red_a[NWJ], red_b[NWJ];
+  // corr_nb: blocks per channel plane of `corr` (a row-strip view launches a
+  // sub-range of the level's blocks, `weights` / `corr` offset to its first)
+  const int bi = blockIdx.x, ch = blockIdx.y, C = gridDim.y;
+  const int nb = corr_nb > 0 ? corr_nb : (int)gridDim.x;
+  const int tile = blockIdx.z;
+  if (active && !active[tile]) return;
+  const int j = threadIdx.x & 31, w = threadIdx.x >> 5, i0 = w * RW;
+  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
+  const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
+  const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
+  const size_t plane = (size_t)H * W;
+  const float* rc = r + ((size_t)tile * C + ch) * plane;
+  const uint8_t* mt = m + (size_t)tile * plane;
+  const bool lane_ok = j < bw;
+  const int gx = x0 + j;
+
+  // ---- load the job: residual rows, mask bits (own rows + the row above
+  // and below the warp's band), validity
+  float res[RW];
+  uint32_t mb = 0, vb = 0;
+#pragma unroll
+  for (int s = 0; s < RW; ++s) {
+    const int i = i0 + s;
+    res[s] = 0.0f;
+    if (i < bh && lane_ok) {
+      const size_t g = (size_t)(y0 + i) * W + gx;
+      res[s] = rc[g];
+      if (mt[g]) mb |= 1u << s;
+      vb |= 1u << s;
+    }
+  }
+  const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
+  const bool has_dn = i0 + RW < bh && lane_ok;
+  // neighbour rows outside the warp's band: 1 if they exist in the block and
+  // are unmasked (their q = p * fm feeds this band's stencil)
+  const float fm_up =
+      has_up && !mt[(size_t)(y0 + i0 - 1) * W + gx] ? 1.0f : 0.0f;
+  const float fm_dn =
+      has_dn && !mt[(size_t)(y0 + i0 + RW) * W + gx] ? 1.0f : 0.0f;
+  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
+  float v[RW];
+  const long it = cg_rows<UNIT_H>(res, v, mb, vb, fm_up, fm_dn, y0, x0, bh, bw, H, W, closure,
+                                  inv_h2, tau, cap, j, w, er_top, er_bot, red_a, red_b);
   float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
   const float* wb = weights + (size_t)bi * bh * bw;
 #pragma unroll
@@ -429,6 +455,123 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
     if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
     atomicMax(&g_oras_stats[3], (unsigned long long)it);
   }
+}
+
+// Persistent variant of k_oras_rows (sp_oras_variant 3, measured slower):
+// a resident CTA walks jobs job, job + gridDim.x, ... and prefetches the
+// NEXT job's residual block, blend weights and mask words into a second
+// shared-memory buffer with cp.async (LDGSTS) while the current job's CG
+// runs.  It hides the per-job DRAM latency (the top stall of the one-job-
+// per-CTA kernel) but the prefetch bookkeeping costs more issue slots than
+// the latency it hides in this issue-bound kernel.  Needs W % 4 == 0.
+constexpr int MWR = 9;  // mask words per block row (32 bytes + misalignment)
+
+__device__ __forceinline__ void job_origin(long job, int nb, int C, int nbx, int bh, int bw,
+                                           int H, int W, int stride, const int* ys,
+                                           const int* xs, int& bi, int& ch, int& tile, int& y0,
+                                           int& x0) {
+  bi = (int)(job % nb);
+  const long rest = job / nb;
+  ch = (int)(rest % C);
+  tile = (int)(rest / C);
+  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
+  y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
+  x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
+}
+
+template <bool UNIT_H>
+__global__ void __launch_bounds__(NTJ, 7) k_oras_rows_p(
+    const float* __restrict__ r, const uint8_t* __restrict__ m,
+    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
+    const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
+    float closure, long cap, float inv_h2, const float* __restrict__ weights,
+    float* __restrict__ corr, const int* __restrict__ active, int corr_nb, int C, long njobs) {
+  __shared__ float er_top[NWJ][32], er_bot[NWJ][32];
+  __shared__ double red_a[NWJ], red_b[NWJ];
+  __shared__ __align__(16) float sr[2][32 * 32];
+  __shared__ __align__(16) float sw[2][32 * 32];
+  __shared__ __align__(16) uint32_t smw[2][32 * MWR];
+  const int nb = corr_nb > 0 ? corr_nb : nbl;
+  const int j = threadIdx.x & 31, w = threadIdx.x >> 5, i0 = w * RW;
+  const size_t plane = (size_t)H * W;
+  auto prefetch = [&](long job, int b) {
+    int bi, ch, tile, y0, x0;
+    job_origin(job, nbl, C, nbx, bh, bw, H, W, stride, ys, xs, bi, ch, tile, y0, x0);
+    if (active && !active[tile]) return;
+    const float* rc = r + ((size_t)tile * C + ch) * plane;
+    const float* wb = weights + (size_t)bi * bh * bw;
+    if (j < bw) {
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+        const int i = i0 + s;
+        if (i < bh) {
+          __pipeline_memcpy_async(&sr[b][i * 32 + j], rc + (size_t)(y0 + i) * W + x0 + j, 4);
+          __pipeline_memcpy_async(&sw[b][i * 32 + j], wb + i * bw + j, 4);
+        }
+      }
+    }
+    const uint8_t* mt = m + (size_t)tile * plane;
+    const int wx0 = x0 >> 2, nwr = ((x0 + bw - 1) >> 2) - wx0 + 1;
+    for (int q = threadIdx.x; q < bh * nwr; q += NTJ) {
+      const int i = q / nwr, k = q - i * nwr;
+      __pipeline_memcpy_async(&smw[b][i * MWR + k],
+                              mt + (size_t)(y0 + i) * W + (size_t)(wx0 + k) * 4, 4);
+    }
+  };
+  int buf = 0;
+  long job = blockIdx.x;
+  if (job < njobs) prefetch(job, buf);
+  __pipeline_commit();
+  for (; job < njobs; job += gridDim.x) {
+    const long nxt = job + gridDim.x;
+    if (nxt < njobs) prefetch(nxt, buf ^ 1);
+    __pipeline_commit();
+    __pipeline_wait_prior(1);  // this thread's copies of the current job landed
+    __syncthreads();           // ... and every other thread's
+    int bi, ch, tile, y0, x0;
+    job_origin(job, nbl, C, nbx, bh, bw, H, W, stride, ys, xs, bi, ch, tile, y0, x0);
+    if (!(active && !active[tile])) {
+      const unsigned char* mrow0 = reinterpret_cast<const unsigned char*>(smw[buf]) + (x0 & 3);
+      auto mbyte = [&](int i) { return mrow0[i * MWR * 4 + j]; };
+      const bool lane_ok = j < bw;
+      float res[RW];
+      uint32_t mb = 0, vb = 0;
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+        const int i = i0 + s;
+        res[s] = 0.0f;
+        if (i < bh && lane_ok) {
+          res[s] = sr[buf][i * 32 + j];
+          if (mbyte(i)) mb |= 1u << s;
+          vb |= 1u << s;
+        }
+      }
+      const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
+      const bool has_dn = i0 + RW < bh && lane_ok;
+      const float fm_up = has_up && !mbyte(i0 - 1) ? 1.0f : 0.0f;
+      const float fm_dn = has_dn && !mbyte(i0 + RW) ? 1.0f : 0.0f;
+      const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
+      float v[RW];
+      const long it = cg_rows<UNIT_H>(res, v, mb, vb, fm_up, fm_dn, y0, x0, bh, bw, H, W,
+                                      closure, inv_h2, tau, cap, j, w, er_top, er_bot, red_a,
+                                      red_b);
+      float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
+#pragma unroll
+      for (int s = 0; s < RW; ++s) {
+        const int i = i0 + s;
+        if ((vb >> s) & 1u) out[i * bw + j] = sw[buf][i * 32 + j] * v[s];
+      }
+      if (threadIdx.x == 0 && g_stats_on) {
+        atomicAdd(&g_oras_stats[0], 1ull);
+        atomicAdd(&g_oras_stats[1], (unsigned long long)it);
+        if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
+        atomicMax(&g_oras_stats[3], (unsigned long long)it);
+      }
+    }
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
+    buf ^= 1;
+  }
+  __pipeline_wait_prior(0);
 }
 
 template <typename T, int PPT>
@@ -743,13 +886,27 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       T* corr, cudaStream_t s, int ntile, const int* active, int stride,
                       int corr_nb) {
   const int npx = bh * bw;
-  if (corr_nb > 0 && !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 0)) {
+  if (corr_nb > 0 && !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1)) {
     set_error("block sub-range launches need the float 32x32 ORAS kernel");
     return -2;
   }
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
-  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 0) {
+  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 3 && W % 4 == 0 &&
+      ((uintptr_t)m & 3) == 0) {
+    const long njobs = (long)nby * nbx * C * ntile;
+    static int occ = 0;
+    if (!occ) {
+      SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_oras_rows_p<true>, NTJ, 0));
+      if (occ < 1) occ = 1;
+    }
+    const long g = std::min<long>(njobs, (long)num_sms() * occ);
+    auto kern = inv_h2 == 1.0 ? k_oras_rows_p<true> : k_oras_rows_p<false>;
+    kern<<<(unsigned)g, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx,
+                                     nby * nbx, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
+                                     (float)inv_h2, (const float*)weights, (float*)corr, active,
+                                     corr_nb, C, njobs);
+  } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
     kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
                               W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,

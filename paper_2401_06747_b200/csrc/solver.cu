@@ -263,6 +263,9 @@ template <typename T>
 int prolong_lv(Hier* h, int lv, int add, cudaStream_t s) {
   Level& F = h->lv[lv];
   Level& G = h->lv[lv + 1];
+  if (sizeof(T) == 4 && h->sweep == 2 && tma_prolong_ok(F.H, F.W) && aligned_level<T>(F))
+    return prolong_tma((const float*)G.u, (float*)F.u, (const float*)F.b, F.mask, h->C, G.H,
+                       G.W, F.H, F.W, add, s, h->ntile, h->d_active);
   if (use_march<T>(h, F))
     return prolong_march((const float*)G.u, (float*)F.u, (const float*)F.b, F.mask, h->C, G.H,
                          G.W, F.H, F.W, add, s, h->ntile, h->d_active);
