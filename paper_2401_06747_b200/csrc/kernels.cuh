@@ -57,7 +57,8 @@ int prolong_march(const float* e, float* u, const float* b, const uint8_t* m, in
 bool tma_ok(int H, int W, size_t npart);
 int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
-              const int* active);
+              const int* active, double* bandcol = nullptr, int band0 = 0, int nbt = 0);
+bool tma_view_ok(int W);
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
                        int H, int W, cudaStream_t s, int ntile, const int* active);
 bool tma_prolong_ok(int H, int W);

@@ -146,7 +146,8 @@ template <int MODE, bool NORMS>
 __global__ void __launch_bounds__(CR * 32) k_resid_tma(
     const __grid_constant__ Maps mp, float* __restrict__ r, double* __restrict__ partial,
     unsigned* __restrict__ counter, double* __restrict__ norms, float* __restrict__ rcoarse,
-    int C, int H, int W, const int* __restrict__ active) {
+    int C, int H, int W, const int* __restrict__ active, double* __restrict__ bandcol,
+    int band0, int nbt) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
   __shared__ uint64_t bars[NS];
@@ -188,6 +189,23 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
       }
     }
     if (MODE == 1) *reinterpret_cast<float4*>(&rrow[w][4 * lane]) = rr;
+    if (MODE == 0 && NORMS && bandcol && ((k & 1) || k == nck - 1)) {
+      // row-band partials for the strip-partitioned solve (strips.cu): the
+      // CTA's sum over each 16-row band (2 chunks), one double per (plane,
+      // band, 128-column group); views start on a band boundary
+      double d = (double)sq;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
+      if (lane == 0) wsum[w] = d;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < CR; ++q2) t += wsum[q2];
+        bandcol[((size_t)z * nbt + band0 + (y0 + k * CR) / 16) * gridDim.x + blockIdx.x] = t;
+      }
+      sq = 0.0f;
+    }
     __syncthreads();  // stage st fully consumed (and the chunk's r rows staged)
     if (threadIdx.x == 0 && k + NS < nck)
       issue_chunk(mp, sm, bars, st, x0, y0 + (k + NS) * CR, z, tile);
@@ -215,7 +233,7 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
       __syncthreads();  // rrow reused by the next chunk
     }
   }
-  if (MODE != 0 || !NORMS) return;
+  if (MODE != 0 || !NORMS || bandcol) return;
   double sqd = (double)sq;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sqd += __shfl_xor_sync(0xFFFFFFFFu, sqd, o);
@@ -288,7 +306,8 @@ bool make_maps(Maps& mp, const float* u, const float* b, const uint8_t* m, int C
 template <int MODE, bool NORMS>
 int launch(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
            unsigned* counter, double* norms, float* rc, int C, int H, int W, cudaStream_t s,
-           int ntile, const int* active) {
+           int ntile, const int* active, double* bandcol = nullptr, int band0 = 0,
+           int nbt = 0) {
   Maps mp;
   if (!make_maps(mp, u, b, m, C, H, W, ntile)) {
     set_error("cuTensorMapEncodeTiled failed (%d x %d x %d)", C * ntile, H, W);
@@ -302,7 +321,7 @@ int launch(const float* u, const float* b, const uint8_t* m, float* r, double* p
   }
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)((long)C * ntile));
   k_resid_tma<MODE, NORMS><<<grid, CR * 32, SMEM, s>>>(mp, r, partial, counter, norms, rc, C, H,
-                                                       W, active);
+                                                       W, active, bandcol, band0, nbt);
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -425,6 +444,9 @@ bool tma_prolong_ok(int H, int W) {
   return W % 16 == 0 && W >= TC && (W / 2) % 4 == 0 && encode_fn() != nullptr;
 }
 
+// strips (band-norm mode: no CTA-partial slots needed)
+bool tma_view_ok(int W) { return W % 16 == 0 && W >= TC && encode_fn() != nullptr; }
+
 bool tma_ok(int H, int W, size_t npart) {
   if (W % 16 != 0 || W < TC || !encode_fn()) return false;
   return (size_t)cdiv(W, TC) * cdiv(H, TR) <= npart;
@@ -432,7 +454,10 @@ bool tma_ok(int H, int W, size_t npart) {
 
 int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
-              const int* active) {
+              const int* active, double* bandcol, int band0, int nbt) {
+  if (bandcol)
+    return launch<0, true>(u, b, m, r, partial, counter, nullptr, nullptr, C, H, W, s, ntile,
+                           active, bandcol, band0, nbt);
   if (norms)
     return launch<0, true>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
                            active);

@@ -295,6 +295,7 @@ __device__ __forceinline__ long cg_rows(float (&res)[RW], float (&v)[RW], uint32
                                         double* red_a, double* red_b) {
   long it;
   const bool lf_in = j > 0, rt_in = j < bw - 1;
+  const float lf = lf_in ? 1.0f : 0.0f, rt = rt_in ? 1.0f : 0.0f;
   const int gx = x0 + j;
   // Branch-free operator (numba_impl.py:196-226 semantics):
   //   (A p)_i = dgp_i * p_i - fm_i * sum_{in-block nbrs k} fm_k p_k
@@ -343,13 +344,13 @@ __device__ __forceinline__ long cg_rows(float (&res)[RW], float (&v)[RW], uint32
     float pap_f = 0.0f;
 #pragma unroll
     for (int s = 0; s < RW; ++s) {
-      float ql = __shfl_up_sync(0xFFFFFFFFu, q[s], 1);
-      float qr = __shfl_down_sync(0xFFFFFFFFu, q[s], 1);
-      ql = lf_in ? ql : 0.0f;
-      qr = rt_in ? qr : 0.0f;
+      const float ql = __shfl_up_sync(0xFFFFFFFFu, q[s], 1);
+      const float qr = __shfl_down_sync(0xFFFFFFFFu, q[s], 1);
       const float up = s > 0 ? q[s - 1] : qu;
       const float dn = s < RW - 1 ? q[s + 1] : qd;
-      const float acc = (up + dn) + (ql + qr);
+      // lane-edge neighbours enter with weight 0 (lf / rt are 0 or 1, so the
+      // fused multiply-add is an exact add where they are 1)
+      const float acc = __fmaf_rn(qr, rt, __fmaf_rn(ql, lf, up + dn));
       const float fa = fm[s] * acc;
       const float a = __fmaf_rn(dgp[s], p[s], UNIT_H ? -fa : -(fa * inv_h2));
       ap[s] = a;

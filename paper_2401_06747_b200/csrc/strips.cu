@@ -267,11 +267,18 @@ int residual_norms(StripGroup& g, int lv, bool exch, cudaStream_t s) {
     const StripView& V = g.v[i][lv];
     Level& L = g.h[i]->lv[lv];
     const int hv = V.e1 - V.e0;
-    for (int c = 0; c < g.C; ++c)
-      SP_TRY(resid_march(rowp(L.u, L, c, V.e0), rowp(L.b, L, c, V.e0), mrow(L, V.e0),
+    const bool tma = tma_view_ok(L.W);
+    for (int c = 0; c < g.C; ++c) {
+      double* bc = g.bandcol[i][lv] + (size_t)c * g.nbt[lv] * g.ncg[lv];
+      if (tma)
+        SP_TRY(resid_tma(rowp(L.u, L, c, V.e0), rowp(L.b, L, c, V.e0), mrow(L, V.e0),
                          rowp(L.r, L, c, V.e0), nullptr, nullptr, nullptr, 1, hv, L.W, s, 1,
-                         nullptr, g.bandcol[i][lv] + (size_t)c * g.nbt[lv] * g.ncg[lv],
-                         V.e0 / BR, g.nbt[lv]));
+                         nullptr, bc, V.e0 / BR, g.nbt[lv]));
+      else
+        SP_TRY(resid_march(rowp(L.u, L, c, V.e0), rowp(L.b, L, c, V.e0), mrow(L, V.e0),
+                           rowp(L.r, L, c, V.e0), nullptr, nullptr, nullptr, 1, hv, L.W, s, 1,
+                           nullptr, bc, V.e0 / BR, g.nbt[lv]));
+    }
     const int n = g.C * g.nbt[lv];
     k_band_sum<<<cdiv(n, 256), 256, 0, s>>>(g.bandcol[i][lv], g.bands[i][lv], g.C, g.nbt[lv],
                                             g.ncg[lv], V.o0 / BR, cdiv(V.o1, BR));
@@ -300,6 +307,14 @@ int residual_norms(StripGroup& g, int lv, bool exch, cudaStream_t s) {
     SP_CHECK_LAUNCH();
   }
   return 0;
+}
+
+// u (+)= P e on a view, one channel plane
+int prolong_view(const float* e, float* u, const float* b, const uint8_t* m, int chh, int cww,
+                 int hv, int W, int add, cudaStream_t s) {
+  if (tma_prolong_ok(hv, W))
+    return prolong_tma(e, u, b, m, 1, chh, cww, hv, W, add, s, 1, nullptr);
+  return prolong_march(e, u, b, m, 1, chh, cww, hv, W, add, s, 1, nullptr);
 }
 
 int oras_blend(StripGroup& g, int lv, cudaStream_t s) {
@@ -342,10 +357,16 @@ int vcycle(StripGroup& g, int lv, bool first_done, cudaStream_t s) {
     const StripView& V = g.v[i][lv];
     Level& F = g.h[i]->lv[lv];
     Level& G = g.h[i]->lv[lv + 1];
-    for (int c = 0; c < g.C; ++c)
-      SP_TRY(resid_restrict_march(rowp(F.u, F, c, V.e0), rowp(F.b, F, c, V.e0), mrow(F, V.e0),
+    for (int c = 0; c < g.C; ++c) {
+      if (tma_view_ok(F.W))
+        SP_TRY(resid_restrict_tma(rowp(F.u, F, c, V.e0), rowp(F.b, F, c, V.e0), mrow(F, V.e0),
                                   rowp(G.r, G, c, V.e0 / 2), 1, V.e1 - V.e0, F.W, s, 1,
                                   nullptr));
+      else
+        SP_TRY(resid_restrict_march(rowp(F.u, F, c, V.e0), rowp(F.b, F, c, V.e0),
+                                    mrow(F, V.e0), rowp(G.r, G, c, V.e0 / 2), 1, V.e1 - V.e0,
+                                    F.W, s, 1, nullptr));
+    }
   }
   if (lv + 1 < g.La) {
     SP_TRY(exchange(g, lv + 1, 2, s));
@@ -380,9 +401,8 @@ int vcycle(StripGroup& g, int lv, bool first_done, cudaStream_t s) {
     Level& G = g.h[i]->lv[lv + 1];
     const int hv = V.e1 - V.e0, ch = std::min((hv + 1) / 2, G.H - V.e0 / 2);
     for (int c = 0; c < g.C; ++c)
-      SP_TRY(prolong_march(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0),
-                           rowp(F.b, F, c, V.e0), mrow(F, V.e0), 1, ch, G.W, hv, F.W, 1, s, 1,
-                           nullptr));
+      SP_TRY(prolong_view(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0),
+                          rowp(F.b, F, c, V.e0), mrow(F, V.e0), ch, G.W, hv, F.W, 1, s));
   }
   SP_TRY(smooth(g, lv, cfg.post, false, s));
   return 0;
@@ -416,9 +436,8 @@ int cascade(StripGroup& g, cudaStream_t s) {
       for (int c = 0; c < g.C; ++c) {
         SP_TRY(masked_sym_rhs<float>(rowp(F.values, F, c, V.e0), mrow(F, V.e0),
                                      rowp(F.b, F, c, V.e0), 1, hv, F.W, s));
-        SP_TRY(prolong_march(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0),
-                             rowp(F.b, F, c, V.e0), mrow(F, V.e0), 1, ch, G.W, hv, F.W, 0, s,
-                             1, nullptr));
+        SP_TRY(prolong_view(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0),
+                            rowp(F.b, F, c, V.e0), mrow(F, V.e0), ch, G.W, hv, F.W, 0, s));
       }
     }
     SP_TRY(smooth(g, lv, 1, false, s));
