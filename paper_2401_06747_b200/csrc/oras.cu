@@ -794,49 +794,79 @@ __global__ void __launch_bounds__(256) k_oras_blend(
     if (x >= W) continue;
     const int kx0 = col_k0[x], nkx = col_n[x];
     const int xo0 = x - xs[kx0], xo1 = nkx > 1 ? x - xs[kx0 + 1] : 0;
+    int yv[2], ky0[2], nky[2];
+    bool ok[2];
+    bool regular = nkx <= 2;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int y = (t / ntx) * 16 + threadIdx.y + 8 * half;
-      if (y >= H) continue;
-      const int ky0 = row_k0[y], nky = row_n[y];
+    for (int h2 = 0; h2 < 2; ++h2) {
+      yv[h2] = (t / ntx) * 16 + threadIdx.y + 8 * h2;
+      ok[h2] = yv[h2] < H;
+      ky0[h2] = ok[h2] ? row_k0[yv[h2]] : 0;
+      nky[h2] = ok[h2] ? row_n[yv[h2]] : 0;
+      regular = regular && nky[h2] <= 2;
+    }
+    if (regular) {
+      // every load of both pixels first (u and the <= 2 x 2 corrections per
+      // channel), then the sums in block order and the stores
+      size_t off[2][4];
+      bool on[2][4];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = q >> 1, b2 = q & 1;
+          on[h2][q] = ok[h2] && a < nky[h2] && b2 < nkx;
+          const int ky = ky0[h2] + (on[h2][q] ? a : 0), kx = kx0 + (on[h2][q] ? b2 : 0);
+          off[h2][q] = ((size_t)ky * nbx + kx) * npx + (size_t)(yv[h2] - ys[ky]) * bw +
+                       (b2 ? xo1 : xo0);
+        }
+      T uu[2][CC], v[2][4][CC];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+        for (int c = 0; c < CC; ++c)
+          uu[h2][c] = (ok[h2] && c < C) ? ut[(size_t)c * plane + (size_t)yv[h2] * W + x] : (T)0;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < CC; ++c)
+            v[h2][q][c] = (on[h2][q] && c < C) ? ct[(size_t)c * cplane + off[h2][q]] : (T)0;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        if (!ok[h2]) continue;
+#pragma unroll
+        for (int c = 0; c < CC; ++c) {
+          if (c >= C) continue;
+          T acc = uu[h2][c];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (on[h2][q]) acc = acc + v[h2][q][c];
+          ut[(size_t)c * plane + (size_t)yv[h2] * W + x] = acc;
+        }
+      }
+      continue;
+    }
+    // three covering blocks in a row or column (a pulled-in last block)
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      if (!ok[h2]) continue;
+      const int y = yv[h2];
       const size_t k = (size_t)y * W + x;
       T acc[CC];
 #pragma unroll
       for (int c = 0; c < CC; ++c)
         if (c < C) acc[c] = ut[(size_t)c * plane + k];
-      if (nky <= 2 && nkx <= 2) {
-        // offsets of the (ky0 + a, kx0 + b) corrections, block order
-        size_t off[4];
-        bool on[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int a = q >> 1, b2 = q & 1;
-          on[q] = a < nky && b2 < nkx;
-          const int ky = ky0 + (on[q] ? a : 0), kx = kx0 + (on[q] ? b2 : 0);
-          off[q] = ((size_t)ky * nbx + kx) * npx + (size_t)(y - ys[ky]) * bw + (b2 ? xo1 : xo0);
-        }
-        T v[4][CC];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < nky[h2]; ++a) {
+        const int ky = ky0[h2] + a;
+        const size_t rowoff = (size_t)ky * nbx * npx + (size_t)(y - ys[ky]) * bw;
+        for (int b2 = 0; b2 < nkx; ++b2) {
+          const int kx = kx0 + b2;
+          const size_t off = rowoff + (size_t)kx * npx + (size_t)(x - xs[kx]);
 #pragma unroll
           for (int c = 0; c < CC; ++c)
-            v[q][c] = (on[q] && c < C) ? ct[(size_t)c * cplane + off[q]] : (T)0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int c = 0; c < CC; ++c)
-            if (on[q] && c < C) acc[c] = acc[c] + v[q][c];
-      } else {
-        for (int a = 0; a < nky; ++a) {
-          const int ky = ky0 + a;
-          const size_t rowoff = (size_t)ky * nbx * npx + (size_t)(y - ys[ky]) * bw;
-          for (int b2 = 0; b2 < nkx; ++b2) {
-            const int kx = kx0 + b2;
-            const size_t off = rowoff + (size_t)kx * npx + (size_t)(x - xs[kx]);
-#pragma unroll
-            for (int c = 0; c < CC; ++c)
-              if (c < C) acc[c] = acc[c] + ct[(size_t)c * cplane + off];
-          }
+            if (c < C) acc[c] = acc[c] + ct[(size_t)c * cplane + off];
         }
       }
 #pragma unroll
