@@ -139,10 +139,12 @@ def run_tonal(f: Image, mask: Mask, cfg: PipelineConfig, solver: InpaintSolver):
     return ras_tonal(f, mask, init=vi, cfg=cfg.ras(), solver=solver)
 
 
-def run_pipeline(f: Image, cfg: PipelineConfig):
-    """cli.py:251-257: (mask, state, spatial history, seconds)."""
+def run_pipeline(f: Image, cfg: PipelineConfig, solver=None):
+    """cli.py:251-257: (mask, state, spatial history, seconds).  `solver`
+    (optional, not in the reference) replaces ``cfg.solver()`` -- e.g. a
+    `strips.StripSolver` that runs every inpainting solve on row strips."""
     cfg.validate()
-    solver = cfg.solver()
+    solver = cfg.solver() if solver is None else solver
     t0 = time.perf_counter()
     # one upload of a host image for the whole run (every stage reads f)
     f = Image(f.tensor())

@@ -165,12 +165,132 @@ class NcclComm:
             pass
 
 
+class _StripGroup:
+    """One native strip group (csrc/strips.cu): P strips of a (C, H, W)
+    float32 hierarchy, the strips [first, first + nloc) held here."""
+
+    def __init__(self, key, comm):
+        C, H, W, block, overlap, levels, pre, post, alpha, rho, P, La, nloc, first = key
+        self.key = key
+        self.La, self.o0, self.o1 = strip_plan(H, W, P, La, _cfg_of(key))
+        flat0 = np.array([v for row in self.o0 for v in row] or [0], np.int32)
+        flat1 = np.array([v for row in self.o1 for v in row] or [0], np.int32)
+        self.h = ctypes.c_void_p()
+        call("sp_strip_create", ctypes.byref(self.h), C, H, W, block, overlap, levels, pre,
+             post, alpha, rho, P, nloc, first, self.La, HALO, ptr(flat0), ptr(flat1),
+             comm.handle if comm is not None else None)
+        self.has_values = False
+
+    def destroy(self):
+        if self.h:
+            _lib.load().sp_strip_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+
+def _cfg_of(key):
+    from .solver import OrasConfig
+    C, H, W, block, overlap, levels, pre, post, alpha, rho = key[:10]
+    return MultigridConfig(levels=levels, pre=pre, post=post,
+                           oras=OrasConfig(block=block, overlap=overlap, alpha=alpha, rho=rho))
+
+
+class _GroupPool:
+    """Free strip groups per geometry key (a group owns P full-size
+    hierarchies, so they are reused across solves and pipeline runs)."""
+
+    def __init__(self, keep=2):
+        self.keep = keep
+        self.free = {}
+
+    def acquire(self, key, comm):
+        lst = self.free.get(key)
+        if lst:
+            return lst.pop()
+        return _StripGroup(key, comm)
+
+    def release(self, g):
+        lst = self.free.setdefault(g.key, [])
+        if len(lst) < self.keep:
+            lst.append(g)
+        else:
+            g.destroy()
+
+    def clear(self):
+        for lst in self.free.values():
+            for g in lst:
+                g.destroy()
+        self.free.clear()
+
+
+_GPOOL = _GroupPool()
+
+
+class StripHierarchy:
+    """`GridHierarchy` on a strip group: the mask (and stored-value) pyramid
+    of one mask and `solve_sym` (solver.py:328-372) over the strips."""
+
+    def __init__(self, owner: "StripSolver", mask_t, values_t):
+        self.owner = owner
+        H, W = mask_t.shape
+        self.channels = owner.channels
+        self.height, self.width = H, W
+        self.cfg = owner.cfg
+        self._g = _GPOOL.acquire(owner._key, owner._comm)
+        call("sp_strip_set_mask", self._g.h, ptr(mask_t), ptr(values_t), stream())
+        self.has_values = values_t is not None
+        self._rep = _CReport()
+
+    def __del__(self):
+        g = getattr(self, "_g", None)
+        if g is not None:
+            try:
+                _GPOOL.release(g)
+            except Exception:
+                pass
+            self._g = None
+
+    @property
+    def nlevels(self):
+        n = ctypes.c_int()
+        dims = (ctypes.c_int * 128)()
+        call("sp_strip_levels", self._g.h, ctypes.byref(n), dims, 128)
+        return n.value
+
+    def solve_sym(self, bsym, init=None, tol=None, cycles=None, max_cycles=None,
+                  cascade=False):
+        cfg = self.cfg
+        t0 = time.perf_counter()
+        b = bsym.to(torch.float32).contiguous()
+        if init is not None:
+            u = init.to(torch.float32).clone()
+            mode = 1
+        else:
+            u = torch.empty_like(b)
+            mode = 2 if (cascade and self.has_values) else 0
+            if cascade and not self.has_values and self.nlevels > 1:
+                raise ValueError("hierarchy was built without stored values")
+        rep = self._rep
+        call("sp_strip_solve", self._g.h, ptr(b), ptr(u), mode,
+             -1.0 if tol is None else float(tol),
+             int(cfg.cycles if cycles is None else cycles),
+             int(cfg.max_cycles if max_cycles is None else max_cycles), ctypes.byref(rep),
+             stream())
+        out = SolverReport(iterations=rep.iterations, converged=bool(rep.converged),
+                           residuals=[rep.residuals[i] for i in range(rep.nres)])
+        out.seconds = time.perf_counter() - t0
+        return u, out
+
+
 class StripSolver:
-    """`InpaintSolver` semantics (solver.py:514-536) on a row-strip partition.
+    """`InpaintSolver` (solver.py:514-536) on a row-strip partition.
 
     ``StripSolver(h, w, c, strips=P)``: all P strips in this process (one
     GPU).  ``StripSolver.distributed(h, w, c)``: one strip per rank of the
-    current ``torch.distributed`` job, NCCL transport.  float32 only.
+    current ``torch.distributed`` job, NCCL transport.  float32 only.  Every
+    rank returns the gathered (full) solution, bit-identical for every P.
+    It can stand in for the `InpaintSolver` of the pipeline stages
+    (`delaunay_densify`, the tonal optimizers, `run_pipeline(...,
+    solver=...)`): `inpaint` and `hierarchy` follow `InpaintSolver`.
     """
 
     def __init__(self, height, width, channels, strips=1, cfg: MultigridConfig | None = None,
@@ -180,19 +300,13 @@ class StripSolver:
             raise ValueError("the strip solver runs float32")
         self.height, self.width, self.channels = height, width, channels
         self.P = strips
-        self.La, o0, o1 = strip_plan(height, width, strips, La, self.cfg)
-        self.o0, self.o1 = o0, o1
-        flat0 = np.array([v for row in o0 for v in row] or [0], np.int32)
-        flat1 = np.array([v for row in o1 for v in row] or [0], np.int32)
+        self.La, self.o0, self.o1 = strip_plan(height, width, strips, La, self.cfg)
         nloc, first = (strips, 0) if _rank is None else (1, _rank)
+        self.rank = 0 if _rank is None else _rank
         self._comm = _comm
         o = self.cfg.oras
-        self._g = ctypes.c_void_p()
-        call("sp_strip_create", ctypes.byref(self._g), channels, height, width, o.block,
-             o.overlap, self.cfg.levels, self.cfg.pre, self.cfg.post, float(o.alpha),
-             float(o.rho), strips, nloc, first, self.La, HALO, ptr(flat0), ptr(flat1),
-             _comm.handle if _comm is not None else None)
-        self._rep = _CReport()
+        self._key = (channels, height, width, o.block, o.overlap, self.cfg.levels, self.cfg.pre,
+                     self.cfg.post, float(o.alpha), float(o.rho), strips, self.La, nloc, first)
 
     @classmethod
     def distributed(cls, height, width, channels, cfg=None, La=None):
@@ -201,14 +315,19 @@ class StripSolver:
         return cls(height, width, channels, strips=dist.get_world_size(), cfg=cfg, La=La,
                    _rank=dist.get_rank(), _comm=comm)
 
-    def __del__(self):
-        g = getattr(self, "_g", None)
-        if g:
-            try:
-                _lib.load().sp_strip_destroy(g)
-            except Exception:
-                pass
-            self._g = None
+    @property
+    def distributed_ranks(self):
+        return self.P if self._comm is not None else 1
+
+    def _check(self, shape):
+        if tuple(shape) != (self.height, self.width):
+            raise ValueError("image does not match the strip solver's geometry")
+
+    def hierarchy(self, mask: Mask, values: Image | None = None, channels=None):
+        m_t = mask.tensor()
+        self._check(m_t.shape)
+        v = None if values is None else values.tensor(torch.float32)
+        return StripHierarchy(self, m_t, v)
 
     def inpaint(self, f: Image, mask: Mask, init: Image | None = None, tol=-1.0, cycles=None):
         """solver.py:485-511 on the strips: FMG cascade unless `init`; the
@@ -222,21 +341,11 @@ class StripSolver:
         m_t = mask.tensor()
         if tuple(f_t.shape) != (self.channels, self.height, self.width):
             raise ValueError("image does not match the strip solver's geometry")
-        call("sp_strip_set_mask", self._g, ptr(m_t), ptr(f_t), stream())
+        hier = StripHierarchy(self, m_t, f_t)
         bsym = _masked_rhs(f_t, m_t)
-        if init is not None:
-            u = init.tensor(torch.float32).clone()
-            mode = 1
-        else:
-            u = torch.empty_like(bsym)
-            mode = 2 if cfg.mode == "fmg" else 0
-        n_cycles = cfg.cycles if cycles is None else cycles
-        rep = self._rep
-        call("sp_strip_solve", self._g, ptr(bsym), ptr(u), mode,
-             -1.0 if tol is None else float(tol), int(n_cycles), int(cfg.max_cycles),
-             ctypes.byref(rep), stream())
+        init_t = None if init is None else init.tensor(torch.float32)
+        u, out = hier.solve_sym(bsym, init=init_t, tol=tol, cycles=cycles,
+                                cascade=cfg.mode == "fmg" and init is None)
         _enforce(u, f_t, m_t)
-        out = SolverReport(iterations=rep.iterations, converged=bool(rep.converged),
-                           residuals=[rep.residuals[i] for i in range(rep.nres)])
         out.seconds = time.perf_counter() - t0
         return Image(u), out

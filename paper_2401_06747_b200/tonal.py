@@ -110,7 +110,9 @@ class _TonalSystem:
     def __init__(self, mask_t, solver: InpaintSolver, channels, inner_cycles=1,
                  inner_tol=None, cold_tol=1e-4, cold_max_cycles=100):
         self.mask = mask_t
-        self.hier = GridHierarchy.build(Mask(mask_t), None, solver.cfg, channels=channels)
+        # the solver's own hierarchy type (GridHierarchy, or the row-strip
+        # hierarchy of strips.StripSolver)
+        self.hier = solver.hierarchy(Mask(mask_t), None, channels=channels)
         self.inner_cycles = inner_cycles
         self.inner_tol = inner_tol
         self.cold_tol = cold_tol

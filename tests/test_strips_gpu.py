@@ -71,3 +71,27 @@ def test_strip_solver_validation():
     s = StripSolver(256, 256, 1, strips=2, La=1)
     with pytest.raises(ValueError):
         s.inpaint(sp.Image(np.ones((1, 256, 256))), sp.Mask(np.zeros((256, 256))))
+
+
+def test_pipeline_on_strips_is_partition_invariant():
+    """run_pipeline with every inpainting / B / B^T solve on row strips:
+    the same mask and tonal values for every strip count, and the same
+    optimisation quality as the single-hierarchy pipeline."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200.strips import StripSolver, max_partitioned_levels
+    c, h, w = 3, 512, 768
+    f = O.synth(h, w, c, 4)
+    cfg = sp.PipelineConfig(iterations=6)
+    La = min(max_partitioned_levels(h, w, P) for P in (2, 3))
+    runs = []
+    for P in (1, 2, 3):
+        solver = StripSolver(h, w, c, strips=P, cfg=cfg.solver().cfg, La=La)
+        mask, st, hist, _ = sp.run_pipeline(sp.Image(f), cfg, solver=solver)
+        runs.append((mask.indicator.copy(), st.g.data.copy(), st.mse, [r[2] for r in hist]))
+    for m, g, mse, hh in runs[1:]:
+        assert np.array_equal(m, runs[0][0])
+        assert np.array_equal(g, runs[0][1])
+        assert mse == runs[0][2] and hh == runs[0][3]
+    mask_r, st_r, hist_r, _ = sp.run_pipeline(sp.Image(f), cfg)
+    assert mask_r.count == int(runs[0][0].sum())
+    assert abs(st_r.mse - runs[0][2]) <= 5e-3 * st_r.mse
