@@ -297,13 +297,24 @@ class _RasBlocks:
              self.bw, ptr(mt_all), stream())
         has = (mt_all.view(nb, -1).sum(1) > 0).cpu().numpy()
         act = np.nonzero(has)[0]
-        self.nt = int(act.size)
+        self.nt_all = int(act.size)
         tile_of = np.full(nb, -1, np.int32)
-        tile_of[act] = np.arange(self.nt, dtype=np.int32)
+        tile_of[act] = np.arange(self.nt_all, dtype=np.int32)
         self.tile_of = torch.from_numpy(tile_of).to(dev)
-        self.oy = torch.from_numpy(oy_all[act].copy()).to(dev)
-        self.ox = torch.from_numpy(ox_all[act].copy()).to(dev)
-        self.tmask = mt_all[torch.from_numpy(act).to(dev)].contiguous() if self.nt else mt_all[:0]
+        # a distributed (multi-rank strip) solver shards the independent block
+        # problems by rank; the block corrections are all-gathered before the
+        # scatter, which every rank then runs over all blocks in block order
+        self.ranks = getattr(solver, "distributed_ranks", 1)
+        self.rank = getattr(solver, "rank", 0) if self.ranks > 1 else 0
+        self.chunk = -(-self.nt_all // self.ranks)
+        self.t0 = min(self.nt_all, self.rank * self.chunk)
+        self.t1 = min(self.nt_all, self.t0 + self.chunk)
+        act_loc = act[self.t0:self.t1]
+        self.nt = int(act_loc.size)
+        self.oy = torch.from_numpy(oy_all[act_loc].copy()).to(dev)
+        self.ox = torch.from_numpy(ox_all[act_loc].copy()).to(dev)
+        self.tmask = (mt_all[torch.from_numpy(act_loc).to(dev)].contiguous() if self.nt
+                      else mt_all[:0])
         rk0, rn = _cover_tables(ys, self.bh, H)
         ck0, cn = _cover_tables(xs, self.bw, W)
         self.ys_t = torch.from_numpy(ys).to(dev)
@@ -335,9 +346,21 @@ class _RasBlocks:
                  self.C, self.H, self.W, self.bh, self.bw, ptr(out), stream())
         return out
 
+    def gather_all(self, v):
+        """All ranks' block corrections in tile order (identity on one rank)."""
+        if self.ranks == 1:
+            return v
+        import torch.distributed as dist
+        pad = torch.zeros((self.chunk,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+        pad[:self.nt] = v
+        out = torch.empty((self.chunk * self.ranks,) + tuple(v.shape[1:]), dtype=v.dtype,
+                          device=v.device)
+        dist.all_gather_into_tensor(out, pad)
+        return out[:self.nt_all].contiguous()
+
     def scatter_add(self, g, v):
-        """g += sum_b T(1/cover) * v_b (tonal.py:375-380)."""
-        if self.nt:
+        """g += sum_b T(1/cover) * v_b (tonal.py:375-380); v holds all blocks."""
+        if self.nt_all:
             call("sp_ras_scatter", dcode(g), ptr(g), ptr(v), ptr(self.tile_of), ptr(self.ys_t),
                  ptr(self.xs_t), ptr(self.rk0), ptr(self.rn), ptr(self.ck0), ptr(self.cn),
                  self.nbx, self.bh, self.bw, self.C, self.H, self.W, stream())
@@ -461,7 +484,7 @@ def ras_tonal(f: Image, mask: Mask, init: TonalState | None = None,
         prev_mse = mse
         rhs, w_warm = sys_.apply_Bt(f_arr - u, warm=w_warm)
         v = blocks.normal_cg(blocks.gather(rhs), cfg.local_iters, cfg.local_tol)
-        g = blocks.scatter_add(g.clone(), v)
+        g = blocks.scatter_add(g.clone(), blocks.gather_all(v))
         outer += 1
     total_inner = sys_.solves + blocks.solves
     state = _final_state(f64, m_t, sys_, best_g, u_warm, history, outer, cfg.final_tol)
