@@ -59,6 +59,7 @@ int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
               const int* active, double* bandcol = nullptr, int band0 = 0, int nbt = 0);
 bool tma_view_ok(int W);
+int tma_prepare();  // one-time kernel attributes (outside graph capture)
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
                        int H, int W, cudaStream_t s, int ntile, const int* active);
 bool tma_prolong_ok(int H, int W);

@@ -47,6 +47,8 @@ constexpr int B_OFF = M_OFF + (M_BYTES + 127) / 128 * 128;
 constexpr int STAGE = B_OFF + (B_BYTES + 127) / 128 * 128;
 constexpr int SMEM = NS * STAGE + 128;
 constexpr int TX_BYTES = U_BYTES + M_BYTES + B_BYTES;
+// (dynamic + static shared memory exceeds the 48 KB default for MODE 1: the
+// opt-in attribute is set once by tma_prepare(), outside any graph capture)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -313,12 +315,6 @@ int launch(const float* u, const float* b, const uint8_t* m, float* r, double* p
     set_error("cuTensorMapEncodeTiled failed (%d x %d x %d)", C * ntile, H, W);
     return -1;
   }
-  static bool attr = false;
-  if (!attr) {
-    SP_CUDA(cudaFuncSetAttribute(k_resid_tma<MODE, NORMS>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr = true;
-  }
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)((long)C * ntile));
   k_resid_tma<MODE, NORMS><<<grid, CR * 32, SMEM, s>>>(mp, r, partial, counter, norms, rc, C, H,
                                                        W, active, bandcol, band0, nbt);
@@ -436,6 +432,25 @@ __global__ void __launch_bounds__(CR * 32) k_prolong_tma(
 
 }  // namespace
 
+// one-time kernel attributes (called at hierarchy / strip-group creation,
+// never inside a stream capture)
+int tma_prepare() {
+  static bool done = false;
+  if (done) return 0;
+  SP_CUDA(cudaFuncSetAttribute(k_resid_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               SMEM));
+  SP_CUDA(cudaFuncSetAttribute(k_resid_tma<0, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  SP_CUDA(cudaFuncSetAttribute(k_resid_tma<1, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  SP_CUDA(cudaFuncSetAttribute(k_prolong_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               PSMEM));
+  SP_CUDA(cudaFuncSetAttribute(k_prolong_tma<false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM));
+  done = true;
+  return 0;
+}
+
 // TMA path: float levels with W % 16 == 0 (16-byte mask row pitch for the
 // tensor map), W >= 128, 16-byte aligned buffers, and few enough CTAs per
 // plane for the partial-sum slots
@@ -476,16 +491,6 @@ int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int 
     return -1;
   }
   if (!add) mp.u = mp.m;  // unused
-  static bool attr[2] = {false, false};
-  if (!attr[add ? 1 : 0]) {
-    if (add)
-      SP_CUDA(cudaFuncSetAttribute(k_prolong_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   PSMEM));
-    else
-      SP_CUDA(cudaFuncSetAttribute(k_prolong_tma<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM));
-    attr[add ? 1 : 0] = true;
-  }
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)nz);
   if (add)
     k_prolong_tma<true><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active);

@@ -88,6 +88,7 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     set_error("block size must be at least overlap + 2");
     return -2;
   }
+  if (tma_ok(64, 128, 1) && tma_prepare()) return -1;
   Hier* h = new Hier();
   h->sweep = march_default(-1);
   h->dtype = dtype;

@@ -134,7 +134,14 @@ struct StripGroup {
   std::vector<std::vector<double*>> bandcol;  // [nloc][La] [C][nbt][ncg]
   std::vector<std::vector<double*>> bands;    // [nloc][La] [C][nbt]
   ncclComm_t comm = nullptr;                  // strips on other ranks (P > nloc)
+  // the V-cycle (kernels, halo copies / NCCL calls) recorded once as a CUDA
+  // graph on a private stream and replayed on the caller's stream
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t cap = nullptr;
+  long long graph_nodes = 0;
   ~StripGroup() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (cap) cudaStreamDestroy(cap);
     for (auto& vs : v)
       for (auto& w : vs)
         for (int* p : {w.ys, w.row_k0, w.row_n})
@@ -461,6 +468,7 @@ int strip_create(StripGroup** out, int C, int H, int W, const HierCfg& cfg, int 
     set_error("strips on other ranks need an NCCL communicator");
     return -2;
   }
+  if (tma_view_ok(128) && tma_prepare()) return -1;
   StripGroup* g = new StripGroup();
   g->P = P; g->nloc = nloc; g->first = first; g->La = La; g->halo = halo;
   g->C = C; g->H = H; g->W = W;
@@ -605,7 +613,33 @@ int strip_solve(StripGroup* g, const float* bsym, float* u_io, int init_mode, do
   }
   int done = 0, cv = 0;
   auto norms0 = [&](bool exch) -> int { return residual_norms(*g, 0, exch, s); };
-  auto cycle = [&]() -> int { return vcycle(*g, 0, true, s); };
+  auto cycle = [&]() -> int {
+    if (!g->graph) {
+      if (!g->cap) SP_CUDA(cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking));
+      // order the private capture stream after the work already queued on s
+      cudaEvent_t ev;
+      SP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      SP_CUDA(cudaEventRecord(ev, s));
+      SP_CUDA(cudaStreamWaitEvent(g->cap, ev, 0));
+      SP_CUDA(cudaStreamSynchronize(g->cap));
+      cudaEventDestroy(ev);
+      cudaGraph_t gr;
+      SP_CUDA(cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeThreadLocal));
+      int rc = vcycle(*g, 0, true, g->cap);
+      cudaError_t e = cudaStreamEndCapture(g->cap, &gr);
+      if (rc) { if (e == cudaSuccess) cudaGraphDestroy(gr); return rc; }
+      SP_CUDA(e);
+      size_t nn = 0;
+      cudaGraphGetNodes(gr, nullptr, &nn);
+      g->graph_nodes = (long long)nn;
+      cudaError_t ie = cudaGraphInstantiate(&g->graph, gr, 0);
+      cudaGraphDestroy(gr);
+      SP_CUDA(ie);
+    }
+    SP_CUDA(cudaGraphLaunch(g->graph, s));
+    count_launches(g->graph_nodes);
+    return 0;
+  };
   if (tol < 0) {
     for (int c = 0; c < cycles; ++c) {
       SP_TRY(norms0(true));
