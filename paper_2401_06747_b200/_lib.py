@@ -13,7 +13,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparsepaint_b200.so")
+# SP_B200_LIB overrides the in-tree library (A/B runs of two builds)
+LIB_PATH = os.environ.get("SP_B200_LIB") or os.path.join(_HERE, "libsparsepaint_b200.so")
 
 c_int, c_long, c_double, c_void_p = ctypes.c_int, ctypes.c_long, ctypes.c_double, ctypes.c_void_p
 P = c_void_p

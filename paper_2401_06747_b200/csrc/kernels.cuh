@@ -27,13 +27,13 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile = 1, const int* active = nullptr,
-                      int stride = 0, int corr_nb = 0);
+                      int stride = 0, int corr_nb = 0, size_t ps = 0);
 // u += weighted corrections of the covering blocks, in block order
 template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile = 1,
-                      const int* active = nullptr, int corr_nb = 0);
+                      const int* active = nullptr, int corr_nb = 0, size_t ps = 0);
 // partition-of-unity weights [nb][bh][bw] (solver.py:142-197)
 template <typename T>
 int block_weights_launch(T* weights, const int* ys, const int* xs, const int* row_k0,
@@ -57,14 +57,19 @@ int prolong_march(const float* e, float* u, const float* b, const uint8_t* m, in
 bool tma_ok(int H, int W, size_t npart);
 int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
-              const int* active, double* bandcol = nullptr, int band0 = 0, int nbt = 0);
+              const int* active, double* bandcol = nullptr, int band0 = 0, int nbt = 0,
+              size_t ps = 0);
 bool tma_view_ok(int W);
 int tma_prepare();  // one-time kernel attributes (outside graph capture)
+// ps / cps: fine / coarse plane strides in elements (0 = H*W / its coarse
+// level's); a row-strip view passes its full level's strides
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
-                       int H, int W, cudaStream_t s, int ntile, const int* active);
+                       int H, int W, cudaStream_t s, int ntile, const int* active,
+                       size_t ps = 0, size_t cps = 0);
 bool tma_prolong_ok(int H, int W);
 int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int C, int chh,
-                int cww, int H, int W, int add, cudaStream_t s, int ntile, const int* active);
+                int cww, int H, int W, int add, cudaStream_t s, int ntile, const int* active,
+                size_t ps = 0, size_t cps = 0);
 
 // ---- vec.cu ------------------------------------------------------------------
 template <typename T>

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
     const __grid_constant__ Maps mp, float* __restrict__ r, double* __restrict__ partial,
     unsigned* __restrict__ counter, double* __restrict__ norms, float* __restrict__ rcoarse,
     int C, int H, int W, const int* __restrict__ active, double* __restrict__ bandcol,
-    int band0, int nbt) {
+    int band0, int nbt, size_t ps, size_t cps) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
   __shared__ uint64_t bars[NS];
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
   if (threadIdx.x == 0)
     for (int k = 0; k < NS && k < nck; ++k) issue_chunk(mp, sm, bars, k, x0, y0 + k * CR, z, tile);
   const int xq = x0 + 4 * lane;
-  const size_t plane = (size_t)H * W;
+  const size_t plane = ps;  // plane stride (a row-strip view: the full level's)
   float sq = 0.0f;
   for (int k = 0; k < nck; ++k) {
     const int st = k % NS;
@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
             o.x = (float)(((double)a.x + (double)a.y) / 2.0);
             o.y = (float)(((double)a.z + (double)a.w) / 2.0);
           }
-          const int cw = W / 2, chh = (H + 1) / 2;
-          *reinterpret_cast<float2*>(rcoarse + (size_t)z * chh * cw + (size_t)(yf >> 1) * cw +
+          const int cw = W / 2;
+          *reinterpret_cast<float2*>(rcoarse + (size_t)z * cps + (size_t)(yf >> 1) * cw +
                                      (xq >> 1)) = o;
         }
       }
@@ -284,11 +284,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, size_t esize, int W,
-              int H, int nz, int box_w, int box_h) {
+              int H, int nz, int box_w, int box_h, size_t ps = 0) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)nz};
-  cuuint64_t strides[2] = {(cuuint64_t)W * esize, (cuuint64_t)W * H * esize};
+  cuuint64_t strides[2] = {(cuuint64_t)W * esize,
+                           (cuuint64_t)(ps ? ps : (size_t)W * H) * esize};
   cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
@@ -298,10 +299,10 @@ bool make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, size_t
 }
 
 bool make_maps(Maps& mp, const float* u, const float* b, const uint8_t* m, int C, int H, int W,
-               int ntile) {
+               int ntile, size_t ps) {
   const int nz = C * ntile;
-  return make_map(&mp.u, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, UW, CR + 2) &&
-         make_map(&mp.b, b, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, TC, CR) &&
+  return make_map(&mp.u, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, UW, CR + 2, ps) &&
+         make_map(&mp.b, b, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, TC, CR, ps) &&
          make_map(&mp.m, m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, W, H, ntile, MW, CR + 2);
 }
 
@@ -309,15 +310,17 @@ template <int MODE, bool NORMS>
 int launch(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
            unsigned* counter, double* norms, float* rc, int C, int H, int W, cudaStream_t s,
            int ntile, const int* active, double* bandcol = nullptr, int band0 = 0,
-           int nbt = 0) {
+           int nbt = 0, size_t ps = 0, size_t cps = 0) {
+  if (!ps) ps = (size_t)H * W;
+  if (!cps) cps = (size_t)((H + 1) / 2) * (W / 2);
   Maps mp;
-  if (!make_maps(mp, u, b, m, C, H, W, ntile)) {
+  if (!make_maps(mp, u, b, m, C, H, W, ntile, ps)) {
     set_error("cuTensorMapEncodeTiled failed (%d x %d x %d)", C * ntile, H, W);
     return -1;
   }
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)((long)C * ntile));
   k_resid_tma<MODE, NORMS><<<grid, CR * 32, SMEM, s>>>(mp, r, partial, counter, norms, rc, C, H,
-                                                       W, active, bandcol, band0, nbt);
+                                                       W, active, bandcol, band0, nbt, ps, cps);
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -357,7 +360,7 @@ template <bool ADD>
 __global__ void __launch_bounds__(CR * 32) k_prolong_tma(
     const __grid_constant__ PMaps mp, float* __restrict__ u, const float* __restrict__ b,
     const uint8_t* __restrict__ m, int C, int chh, int cww, int H, int W,
-    const int* __restrict__ active) {
+    const int* __restrict__ active, size_t ps) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
   __shared__ uint64_t bars[NS];
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(CR * 32) k_prolong_tma(
   if (threadIdx.x == 0)
     for (int k = 0; k < NS && k < nck; ++k) issue(k, y0 + k * CR);
   const int xq = x0 + 4 * lane;
-  const size_t plane = (size_t)H * W;
+  const size_t plane = ps;
   // x interpolation of the lane's 4 pixels (chunk-independent)
   int xa[4], xb[4];
   double wx[4];
@@ -469,10 +472,10 @@ bool tma_ok(int H, int W, size_t npart) {
 
 int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
-              const int* active, double* bandcol, int band0, int nbt) {
+              const int* active, double* bandcol, int band0, int nbt, size_t ps) {
   if (bandcol)
     return launch<0, true>(u, b, m, r, partial, counter, nullptr, nullptr, C, H, W, s, ntile,
-                           active, bandcol, band0, nbt);
+                           active, bandcol, band0, nbt, ps);
   if (norms)
     return launch<0, true>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
                            active);
@@ -481,29 +484,35 @@ int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double
 }
 
 int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int C, int chh,
-                int cww, int H, int W, int add, cudaStream_t s, int ntile, const int* active) {
+                int cww, int H, int W, int add, cudaStream_t s, int ntile, const int* active,
+                size_t ps, size_t cps) {
+  if (!ps) ps = (size_t)H * W;
+  if (!cps) cps = (size_t)chh * cww;
   PMaps mp;
   const int nz = C * ntile;
-  if ((add && !make_map(&mp.u, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, TC, CR)) ||
+  if ((add && !make_map(&mp.u, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, nz, TC, CR, ps)) ||
       !make_map(&mp.m, m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, W, H, ntile, TC, CR) ||
-      !make_map(&mp.e, e, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cww, chh, nz, EW, EH)) {
+      !make_map(&mp.e, e, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cww, chh, nz, EW, EH, cps)) {
     set_error("cuTensorMapEncodeTiled failed (prolongation %d x %d x %d)", nz, H, W);
     return -1;
   }
   if (!add) mp.u = mp.m;  // unused
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)nz);
   if (add)
-    k_prolong_tma<true><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active);
+    k_prolong_tma<true><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active,
+                                                     ps);
   else
-    k_prolong_tma<false><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active);
+    k_prolong_tma<false><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active,
+                                                      ps);
   SP_CHECK_LAUNCH();
   return 0;
 }
 
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
-                       int H, int W, cudaStream_t s, int ntile, const int* active) {
+                       int H, int W, cudaStream_t s, int ntile, const int* active, size_t ps,
+                       size_t cps) {
   return launch<1, false>(u, b, m, nullptr, nullptr, nullptr, nullptr, rc, C, H, W, s, ntile,
-                          active);
+                          active, nullptr, 0, 0, ps, cps);
 }
 
 }  // namespace sp

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
     const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W, int stride,
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
-    float* __restrict__ corr, const int* __restrict__ active, int corr_nb) {
+    float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps) {
   __shared__ float er_top[NWJ][32], er_bot[NWJ][32];  // edge rows of r (new)
   __shared__ double red_a[NWJ], red_b[NWJ];
   // corr_nb: blocks per channel plane of `corr` (a row-strip view launches a
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
   const int kyb = bi / nbx, kxb = bi - kyb * nbx;
   const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
   const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
-  const size_t plane = (size_t)H * W;
+  const size_t plane = ps;  // channel-plane stride (row-strip views: the level's)
   const float* rc = r + ((size_t)tile * C + ch) * plane;
   const uint8_t* mt = m + (size_t)tile * plane;
   const bool lane_ok = j < bw;
@@ -418,17 +418,27 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
 
   // ---- load the job: residual rows, mask bits (own rows + the row above
   // and below the warp's band), validity
+  // branch-free: every row is loaded from a clamped (valid) address and the
+  // invalid ones are zeroed afterwards, so the 8 + 8 loads issue back to
+  // back (a branch per row serialises their DRAM latencies)
   float res[RW];
+  uint8_t mk[RW];
   uint32_t mb = 0, vb = 0;
+  const int jc = lane_ok ? j : bw - 1;
 #pragma unroll
   for (int s = 0; s < RW; ++s) {
-    const int i = i0 + s;
-    res[s] = 0.0f;
-    if (i < bh && lane_ok) {
-      const size_t g = (size_t)(y0 + i) * W + gx;
-      res[s] = rc[g];
-      if (mt[g]) mb |= 1u << s;
+    const int ic = min(i0 + s, bh - 1);
+    const size_t g = (size_t)(y0 + ic) * W + (x0 + jc);
+    res[s] = rc[g];
+    mk[s] = mt[g];
+  }
+#pragma unroll
+  for (int s = 0; s < RW; ++s) {
+    const bool ok = i0 + s < bh && lane_ok;
+    res[s] = ok ? res[s] : 0.0f;
+    if (ok) {
       vb |= 1u << s;
+      if (mk[s]) mb |= 1u << s;
     }
   }
   const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
@@ -776,12 +786,12 @@ __global__ void __launch_bounds__(256) k_oras_blend(
     const int* __restrict__ xs, const int* __restrict__ row_k0,
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
     const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int Cdyn,
-    const int* __restrict__ active, int corr_nb) {
+    const int* __restrict__ active, int corr_nb, size_t ps) {
   const int C = CM > 0 ? CM : Cdyn;
   const int tile = blockIdx.y;
   if (active && !active[tile]) return;
   const int nb = corr_nb > 0 ? corr_nb : nby * nbx;
-  const size_t plane = (size_t)H * W, npx = (size_t)bh * bw, cplane = (size_t)nb * npx;
+  const size_t plane = ps, npx = (size_t)bh * bw, cplane = (size_t)nb * npx;
   T* ut = u + (size_t)tile * C * plane;
   const T* ct = corr + (size_t)tile * C * cplane;
   constexpr int CC = CM > 0 ? CM : 4;
@@ -883,11 +893,11 @@ __global__ void __launch_bounds__(256) k_oras_blend_plane(
     const int* __restrict__ xs, const int* __restrict__ row_k0,
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
     const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int C,
-    const int* __restrict__ active, int corr_nb) {
+    const int* __restrict__ active, int corr_nb, size_t ps) {
   const int z = blockIdx.y, tile = z / C;
   if (active && !active[tile]) return;
   const int nb = corr_nb > 0 ? corr_nb : nby * nbx;
-  const size_t plane = (size_t)H * W, npx = (size_t)bh * bw;
+  const size_t plane = ps, npx = (size_t)bh * bw;
   T* uc = u + (size_t)z * plane;
   const T* cc = corr + (size_t)z * nb * npx;
   const int ntx = (W + 31) / 32, nty = (H + 7) / 8, per = ntx * nty;
@@ -915,8 +925,14 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile, const int* active, int stride,
-                      int corr_nb) {
+                      int corr_nb, size_t ps) {
   const int npx = bh * bw;
+  if (ps && ps != (size_t)H * W &&
+      !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && (oras_kernel == 0 || oras_kernel == 2))) {
+    set_error("plane-strided ORAS launches need the float 32x32 4-warp kernel");
+    return -2;
+  }
+  if (!ps) ps = (size_t)H * W;
   if (corr_nb > 0 && !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1)) {
     set_error("block sub-range launches need the float 32x32 ORAS kernel");
     return -2;
@@ -924,7 +940,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
   if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 3 && W % 4 == 0 &&
-      ((uintptr_t)m & 3) == 0) {
+      ((uintptr_t)m & 3) == 0 && ps == (size_t)H * W) {
     const long njobs = (long)nby * nbx * C * ntile;
     static int occ = 0;
     if (!occ) {
@@ -941,7 +957,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
     kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
                               W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
-                              (const float*)weights, (float*)corr, active, corr_nb);
+                              (const float*)weights, (float*)corr, active, corr_nb, ps);
   } else if (bw == 32 && bh <= 32) {
     k_oras_local32<T><<<grid, NT, 0, s>>>(r, m, tau_src, tau_scale, ys, xs, nbx, bh, H, W,
                                           stride, gamma, cap, inv_h2, weights, corr, active);
@@ -966,7 +982,8 @@ template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile,
-                      const int* active, int corr_nb) {
+                      const int* active, int corr_nb, size_t ps) {
+  if (!ps) ps = (size_t)H * W;
   long per = (long)cdiv(W, 32) * cdiv(H, C <= 4 ? 16 : 8);
   long nz = C <= 4 ? (long)ntile : (long)ntile * C;
   long nbx_cta = (2L * 148 * 8 + nz - 1) / nz;
@@ -975,13 +992,13 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   dim3 grid((unsigned)nbx_cta, (unsigned)nz), blk(32, 8);
 #define SP_BLEND(CM)                                                                      \
   k_oras_blend<T, CM><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n, \
-                                          nby, nbx, bh, bw, H, W, C, active, corr_nb)
+                                          nby, nbx, bh, bw, H, W, C, active, corr_nb, ps)
   if (C == 1) SP_BLEND(1);
   else if (C == 3) SP_BLEND(3);
   else if (C <= 4) SP_BLEND(0);
   else
     k_oras_blend_plane<T><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n,
-                                               nby, nbx, bh, bw, H, W, C, active, corr_nb);
+                                               nby, nbx, bh, bw, H, W, C, active, corr_nb, ps);
 #undef SP_BLEND
   SP_CHECK_LAUNCH();
   return 0;
@@ -1003,10 +1020,11 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
   template int oras_local_launch<T>(const T*, const uint8_t*, const double*, double,        \
                                     const int*, const int*, int, int, int, int, int, int,   \
                                     int, double, long, double, const T*, T*, cudaStream_t,  \
-                                    int, const int*, int, int);                             \
+                                    int, const int*, int, int, size_t);                     \
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
-                                    int, int, int, cudaStream_t, int, const int*, int);     \
+                                    int, int, int, cudaStream_t, int, const int*, int,      \
+                                    size_t);                                                \
   template int block_weights_launch<T>(T*, const int*, const int*, const int*, const int*,  \
                                        const int*, const int*, int, int, int, int, int,     \
                                        int, int, cudaStream_t);

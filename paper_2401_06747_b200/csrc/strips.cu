@@ -274,17 +274,18 @@ int residual_norms(StripGroup& g, int lv, bool exch, cudaStream_t s) {
     const StripView& V = g.v[i][lv];
     Level& L = g.h[i]->lv[lv];
     const int hv = V.e1 - V.e0;
-    const bool tma = tma_view_ok(L.W);
-    for (int c = 0; c < g.C; ++c) {
-      double* bc = g.bandcol[i][lv] + (size_t)c * g.nbt[lv] * g.ncg[lv];
-      if (tma)
-        SP_TRY(resid_tma(rowp(L.u, L, c, V.e0), rowp(L.b, L, c, V.e0), mrow(L, V.e0),
-                         rowp(L.r, L, c, V.e0), nullptr, nullptr, nullptr, 1, hv, L.W, s, 1,
-                         nullptr, bc, V.e0 / BR, g.nbt[lv]));
-      else
+    const size_t ps = (size_t)L.H * L.W;
+    if (tma_view_ok(L.W)) {
+      // all channels in one launch: the view's planes keep the level's stride
+      SP_TRY(resid_tma(rowp(L.u, L, 0, V.e0), rowp(L.b, L, 0, V.e0), mrow(L, V.e0),
+                       rowp(L.r, L, 0, V.e0), nullptr, nullptr, nullptr, g.C, hv, L.W, s, 1,
+                       nullptr, g.bandcol[i][lv], V.e0 / BR, g.nbt[lv], ps));
+    } else {
+      for (int c = 0; c < g.C; ++c)
         SP_TRY(resid_march(rowp(L.u, L, c, V.e0), rowp(L.b, L, c, V.e0), mrow(L, V.e0),
                            rowp(L.r, L, c, V.e0), nullptr, nullptr, nullptr, 1, hv, L.W, s, 1,
-                           nullptr, bc, V.e0 / BR, g.nbt[lv]));
+                           nullptr, g.bandcol[i][lv] + (size_t)c * g.nbt[lv] * g.ncg[lv],
+                           V.e0 / BR, g.nbt[lv]));
     }
     const int n = g.C * g.nbt[lv];
     k_band_sum<<<cdiv(n, 256), 256, 0, s>>>(g.bandcol[i][lv], g.bands[i][lv], g.C, g.nbt[lv],
@@ -316,12 +317,17 @@ int residual_norms(StripGroup& g, int lv, bool exch, cudaStream_t s) {
   return 0;
 }
 
-// u (+)= P e on a view, one channel plane
-int prolong_view(const float* e, float* u, const float* b, const uint8_t* m, int chh, int cww,
-                 int hv, int W, int add, cudaStream_t s) {
-  if (tma_prolong_ok(hv, W))
-    return prolong_tma(e, u, b, m, 1, chh, cww, hv, W, add, s, 1, nullptr);
-  return prolong_march(e, u, b, m, 1, chh, cww, hv, W, add, s, 1, nullptr);
+// u (+)= P e on a view (coarse view from row e0 / 2, ch rows)
+int prolong_view(StripGroup& g, Level& F, Level& G, const StripView& V, int ch, int hv,
+                 int add, cudaStream_t s) {
+  if (tma_prolong_ok(hv, F.W))
+    return prolong_tma(rowp(G.u, G, 0, V.e0 / 2), rowp(F.u, F, 0, V.e0), rowp(F.b, F, 0, V.e0),
+                       mrow(F, V.e0), g.C, ch, G.W, hv, F.W, add, s, 1, nullptr,
+                       (size_t)F.H * F.W, (size_t)G.H * G.W);
+  for (int c = 0; c < g.C; ++c)
+    SP_TRY(prolong_march(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0), rowp(F.b, F, c, V.e0),
+                         mrow(F, V.e0), 1, ch, G.W, hv, F.W, add, s, 1, nullptr));
+  return 0;
 }
 
 int oras_blend(StripGroup& g, int lv, cudaStream_t s) {
@@ -330,18 +336,17 @@ int oras_blend(StripGroup& g, int lv, cudaStream_t s) {
     const StripView& V = g.v[i][lv];
     Level& L = hh->lv[lv];
     const int hv = V.e1 - V.e0, npx = L.bh * L.bw, nb = L.nby * L.nbx;
-    const size_t boff = (size_t)V.kya * L.nbx * npx;
-    for (int c = 0; c < g.C; ++c) {
-      float* corr = (float*)L.corr + (size_t)c * nb * npx + boff;
-      SP_TRY(oras_local_launch<float>(rowp(L.r, L, c, V.e0), mrow(L, V.e0), L.norms + c,
-                                      L.tau_scale, V.ys, L.xs, V.nby, L.nbx, L.bh, L.bw, hv,
-                                      L.W, 1, hh->gamma, (long)npx, 1.0,
-                                      (const float*)L.weights + boff, corr, s, 1, nullptr, 0,
-                                      nb));
-      SP_TRY(oras_blend_launch<float>(rowp(L.u, L, c, V.e0), corr, V.ys, L.xs, V.row_k0,
-                                      V.row_n, L.col_k0, L.col_n, V.nby, L.nbx, L.bh, L.bw, hv,
-                                      L.W, 1, s, 1, nullptr, nb));
-    }
+    const size_t boff = (size_t)V.kya * L.nbx * npx, ps = (size_t)L.H * L.W;
+    // all channels in one launch: corr channel planes keep the level's
+    // block count (corr_nb), image planes the level's stride (ps)
+    float* corr = (float*)L.corr + boff;
+    SP_TRY(oras_local_launch<float>(rowp(L.r, L, 0, V.e0), mrow(L, V.e0), L.norms, L.tau_scale,
+                                    V.ys, L.xs, V.nby, L.nbx, L.bh, L.bw, hv, L.W, g.C,
+                                    hh->gamma, (long)npx, 1.0, (const float*)L.weights + boff,
+                                    corr, s, 1, nullptr, 0, nb, ps));
+    SP_TRY(oras_blend_launch<float>(rowp(L.u, L, 0, V.e0), corr, V.ys, L.xs, V.row_k0,
+                                    V.row_n, L.col_k0, L.col_n, V.nby, L.nbx, L.bh, L.bw, hv,
+                                    L.W, g.C, s, 1, nullptr, nb, ps));
   }
   return 0;
 }
@@ -364,12 +369,12 @@ int vcycle(StripGroup& g, int lv, bool first_done, cudaStream_t s) {
     const StripView& V = g.v[i][lv];
     Level& F = g.h[i]->lv[lv];
     Level& G = g.h[i]->lv[lv + 1];
-    for (int c = 0; c < g.C; ++c) {
-      if (tma_view_ok(F.W))
-        SP_TRY(resid_restrict_tma(rowp(F.u, F, c, V.e0), rowp(F.b, F, c, V.e0), mrow(F, V.e0),
-                                  rowp(G.r, G, c, V.e0 / 2), 1, V.e1 - V.e0, F.W, s, 1,
-                                  nullptr));
-      else
+    if (tma_view_ok(F.W)) {
+      SP_TRY(resid_restrict_tma(rowp(F.u, F, 0, V.e0), rowp(F.b, F, 0, V.e0), mrow(F, V.e0),
+                                rowp(G.r, G, 0, V.e0 / 2), g.C, V.e1 - V.e0, F.W, s, 1, nullptr,
+                                (size_t)F.H * F.W, (size_t)G.H * G.W));
+    } else {
+      for (int c = 0; c < g.C; ++c)
         SP_TRY(resid_restrict_march(rowp(F.u, F, c, V.e0), rowp(F.b, F, c, V.e0),
                                     mrow(F, V.e0), rowp(G.r, G, c, V.e0 / 2), 1, V.e1 - V.e0,
                                     F.W, s, 1, nullptr));
@@ -407,9 +412,7 @@ int vcycle(StripGroup& g, int lv, bool first_done, cudaStream_t s) {
     Level& F = g.h[i]->lv[lv];
     Level& G = g.h[i]->lv[lv + 1];
     const int hv = V.e1 - V.e0, ch = std::min((hv + 1) / 2, G.H - V.e0 / 2);
-    for (int c = 0; c < g.C; ++c)
-      SP_TRY(prolong_view(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0),
-                          rowp(F.b, F, c, V.e0), mrow(F, V.e0), ch, G.W, hv, F.W, 1, s));
+    SP_TRY(prolong_view(g, F, G, V, ch, hv, 1, s));
   }
   SP_TRY(smooth(g, lv, cfg.post, false, s));
   return 0;
@@ -440,12 +443,10 @@ int cascade(StripGroup& g, cudaStream_t s) {
       Level& F = g.h[i]->lv[lv];
       Level& G = g.h[i]->lv[lv + 1];
       const int hv = V.e1 - V.e0, ch = std::min((hv + 1) / 2, G.H - V.e0 / 2);
-      for (int c = 0; c < g.C; ++c) {
+      for (int c = 0; c < g.C; ++c)
         SP_TRY(masked_sym_rhs<float>(rowp(F.values, F, c, V.e0), mrow(F, V.e0),
                                      rowp(F.b, F, c, V.e0), 1, hv, F.W, s));
-        SP_TRY(prolong_view(rowp(G.u, G, c, V.e0 / 2), rowp(F.u, F, c, V.e0),
-                            rowp(F.b, F, c, V.e0), mrow(F, V.e0), ch, G.W, hv, F.W, 0, s));
-      }
+      SP_TRY(prolong_view(g, F, G, V, ch, hv, 0, s));
     }
     SP_TRY(smooth(g, lv, 1, false, s));
   }
