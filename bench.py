@@ -299,8 +299,9 @@ def run_ours(args):
     for _ in range(args.steps):
         m_e, st_e, _, _ = sp.run_pipeline(sp.Image(f_pinned), cfg, solver=solver)
         mask_h = m_e.indicator          # D2H: mask
-        g_h = st_e.g.data               # D2H: stored values
-        d2h = mask_h.nbytes + g_h.nbytes
+        g_h = st_e.g.data               # D2H: stored values (moved sparsely:
+        n_st = int(mask_h.sum())        # indices + values of the stored pixels)
+        d2h = mask_h.nbytes + n_st * (8 + C * g_h.itemsize)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.steps
     e2e_s = _max_over_ranks(e2e_s, world)

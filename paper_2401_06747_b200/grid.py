@@ -74,12 +74,32 @@ class Image:
             self._host = arr
             self._dev = None
 
+    @classmethod
+    def sparse(cls, t: torch.Tensor, support: torch.Tensor) -> "Image":
+        """A device image that is zero outside `support` (H, W) -- e.g. the
+        stored tonal values g: the host copy moves only the supported
+        values (5% of the pixels) and scatters them into zeros."""
+        img = cls(t)
+        img._support = support
+        return img
+
     # -- storage -----------------------------------------------------------
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            self._host = _to_host(self._dev)
+            sup = getattr(self, "_support", None)
+            if sup is not None and self._dev.is_cuda:
+                C = self._dev.shape[0]
+                idx = torch.nonzero(sup.reshape(-1)).squeeze(1)
+                vals = self._dev.reshape(C, -1)[:, idx]
+                npdt = np.float32 if self._dev.dtype == torch.float32 else np.float64
+                out = np.zeros(tuple(self._dev.shape), dtype=npdt)
+                out.reshape(C, -1)[:, _to_host(idx)] = _to_host(vals)
+                self._host = out
+            else:
+                self._host = _to_host(self._dev)
             self._dev = None
+            self._support = None
         return self._host
 
     @data.setter

@@ -189,7 +189,10 @@ def _final_state(f64, mask_t, sys_: _TonalSystem, g_best, warm, history, iterati
     u, rep = sys_.hier.solve_sym(bsym, init=warm, tol=final_tol)
     sys_.solves += 1
     _enforce(u, g_best.to(u.dtype).contiguous(), mask_t)
-    return TonalState(g=Image(g_best.clone()), u=Image(u), mse=mse_t(f64, u),
+    # g is zero off the mask by construction; make it exact and let the host
+    # copy move only the stored values
+    g_out = _where_mask(g_best.contiguous(), mask_t)
+    return TonalState(g=Image.sparse(g_out, mask_t), u=Image(u), mse=mse_t(f64, u),
                       history=history, iterations=iterations, inner_solves=sys_.solves,
                       converged=rep.converged)
 
