@@ -50,6 +50,25 @@ REF_SAMPLE = (128, 128, 3)
 REF_SLOPE = 0.789
 
 
+def _ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one finest-level 4K
+    launch of `kernel` from the newest committed ncu --set full summary
+    (profiles/ncu_<tag>_<kernel>.txt, scripts/summarize_prof.py), or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_*_{kernel}.txt")),
+                   key=os.path.getmtime)
+    if not files:
+        return None
+    tot = 0.0
+    for line in open(files[-1]):
+        m = re.match(r"dram__bytes_(read|write)\.sum\s+([\d.]+)\s+(\w+)", line)
+        if m:
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(3), 1)
+            tot += float(m.group(2)) * scale
+    return {"bytes": tot, "source": os.path.relpath(files[-1], ROOT)} if tot else None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -316,8 +335,8 @@ def run_ours(args):
     bsym = _masked_rhs(f_dev.float().contiguous(), mask.tensor())
     hier.solve_sym(bsym, tol=1e-4, cascade=True)
     import ctypes
-    names = {0: "k4_residual (sym_residual sweep)", 1: "k_oras_rows (ORAS local CG)",
-             2: "k_oras_blend", 3: "k4_residual_restrict"}
+    names = {0: "k_resid_tma (sym_residual sweep)", 1: "k_oras_rows (ORAS local CG)",
+             2: "k_oras_blend", 3: "k_resid_tma<1> (residual + restriction)"}
     for which in (0, 1, 2, 3):
         t_ms, nbytes = ctypes.c_double(), ctypes.c_double()
         _lib.call("sp_hier_bench", hier._h, which, 20, ctypes.byref(t_ms), ctypes.byref(nbytes),
@@ -326,14 +345,20 @@ def run_ours(args):
         kern[names[which]] = {"us": t_ms.value * 1e3, "bytes": nbytes.value,
                               "gbs": gbs, "frac": gbs / peak}
     dom = names[1]
+    tr = _ncu_traffic("k_oras_rows")
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
-            "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": None,
+            "unit": "GB/s", "frac": kern[dom]["frac"],
+            "traffic": tr["bytes"] if tr else None,
+            "traffic_source": tr["source"] if tr else None,
             "peak_kind": peak_kind,
             "note": "dominant kernel = ORAS local CG (on-chip, latency bound); "
                     "stencil sweep roofline in `stencil_roofline`"}
     sten = names[0]
+    trs = _ncu_traffic("k_resid_tma")
     stencil_roofline = {"bound": "hbm", "kernel": sten, "achieved": kern[sten]["gbs"],
-                        "peak": peak, "unit": "GB/s", "frac": kern[sten]["frac"]}
+                        "peak": peak, "unit": "GB/s", "frac": kern[sten]["frac"],
+                        "traffic": trs["bytes"] if trs else None,
+                        "traffic_source": trs["source"] if trs else None}
 
     strips = None if args.no_strips else run_strips(world, rank)
 
