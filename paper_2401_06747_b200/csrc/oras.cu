@@ -42,7 +42,7 @@ __device__ int g_stats_on;
 // stencil, 3 = persistent k_oras_rows_p with cp.async prefetch of the next
 // job (it removes the load stalls but issues 32% more instructions and
 // loses: 1.80 vs 1.58 ms per 4K V-cycle, profiles/oras_ab_r01j.txt)
-static int oras_kernel = 0;
+static int oras_kernel = 4;
 int oras_variant(int v) {
   if (v >= 0) oras_kernel = v;
   return oras_kernel;
@@ -461,6 +461,172 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
     if ((vb >> s) & 1u) out[i * bw + j] = wb[i * bw + j] * v[s];
   }
   if (threadIdx.x == 0 && g_stats_on) {
+    atomicAdd(&g_oras_stats[0], 1ull);
+    atomicAdd(&g_oras_stats[1], (unsigned long long)it);
+    if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
+    atomicMax(&g_oras_stats[3], (unsigned long long)it);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One WARP per (block, channel, tile) job (sp_oras_variant 4): lane j owns
+// column j and all 32 rows of the block in registers, so the local CG needs
+// no shared memory and no barrier at all -- up/down neighbours are adjacent
+// registers, left/right one shuffle each, and the dots are warp reductions.
+// A CTA holds 4 independent jobs (consecutive blocks).
+//
+// The arithmetic is bit-identical to k_oras_rows: the same per-pixel fused
+// operations, the dot partials accumulated in float over the same 8-row
+// groups (rows 8g..8g+7, one accumulator per group -- which also gives the
+// chain 4-way ILP), each group reduced over the 32 lanes by the same xor
+// butterfly (done for the 4 groups at once by the transpose trick: 6
+// shuffles instead of 20; IEEE addition is commutative, so every pair sum
+// is the one the butterfly forms) and the 4 group sums added in double in
+// group order.  tests/test_solver_gpu.py checks the two kernels agree
+// bitwise.
+// ---------------------------------------------------------------------------
+constexpr int WJ = 4;  // jobs (warps) per CTA
+
+// the xor-butterfly sums of x[0..3] over the warp, all four in every lane
+__device__ __forceinline__ void warp_sum4(const float (&x)[4], float (&t)[4], int j) {
+  const bool hi16 = j & 16, hi8 = j & 8;
+  // o = 16: keep groups {0,1} (low half) or {2,3} (high half)
+  const float s0 = hi16 ? x[0] : x[2], s1 = hi16 ? x[1] : x[3];
+  const float k0 = hi16 ? x[2] : x[0], k1 = hi16 ? x[3] : x[1];
+  const float y0 = k0 + __shfl_xor_sync(0xFFFFFFFFu, s0, 16);
+  const float y1 = k1 + __shfl_xor_sync(0xFFFFFFFFu, s1, 16);
+  // o = 8: keep the first or second of the pair
+  const float sd = hi8 ? y0 : y1, kp = hi8 ? y1 : y0;
+  float z = kp + __shfl_xor_sync(0xFFFFFFFFu, sd, 8);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) z += __shfl_xor_sync(0xFFFFFFFFu, z, o);
+  // lanes 0 / 8 / 16 / 24 hold the totals of groups 0 / 1 / 2 / 3
+#pragma unroll
+  for (int g = 0; g < 4; ++g) t[g] = __shfl_sync(0xFFFFFFFFu, z, 8 * g);
+}
+
+__device__ __forceinline__ double sum4_double(const float (&t)[4]) {
+  double s = 0.0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) s += (double)t[g];
+  return s;
+}
+
+template <bool UNIT_H, bool FULLH>
+__global__ void __launch_bounds__(WJ * 32, 3) k_oras_warp(
+    const float* __restrict__ r, const uint8_t* __restrict__ m,
+    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
+    const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
+    float closure, long cap, float inv_h2, const float* __restrict__ weights,
+    float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps) {
+  constexpr int R = 32;
+  const int j = threadIdx.x & 31;
+  const int bi = blockIdx.x * WJ + (threadIdx.x >> 5), ch = blockIdx.y, C = gridDim.y;
+  const int tile = blockIdx.z;
+  if (bi >= nbl) return;
+  if (active && !active[tile]) return;
+  const int nb = corr_nb > 0 ? corr_nb : nbl;
+  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
+  const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
+  const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
+  const float* rc = r + ((size_t)tile * C + ch) * ps;
+  const uint8_t* mt = m + (size_t)tile * ps;
+  const bool lane_ok = j < bw;
+  const int jc = lane_ok ? j : bw - 1, gx = x0 + j;
+
+  // ---- load the job (branch-free, clamped addresses; invalid zeroed)
+  float res[R];
+  uint8_t mk[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int ic = FULLH ? s : min(s, bh - 1);
+    const size_t g = (size_t)(y0 + ic) * W + (x0 + jc);
+    res[s] = rc[g];
+    mk[s] = mt[g];
+  }
+  // off: bit s set where row s is masked or outside the block (q = 0 there,
+  // and A p = p, which is 0 outside the block)
+  uint32_t off = 0;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const bool ok = (FULLH || s < bh) && lane_ok;
+    res[s] = ok ? res[s] : 0.0f;
+    if (!ok || mk[s]) off |= 1u << s;
+  }
+  // Robin-closed diagonal of the three row classes (k_oras_rows' float
+  // addition order): top row, interior rows, bottom row
+  auto diag_of = [&](int i) {
+    const int gy = y0 + i;
+    float d = 0.0f;
+    if (gy > 0) d += i > 0 ? 1.0f : closure;
+    if (gy < H - 1) d += i < bh - 1 ? 1.0f : closure;
+    if (gx > 0) d += j > 0 ? 1.0f : closure;
+    if (gx < W - 1) d += j < bw - 1 ? 1.0f : closure;
+    return d * inv_h2;
+  };
+  const float dtop = diag_of(0), dmid = diag_of(1), dbot = diag_of(bh - 1);
+  const float lf = j > 0 ? 1.0f : 0.0f, rt = j < bw - 1 ? 1.0f : 0.0f;
+  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
+
+  float p[R], v[R], ap[R];
+  float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f}, t4[4];
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    p[s] = res[s];
+    v[s] = 0.0f;
+    acc4[s >> 3] = __fmaf_rn(res[s], res[s], acc4[s >> 3]);
+  }
+  warp_sum4(acc4, t4, j);
+  double rs = sum4_double(t4);
+  long it = 0;
+  while (rs > tau && it < cap) {
+    float q[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) q[s] = ((off >> s) & 1u) ? 0.0f : p[s];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const float ql = __shfl_up_sync(0xFFFFFFFFu, q[s], 1);
+      const float qr = __shfl_down_sync(0xFFFFFFFFu, q[s], 1);
+      const float up = s > 0 ? q[s - 1] : 0.0f;
+      const float dn = s < R - 1 ? q[s + 1] : 0.0f;
+      const float acc = __fmaf_rn(qr, rt, __fmaf_rn(ql, lf, up + dn));
+      float dg;
+      if (FULLH) dg = s == 0 ? dtop : (s == R - 1 ? dbot : dmid);
+      else dg = s == 0 ? dtop : (s == bh - 1 ? dbot : dmid);
+      const float a = __fmaf_rn(dg, p[s], UNIT_H ? -acc : -(acc * inv_h2));
+      ap[s] = ((off >> s) & 1u) ? p[s] : a;
+      acc4[s >> 3] = __fmaf_rn(p[s], ap[s], acc4[s >> 3]);
+    }
+    warp_sum4(acc4, t4, j);
+    const double pap = sum4_double(t4);
+    if (pap <= 0.0) break;
+    const float alpha = (float)rs / (float)pap;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      v[s] = __fmaf_rn(alpha, p[s], v[s]);
+      res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
+      acc4[s >> 3] = __fmaf_rn(res[s], res[s], acc4[s >> 3]);
+    }
+    warp_sum4(acc4, t4, j);
+    const double rsn = sum4_double(t4);
+    const float beta = (float)rsn / (float)rs;
+    rs = rsn;
+#pragma unroll
+    for (int s = 0; s < R; ++s) p[s] = __fmaf_rn(beta, p[s], res[s]);
+    ++it;
+  }
+  float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
+  const float* wb = weights + (size_t)bi * bh * bw;
+  if (lane_ok) {
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if (FULLH || s < bh) out[s * bw + j] = wb[s * bw + j] * v[s];
+  }
+  if (j == 0 && g_stats_on) {
     atomicAdd(&g_oras_stats[0], 1ull);
     atomicAdd(&g_oras_stats[1], (unsigned long long)it);
     if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
@@ -928,7 +1094,8 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       int corr_nb, size_t ps) {
   const int npx = bh * bw;
   if (ps && ps != (size_t)H * W &&
-      !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && (oras_kernel == 0 || oras_kernel == 2))) {
+      !(sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
+        (oras_kernel == 0 || oras_kernel == 2 || oras_kernel == 4))) {
     set_error("plane-strided ORAS launches need the float 32x32 4-warp kernel");
     return -2;
   }
@@ -953,6 +1120,15 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                                      nby * nbx, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
                                      (float)inv_h2, (const float*)weights, (float*)corr, active,
                                      corr_nb, C, njobs);
+  } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 4) {
+    const int nbl = nby * nbx;
+    dim3 g4(cdiv(nbl, WJ), C, ntile);
+    const bool unit = inv_h2 == 1.0, full = bh == 32;
+    auto kern = unit ? (full ? k_oras_warp<true, true> : k_oras_warp<true, false>)
+                     : (full ? k_oras_warp<false, true> : k_oras_warp<false, false>);
+    kern<<<g4, WJ * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
+                                bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
+                                (const float*)weights, (float*)corr, active, corr_nb, ps);
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
     kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,

@@ -13,7 +13,8 @@ for dens in (0.05, 0.0024):
     mask = (np.random.default_rng(2).random((H, W)) < dens).astype(np.uint8)
     fi, mi = sp.Image(torch.from_numpy(f).cuda()), sp.Mask(torch.from_numpy(mask).cuda())
     u, rep = sp.inpaint(fi, mi)
-    for var, mv in ((0, 2), (2, 2), (0, 0), (0, 2)):
+    VARS = [tuple(map(int, a.split(':'))) for a in sys.argv[1:]] or [(0, 2), (4, 2), (0, 2), (4, 2)]
+    for var, mv in VARS:
         lib.sp_oras_variant(var)
         lib.sp_march_variant(mv)
         sp.solver._POOL.clear()

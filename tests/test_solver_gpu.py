@@ -124,3 +124,51 @@ def test_sweep_kernel_residuals_bit_identical(shape):
     for v in (1, 2):
         assert np.array_equal(res[v][0], res[0][0])
         assert np.allclose(res[v][1], res[0][1], rtol=1e-6, atol=0)
+
+
+def _with_oras_variant(v, fn):
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    prev = lib.sp_oras_variant(-1)
+    try:
+        lib.sp_oras_variant(v)
+        _POOL.clear()
+        return fn()
+    finally:
+        lib.sp_oras_variant(prev)
+        _POOL.clear()
+
+
+@pytest.mark.parametrize("shape", [(3, 301, 512), (1, 100, 150), (3, 40, 70)])
+def test_oras_warp_kernel_bit_identical(shape):
+    """One-warp-per-job ORAS local CG (k_oras_warp, variant 4) vs the 4-warp
+    k_oras_rows (variant 0): same fused operations, same 8-row dot groups
+    and butterfly pairings, so the V-cycles agree bitwise -- on full 32-row
+    blocks and on the short blocks of small / coarse levels."""
+    import paper_2401_06747_b200 as sp
+    c, h, w = shape
+    f = O.synth(h, w, c, 3)
+    mask = (np.random.default_rng(4).random((h, w)) < 0.05).astype(np.uint8)
+
+    def run():
+        u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
+        return u.data
+
+    a, b = _with_oras_variant(0, run), _with_oras_variant(4, run)
+    assert np.array_equal(a, b)
+
+
+def test_oras_warp_kernel_bit_identical_ras():
+    """Batched-tile path (RAS local normal equations, ntile > 1)."""
+    import paper_2401_06747_b200 as sp
+    f = O.synth(128, 160, 3, 1)
+    mask = (np.random.default_rng(2).random((128, 160)) < 0.05).astype(np.uint8)
+
+    def run():
+        st = sp.ras_tonal(sp.Image(f), sp.Mask(mask))
+        return st.g.data, st.mse
+
+    (ga, ma), (gb, mb) = _with_oras_variant(0, run), _with_oras_variant(4, run)
+    assert ma == mb
+    assert np.array_equal(ga, gb)
