@@ -267,10 +267,17 @@ int sp_ct_apply_tiles(int dtype, const void* w, const uint8_t* mask, void* out, 
 /* ORAS local-CG statistics {jobs, iterations, converged-on-entry, max it};
  * enable 1 = reset+start, 0 = reset+stop, -1 = read only */
 int sp_stats(int enable, uint64_t* out_h);
-/* float ORAS kernel for blocks <= 32x32: 0 = register-resident 4-warp job
- * kernel, one job per CTA (default), 1 = 256-thread CTA kernel, 3 = the
- * 4-warp kernel persistent with cp.async prefetch; v < 0 query */
+/* float ORAS kernel for blocks <= 32x32: 4 = one warp per job, registers
+ * only (default), 0 = register-resident 4-warp job kernel, one job per CTA
+ * (bit-identical to 4), 1 = 256-thread CTA kernel, 3 = the 4-warp kernel
+ * persistent with cp.async prefetch; v < 0 query */
 int sp_oras_variant(int v);
+/* Batched cold tile solves (sp_hier_solve_tiles, the RAS block-local
+ * products tonal.py:120-131) on the fused on-chip kernel (tilesolve.cu: one
+ * cluster of C CTAs per block, whole solve in shared memory) when the
+ * hierarchy qualifies (float, two levels, <= 64x64): 1 = on (default),
+ * 0 = the batched V-cycle path; v < 0 queries.  A/B aid. */
+int sp_tile_fused(int v);
 /* Default sweep kernels of hierarchies created afterwards (all bit-identical
  * per element): 2 = TMA-staged residual sweeps on wide float levels
  * (mgtma.cu, default), 1 = row-marching register kernels (mgfast.cu), 0 =

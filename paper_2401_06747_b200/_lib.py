@@ -91,6 +91,7 @@ _SIGS = {
     "sp_pairwise_sum": [P, ctypes.c_longlong, P, P],
     "sp_oras_variant": [c_int],
     "sp_march_variant": [c_int],
+    "sp_tile_fused": [c_int],
     "sp_hier_residual": [P, c_int, P, P, P],
     "sp_geo_export": [P, P, P, P, P, P, P, P, c_long, P],
 }

@@ -470,6 +470,8 @@ namespace sp {
 int march_default(int v);
 }
 extern "C" int sp_march_variant(int v) { return sp::march_default(v); }
+namespace sp { int tile_fused(int v); }
+extern "C" int sp_tile_fused(int v) { return sp::tile_fused(v); }
 
 // ---- dithered initial mask (spatial.py:107-148) -------------------------------
 namespace sp {

@@ -28,6 +28,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "oras_warp.cuh"
 
 namespace sp {
 
@@ -487,31 +488,6 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
 // ---------------------------------------------------------------------------
 constexpr int WJ = 4;  // jobs (warps) per CTA
 
-// the xor-butterfly sums of x[0..3] over the warp, all four in every lane
-__device__ __forceinline__ void warp_sum4(const float (&x)[4], float (&t)[4], int j) {
-  const bool hi16 = j & 16, hi8 = j & 8;
-  // o = 16: keep groups {0,1} (low half) or {2,3} (high half)
-  const float s0 = hi16 ? x[0] : x[2], s1 = hi16 ? x[1] : x[3];
-  const float k0 = hi16 ? x[2] : x[0], k1 = hi16 ? x[3] : x[1];
-  const float y0 = k0 + __shfl_xor_sync(0xFFFFFFFFu, s0, 16);
-  const float y1 = k1 + __shfl_xor_sync(0xFFFFFFFFu, s1, 16);
-  // o = 8: keep the first or second of the pair
-  const float sd = hi8 ? y0 : y1, kp = hi8 ? y1 : y0;
-  float z = kp + __shfl_xor_sync(0xFFFFFFFFu, sd, 8);
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) z += __shfl_xor_sync(0xFFFFFFFFu, z, o);
-  // lanes 0 / 8 / 16 / 24 hold the totals of groups 0 / 1 / 2 / 3
-#pragma unroll
-  for (int g = 0; g < 4; ++g) t[g] = __shfl_sync(0xFFFFFFFFu, z, 8 * g);
-}
-
-__device__ __forceinline__ double sum4_double(const float (&t)[4]) {
-  double s = 0.0;
-#pragma unroll
-  for (int g = 0; g < 4; ++g) s += (double)t[g];
-  return s;
-}
-
 template <bool UNIT_H, bool FULLH>
 __global__ void __launch_bounds__(WJ * 32, 3) k_oras_warp(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
@@ -568,57 +544,9 @@ __global__ void __launch_bounds__(WJ * 32, 3) k_oras_warp(
   const float lf = j > 0 ? 1.0f : 0.0f, rt = j < bw - 1 ? 1.0f : 0.0f;
   const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
 
-  float p[R], v[R], ap[R];
-  float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f}, t4[4];
-#pragma unroll
-  for (int s = 0; s < R; ++s) {
-    p[s] = res[s];
-    v[s] = 0.0f;
-    acc4[s >> 3] = __fmaf_rn(res[s], res[s], acc4[s >> 3]);
-  }
-  warp_sum4(acc4, t4, j);
-  double rs = sum4_double(t4);
-  long it = 0;
-  while (rs > tau && it < cap) {
-    float q[R];
-#pragma unroll
-    for (int s = 0; s < R; ++s) q[s] = ((off >> s) & 1u) ? 0.0f : p[s];
-#pragma unroll
-    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const float ql = __shfl_up_sync(0xFFFFFFFFu, q[s], 1);
-      const float qr = __shfl_down_sync(0xFFFFFFFFu, q[s], 1);
-      const float up = s > 0 ? q[s - 1] : 0.0f;
-      const float dn = s < R - 1 ? q[s + 1] : 0.0f;
-      const float acc = __fmaf_rn(qr, rt, __fmaf_rn(ql, lf, up + dn));
-      float dg;
-      if (FULLH) dg = s == 0 ? dtop : (s == R - 1 ? dbot : dmid);
-      else dg = s == 0 ? dtop : (s == bh - 1 ? dbot : dmid);
-      const float a = __fmaf_rn(dg, p[s], UNIT_H ? -acc : -(acc * inv_h2));
-      ap[s] = ((off >> s) & 1u) ? p[s] : a;
-      acc4[s >> 3] = __fmaf_rn(p[s], ap[s], acc4[s >> 3]);
-    }
-    warp_sum4(acc4, t4, j);
-    const double pap = sum4_double(t4);
-    if (pap <= 0.0) break;
-    const float alpha = (float)rs / (float)pap;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      v[s] = __fmaf_rn(alpha, p[s], v[s]);
-      res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
-      acc4[s >> 3] = __fmaf_rn(res[s], res[s], acc4[s >> 3]);
-    }
-    warp_sum4(acc4, t4, j);
-    const double rsn = sum4_double(t4);
-    const float beta = (float)rsn / (float)rs;
-    rs = rsn;
-#pragma unroll
-    for (int s = 0; s < R; ++s) p[s] = __fmaf_rn(beta, p[s], res[s]);
-    ++it;
-  }
+  float v[R];
+  const long it = warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh,
+                                           tau, cap, j);
   float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
   const float* wb = weights + (size_t)bi * bh * bw;
   if (lane_ok) {

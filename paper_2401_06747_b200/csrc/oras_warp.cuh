@@ -1,0 +1,103 @@
+// oras_warp.cuh -- the ORAS local CG of one 32x32 block job on ONE warp
+// (numba_impl.py:188-251 semantics; see k_oras_warp in oras.cu for the
+// design and the arithmetic contract).  Shared by the global ORAS sweep
+// (oras.cu) and the fused on-chip tile solver (tilesolve.cu).
+#pragma once
+#include "common.cuh"
+
+namespace sp {
+
+// the xor-butterfly sums of x[0..3] over the warp, all four in every lane
+__device__ __forceinline__ void warp_sum4(const float (&x)[4], float (&t)[4], int j) {
+  const bool hi16 = j & 16, hi8 = j & 8;
+  // o = 16: keep groups {0,1} (low half) or {2,3} (high half)
+  const float s0 = hi16 ? x[0] : x[2], s1 = hi16 ? x[1] : x[3];
+  const float k0 = hi16 ? x[2] : x[0], k1 = hi16 ? x[3] : x[1];
+  const float y0 = k0 + __shfl_xor_sync(0xFFFFFFFFu, s0, 16);
+  const float y1 = k1 + __shfl_xor_sync(0xFFFFFFFFu, s1, 16);
+  // o = 8: keep the first or second of the pair
+  const float sd = hi8 ? y0 : y1, kp = hi8 ? y1 : y0;
+  float z = kp + __shfl_xor_sync(0xFFFFFFFFu, sd, 8);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) z += __shfl_xor_sync(0xFFFFFFFFu, z, o);
+  // lanes 0 / 8 / 16 / 24 hold the totals of groups 0 / 1 / 2 / 3
+#pragma unroll
+  for (int g = 0; g < 4; ++g) t[g] = __shfl_sync(0xFFFFFFFFu, z, 8 * g);
+}
+
+__device__ __forceinline__ double sum4_double(const float (&t)[4]) {
+  double s = 0.0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) s += (double)t[g];
+  return s;
+}
+
+// Local CG on the block held in registers: lane j = column j, res[s] = row s
+// (in: the block residual, out: the final local residual), v (out: the
+// local correction).  off bit s: row s masked or outside the block.  dtop /
+// dmid / dbot: the Robin-closed diagonal (times inv_h2) of the top, interior
+// and bottom rows; lf / rt: 1 where the lane has an in-block left / right
+// neighbour.  Stops on rs <= tau or after cap steps or on pap <= 0.
+// Returns the number of CG steps.
+template <bool UNIT_H, bool FULLH>
+__device__ __forceinline__ long warp_cg32(float (&res)[32], float (&v)[32], uint32_t off,
+                                          float dtop, float dmid, float dbot, float lf,
+                                          float rt, float inv_h2, int bh, double tau, long cap,
+                                          int j) {
+  constexpr int R = 32;
+  float p[R], ap[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) v[s] = 0.0f;
+  float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f}, t4[4];
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    p[s] = res[s];
+    acc4[s >> 3] = __fmaf_rn(res[s], res[s], acc4[s >> 3]);
+  }
+  warp_sum4(acc4, t4, j);
+  double rs = sum4_double(t4);
+  long it = 0;
+  while (rs > tau && it < cap) {
+    float q[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) q[s] = ((off >> s) & 1u) ? 0.0f : p[s];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const float ql = __shfl_up_sync(0xFFFFFFFFu, q[s], 1);
+      const float qr = __shfl_down_sync(0xFFFFFFFFu, q[s], 1);
+      const float up = s > 0 ? q[s - 1] : 0.0f;
+      const float dn = s < R - 1 ? q[s + 1] : 0.0f;
+      const float acc = __fmaf_rn(qr, rt, __fmaf_rn(ql, lf, up + dn));
+      float dg;
+      if (FULLH) dg = s == 0 ? dtop : (s == R - 1 ? dbot : dmid);
+      else dg = s == 0 ? dtop : (s == bh - 1 ? dbot : dmid);
+      const float a = __fmaf_rn(dg, p[s], UNIT_H ? -acc : -(acc * inv_h2));
+      ap[s] = ((off >> s) & 1u) ? p[s] : a;
+      acc4[s >> 3] = __fmaf_rn(p[s], ap[s], acc4[s >> 3]);
+    }
+    warp_sum4(acc4, t4, j);
+    const double pap = sum4_double(t4);
+    if (pap <= 0.0) break;
+    const float alpha = (float)rs / (float)pap;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      v[s] = __fmaf_rn(alpha, p[s], v[s]);
+      res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
+      acc4[s >> 3] = __fmaf_rn(res[s], res[s], acc4[s >> 3]);
+    }
+    warp_sum4(acc4, t4, j);
+    const double rsn = sum4_double(t4);
+    const float beta = (float)rsn / (float)rs;
+    rs = rsn;
+#pragma unroll
+    for (int s = 0; s < R; ++s) p[s] = __fmaf_rn(beta, p[s], res[s]);
+    ++it;
+  }
+  return it;
+}
+
+}  // namespace sp

@@ -367,6 +367,11 @@ template <typename T>
 static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, int cycles,
                    int max_cycles, cudaStream_t s, const int* active_in, int* iters,
                    int* conv, SolveReport* rep) {
+  // batched cold tile solves to a tolerance (RAS block-local products): the
+  // fused on-chip kernel when the hierarchy qualifies (tilesolve.cu)
+  if (sizeof(T) == 4 && active_in && !rep && init_mode == 0 && tol >= 0 && tile_fused_ok(h))
+    return tile_solve_fused(h, (const float*)bsym, (float*)u_io, tol, max_cycles, s, active_in,
+                            iters, conv);
   Level& L0 = h->lv[0];
   const int C = h->C, nt = h->ntile;
   size_t per = (size_t)C * L0.H * L0.W, n = per * nt;

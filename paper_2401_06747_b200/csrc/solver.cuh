@@ -61,6 +61,11 @@ int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
                int* conv, SolveReport* rep);
 int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s);
 
+// tilesolve.cu: fused on-chip cold solve of a batch of small tiles
+bool tile_fused_ok(const Hier* h);
+int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int max_cycles,
+                     cudaStream_t s, const int* active_in, int* iters, int* conv);
+
 // level operations (solver.cu), used by the row-strip solver (strips.cu)
 template <typename T>
 int prolong_lv(Hier* h, int lv, int add, cudaStream_t s);

@@ -8,9 +8,10 @@ from oracle.oracle import synth
 lib = _lib.load()
 f = torch.from_numpy(synth(2160, 3840, 3, 0)).cuda()
 cfg = sp.PipelineConfig()
-variants = [int(a) for a in sys.argv[1:]] or [0, 4]
-for v in variants * 2:
+variants = [tuple(int(x) for x in a.split(":")) for a in sys.argv[1:]] or [(4, 0), (4, 1)]
+for v, tf in variants * 2:
     lib.sp_oras_variant(v)
+    lib.sp_tile_fused(tf)
     sp.solver._POOL.clear()
     sp.run_pipeline(sp.Image(f), cfg)
     torch.cuda.synchronize()
@@ -20,5 +21,5 @@ for v in variants * 2:
         mask, st, hist, _ = sp.run_pipeline(sp.Image(f), cfg)
     e1.record()
     torch.cuda.synchronize()
-    print(f"oras variant {v}: {e0.elapsed_time(e1) / 2:.1f} ms/pipeline  mse={st.mse:.9f} "
+    print(f"oras variant {v} tile_fused {tf}: {e0.elapsed_time(e1) / 2:.1f} ms/pipeline  mse={st.mse:.9f} "
           f"dd_mse={hist[-1][2]:.9f} count={mask.count}", flush=True)

@@ -132,3 +132,67 @@ def test_initial_state_and_balance(sp, rng):
 def test_empty_mask_rejected(sp):
     with pytest.raises(ValueError):
         sp.ras_tonal(sp.Image(np.ones((1, 8, 8))), sp.Mask(np.zeros((8, 8))))
+
+
+def _with_tile_fused(on, fn):
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    prev = lib.sp_tile_fused(-1)
+    try:
+        lib.sp_tile_fused(on)
+        _POOL.clear()
+        return fn()
+    finally:
+        lib.sp_tile_fused(prev)
+        _POOL.clear()
+
+
+@pytest.mark.parametrize("shape,density", [((3, 200, 260), 0.05), ((1, 130, 100), 0.08),
+                                           ((3, 64, 64), 0.05), ((2, 90, 50), 0.04)])
+def test_fused_tile_solver_matches_batched(sp, shape, density):
+    """RAS block-local products on the fused on-chip tile solver (tilesolve.cu,
+    one cluster per block) vs the batched V-cycle hierarchy: the same
+    element operations, norms summed in another order -> equal to rounding;
+    the V-cycle counts per block agree."""
+    import torch
+    from paper_2401_06747_b200 import tonal
+    c, h, w = shape
+    f = O.synth(h, w, c, 4)
+    mask = (np.random.default_rng(9).random((h, w)) < density).astype(np.uint8)
+
+    def run():
+        solver = sp.InpaintSolver()
+        blocks = tonal._RasBlocks(torch.from_numpy(mask).cuda(), solver, c, sp.RasTonalConfig())
+        rng = np.random.default_rng(3)
+        x = torch.from_numpy(rng.standard_normal((blocks.nt, c, blocks.bh, blocks.bw))
+                             ).float().cuda()
+        act = np.ones(blocks.nt, np.int32)
+        act[::3] = 0 if blocks.nt > 2 else 1
+        act_d = torch.from_numpy(act).cuda()
+        bp = blocks.apply_B(x, act, act_d)
+        it = blocks._iters.copy()
+        mp = blocks.apply_Bt(bp, act, act_d)
+        keep = torch.from_numpy(act > 0).cuda()
+        return bp[keep].cpu().numpy(), mp[keep].cpu().numpy(), it[act > 0]
+
+    b1, m1, i1 = _with_tile_fused(1, run)
+    b0, m0, i0 = _with_tile_fused(0, run)
+    assert np.array_equal(i1, i0)
+    for a, b in ((b1, b0), (m1, m0)):
+        scale = np.abs(b).max()
+        assert np.abs(a - b).max() <= 2e-5 * scale
+
+
+def test_fused_tile_solver_ras_mse(sp):
+    """ras_tonal end to end with and without the fused tile solver."""
+    f = O.synth(160, 200, 3, 1)
+    mask = (np.random.default_rng(2).random((160, 200)) < 0.05).astype(np.uint8)
+
+    def run():
+        st = sp.ras_tonal(sp.Image(f), sp.Mask(mask))
+        return st.mse, st.iterations
+
+    (ma, ia), (mb, ib) = _with_tile_fused(1, run), _with_tile_fused(0, run)
+    assert ia == ib
+    assert abs(ma - mb) <= 1e-6 * mb
