@@ -56,8 +56,8 @@ def _ncu_traffic(kernel):
     (profiles/ncu_<tag>_<kernel>.txt, scripts/summarize_prof.py), or None."""
     import glob
     import re
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_*_{kernel}.txt")),
-                   key=os.path.getmtime)
+    # newest round tag last (ncu_r01a_... < ncu_r01w_...)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_*_{kernel}.txt")))
     if not files:
         return None
     tot = 0.0
@@ -335,7 +335,7 @@ def run_ours(args):
     bsym = _masked_rhs(f_dev.float().contiguous(), mask.tensor())
     hier.solve_sym(bsym, tol=1e-4, cascade=True)
     import ctypes
-    names = {0: "k_resid_tma (sym_residual sweep)", 1: "k_oras_rows (ORAS local CG)",
+    names = {0: "k_resid_tma (sym_residual sweep)", 1: "k_oras_warp (ORAS local CG)",
              2: "k_oras_blend", 3: "k_resid_tma<1> (residual + restriction)"}
     for which in (0, 1, 2, 3):
         t_ms, nbytes = ctypes.c_double(), ctypes.c_double()
@@ -345,7 +345,7 @@ def run_ours(args):
         kern[names[which]] = {"us": t_ms.value * 1e3, "bytes": nbytes.value,
                               "gbs": gbs, "frac": gbs / peak}
     dom = names[1]
-    tr = _ncu_traffic("k_oras_rows")
+    tr = _ncu_traffic("k_oras_warp")
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
             "unit": "GB/s", "frac": kern[dom]["frac"],
             "traffic": tr["bytes"] if tr else None,

@@ -110,6 +110,99 @@ __global__ void k_seed_init(const int* __restrict__ idx, long m, int W, int* __r
   lab[p] = (int)i;
 }
 
+
+// ---- jump flooding on packed seed coordinates ---------------------------------
+// The pipeline's seeds are the stored pixels in row-major order
+// (np.nonzero, geometry.py:92-110), so seed index order IS the row-major
+// order of the seed coordinates: a label can carry the seed's coordinates
+// key = (sy << 16) | sx instead of its index, and "lower index wins a tie"
+// becomes "lower key wins".  A pass then needs no seed-table gathers (the
+// index form reads sy/sx of all nine candidates, 18 scattered L2 reads per
+// pixel); the keys are mapped back to indices once at the end.
+constexpr unsigned KNONE = 0xFFFFFFFFu;
+
+__global__ void k_jfa_key_init(const uint8_t* __restrict__ m, unsigned* __restrict__ lab, int H,
+                               int W) {
+  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+  if (x >= W || y >= H) return;
+  size_t k = (size_t)y * W + x;
+  lab[k] = m[k] ? (((unsigned)y << 16) | (unsigned)x) : KNONE;
+}
+
+__device__ __forceinline__ int key_d2(unsigned key, int y, int x) {
+  const int dy = y - (int)(key >> 16), dx = x - (int)(key & 0xFFFFu);
+  return dy * dy + dx * dx;
+}
+
+__global__ void k_jfa_pass_key(const unsigned* __restrict__ cur, unsigned* __restrict__ nxt,
+                               int step, int H, int W) {
+  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+  if (x >= W || y >= H) return;
+  unsigned best = cur[(size_t)y * W + x];
+  int bd = best != KNONE ? key_d2(best, y, x) : 4 * (H * H + W * W);
+#pragma unroll
+  for (int oy = -1; oy <= 1; ++oy) {
+    int ny = y + oy * step;
+    if (ny < 0 || ny >= H) continue;
+#pragma unroll
+    for (int ox = -1; ox <= 1; ++ox) {
+      if (oy == 0 && ox == 0) continue;
+      int nx = x + ox * step;
+      if (nx < 0 || nx >= W) continue;
+      unsigned cand = cur[(size_t)ny * W + nx];
+      if (cand == KNONE) continue;
+      int cd = key_d2(cand, y, x);
+      if (cd < bd || (cd == bd && best != KNONE && cand < best)) {
+        bd = cd;
+        best = cand;
+      }
+    }
+  }
+  nxt[(size_t)y * W + x] = best;
+}
+
+// keys -> seed indices (rank of the seed pixel), in place; fused with the
+// max squared distance of jfa_dist2 (unlabelled pixels: numba's seeds[-1])
+__global__ void k_jfa_key_finish(unsigned* __restrict__ lab, const int* __restrict__ rank,
+                                 const int* __restrict__ sy, const int* __restrict__ sx, long m,
+                                 unsigned long long* __restrict__ dmax, int H, int W) {
+  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+  long long d = 0;
+  if (x < W && y < H) {
+    size_t k = (size_t)y * W + x;
+    unsigned key = lab[k];
+    long long dy, dx;
+    int s;
+    if (key == KNONE) {
+      s = -1;
+      dy = (long long)y - sy[m - 1];
+      dx = (long long)x - sx[m - 1];
+    } else {
+      const int ky = (int)(key >> 16), kx = (int)(key & 0xFFFFu);
+      s = rank[(size_t)ky * W + kx];
+      dy = (long long)y - ky;
+      dx = (long long)x - kx;
+    }
+    d = dy * dy + dx * dx;
+    lab[k] = (unsigned)s;
+  }
+  // CTA max, one atomic per CTA (same-address atomics serialise in L2)
+  __shared__ unsigned long long wmax[BX * BY / 32];
+  unsigned long long v = (unsigned long long)d;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  const int tid = threadIdx.y * BX + threadIdx.x;
+  if ((tid & 31) == 0) wmax[tid >> 5] = v;
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < BX * BY / 32; ++i) v = wmax[i] > v ? wmax[i] : v;
+    atomicMax(dmax, v);
+  }
+}
+
 __global__ void k_fill_i32(int* __restrict__ p, size_t n, int v) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -179,11 +272,22 @@ __global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
     unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= (unsigned)o) incl += v;
   }
-  unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-  unsigned long long base = 0;
-  if (lane == 31 && total) base = atomicAdd(nkeys, (unsigned long long)total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  unsigned long long pos = base + incl - cnt;
+  // CTA-aggregated: one atomic per CTA (same-address atomics serialise in L2)
+  __shared__ unsigned wtot[BY];
+  __shared__ unsigned long long cbase;
+  if (lane == 31) wtot[threadIdx.y] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    unsigned acc = 0;
+    for (int i = 0; i < BY; ++i) {
+      const unsigned t = wtot[i];
+      wtot[i] = acc;
+      acc += t;
+    }
+    cbase = acc ? atomicAdd(nkeys, (unsigned long long)acc) : 0ull;
+  }
+  __syncthreads();
+  unsigned long long pos = cbase + wtot[threadIdx.y] + incl - cnt;
   if (nk >= 1) keys[pos] = k0;
   if (nk == 2) keys[pos + 1] = k1;
 }
@@ -202,9 +306,13 @@ __global__ void k_decode_tris(const unsigned long long* __restrict__ keys, long 
 template <typename V>
 __global__ void k_assign_tris(const V* __restrict__ tris, long T, const V* __restrict__ vy,
                               const V* __restrict__ vx, int H, int W, int* __restrict__ assign) {
-  long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  // one 8-lane group per triangle (Delaunay triangles cover ~20-40 box
+  // pixels): four triangles in flight per warp, so the per-triangle vertex
+  // gathers overlap instead of serialising a warp's whole triangle list
+  constexpr int G = 8;
+  long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  int lane = threadIdx.x & (G - 1);
+  long nwarps = ((long)gridDim.x * blockDim.x) / G;
   for (long t = warp; t < T; t += nwarps) {
     long long ay = vy[tris[3 * t]], ax = vx[tris[3 * t]];
     long long by = vy[tris[3 * t + 1]], bx = vx[tris[3 * t + 1]];
@@ -212,15 +320,33 @@ __global__ void k_assign_tris(const V* __restrict__ tris, long T, const V* __res
     long long ylo = max(0LL, min(ay, min(by, cy))), yhi = min((long long)H - 1, max(ay, max(by, cy)));
     long long xlo = max(0LL, min(ax, min(bx, cx))), xhi = min((long long)W - 1, max(ax, max(bx, cx)));
     if (ylo > yhi || xlo > xhi) continue;
-    long long bw = xhi - xlo + 1;
-    long long area = (yhi - ylo + 1) * bw;
-    for (long long q = lane; q < area; q += 32) {
-      long long y = ylo + q / bw, x = xlo + q % bw;
-      long long e0 = (bx - ax) * (y - ay) - (by - ay) * (x - ax);
-      long long e1 = (cx - bx) * (y - by) - (cy - by) * (x - bx);
-      long long e2 = (ax - cx) * (y - cy) - (ay - cy) * (x - cx);
+    // the clamped box lies inside the image: 32-bit pixel coordinates and
+    // box index (no 64-bit division), 64-bit edge-function products
+    const int bw = (int)(xhi - xlo + 1), y0 = (int)ylo, x0 = (int)xlo;
+    const long long area = (yhi - ylo + 1) * (long long)bw;
+    const long long lim = 1LL << 30;
+    const bool in32 = ay > -lim && ay < lim && ax > -lim && ax < lim && by > -lim && by < lim &&
+                      bx > -lim && bx < lim && cy > -lim && cy < lim && cx > -lim && cx < lim;
+    if (area >= (1LL << 31) || !in32) {
+      for (long long q = lane; q < area; q += G) {
+        long long y = ylo + q / bw, x = xlo + q % bw;
+        long long e0 = (bx - ax) * (y - ay) - (by - ay) * (x - ax);
+        long long e1 = (cx - bx) * (y - by) - (cy - by) * (x - bx);
+        long long e2 = (ax - cx) * (y - cy) - (ay - cy) * (x - cx);
+        if ((e0 >= 0 && e1 >= 0 && e2 >= 0) || (e0 <= 0 && e1 <= 0 && e2 <= 0))
+          atomicMin(&assign[y * W + x], (int)t);
+      }
+      continue;
+    }
+    const int iay = (int)ay, iax = (int)ax, iby = (int)by, ibx = (int)bx, icy = (int)cy,
+              icx = (int)cx;
+    for (int q = lane; q < (int)area; q += G) {
+      const int r = q / bw, y = y0 + r, x = x0 + (q - r * bw);
+      long long e0 = (long long)(ibx - iax) * (y - iay) - (long long)(iby - iay) * (x - iax);
+      long long e1 = (long long)(icx - ibx) * (y - iby) - (long long)(icy - iby) * (x - ibx);
+      long long e2 = (long long)(iax - icx) * (y - icy) - (long long)(iay - icy) * (x - icx);
       if ((e0 >= 0 && e1 >= 0 && e2 >= 0) || (e0 <= 0 && e1 <= 0 && e2 <= 0))
-        atomicMin(&assign[y * W + x], (int)t);
+        atomicMin(&assign[(size_t)y * W + x], (int)t);
     }
   }
 }
@@ -487,7 +613,7 @@ int reduce_cells(const int* assign, const double* err, long nseg, double* sums,
 // ---------------------------------------------------------------------------
 
 Geo::~Geo() {
-  for (void* p : {(void*)lab_a, (void*)lab_b, (void*)sy, (void*)sx, (void*)keys,
+  for (void* p : {(void*)lab_a, (void*)lab_b, (void*)rank, (void*)sy, (void*)sx, (void*)keys,
                   (void*)nkeys, (void*)tris, (void*)assign, (void*)smt, (void*)sums,
                   (void*)amax, (void*)amax_val, (void*)dmax, (void*)flags, (void*)idx,
                   (void*)nsel, (void*)h_small})
@@ -508,6 +634,7 @@ int geo_create(Geo** out, int H, int W) {
   g->tri_cap = g->key_cap;
   bool ok = cudaMalloc(&g->lab_a, sizeof(int) * n) == cudaSuccess &&
             cudaMalloc(&g->lab_b, sizeof(int) * n) == cudaSuccess &&
+            cudaMalloc(&g->rank, sizeof(int) * n) == cudaSuccess &&
             cudaMalloc(&g->sy, sizeof(int) * n) == cudaSuccess &&
             cudaMalloc(&g->sx, sizeof(int) * n) == cudaSuccess &&
             cudaMalloc(&g->idx, sizeof(int) * n) == cudaSuccess &&
@@ -572,16 +699,37 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
     return -3;
   }
   g->m = m;
-  k_fill_i32<<<cdiv(n, 256), 256, 0, s>>>(g->lab_a, n, -1);
-  SP_CHECK_LAUNCH();
-  k_seed_init<<<cdiv(m, 256), 256, 0, s>>>(g->idx, m, W, g->sy, g->sx, g->lab_a);
-  SP_CHECK_LAUNCH();
   std::vector<long long> steps = steps_for(std::max(H, W), hint);
-  int* res = nullptr;
-  SP_TRY(jfa_passes(g->lab_a, g->lab_b, g->sy, g->sx, steps.data(), (int)steps.size(), H, W,
-                    &res, s));
-  if (res != g->lab_a) std::swap(g->lab_a, g->lab_b);  // labels live in lab_a
-  SP_TRY(dist2(g->lab_a, g->sy, g->sx, nullptr, g->dmax, H, W, (int)g->m, s));
+  const bool keyed = H < 65536 && W < 65536 && 4.0 * ((double)H * H + (double)W * W) < 2.0e9;
+  if (keyed) {
+    // packed-coordinate labels (k_jfa_pass_key); rank[] maps keys back
+    k_seed_init<<<cdiv(m, 256), 256, 0, s>>>(g->idx, m, W, g->sy, g->sx, g->rank);
+    SP_CHECK_LAUNCH();
+    unsigned* cur = (unsigned*)g->lab_a;
+    unsigned* nxt = (unsigned*)g->lab_b;
+    k_jfa_key_init<<<grid2(W, H), dim3(BX, BY), 0, s>>>(mask, cur, H, W);
+    SP_CHECK_LAUNCH();
+    for (size_t i = 0; i < steps.size(); ++i) {
+      k_jfa_pass_key<<<grid2(W, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
+      SP_CHECK_LAUNCH();
+      std::swap(cur, nxt);
+    }
+    if ((int*)cur != g->lab_a) std::swap(g->lab_a, g->lab_b);  // labels live in lab_a
+    SP_CUDA(cudaMemsetAsync(g->dmax, 0, sizeof(unsigned long long), s));
+    k_jfa_key_finish<<<grid2(W, H), dim3(BX, BY), 0, s>>>((unsigned*)g->lab_a, g->rank, g->sy,
+                                                          g->sx, m, g->dmax, H, W);
+    SP_CHECK_LAUNCH();
+  } else {
+    k_fill_i32<<<cdiv(n, 256), 256, 0, s>>>(g->lab_a, n, -1);
+    SP_CHECK_LAUNCH();
+    k_seed_init<<<cdiv(m, 256), 256, 0, s>>>(g->idx, m, W, g->sy, g->sx, g->lab_a);
+    SP_CHECK_LAUNCH();
+    int* res = nullptr;
+    SP_TRY(jfa_passes(g->lab_a, g->lab_b, g->sy, g->sx, steps.data(), (int)steps.size(), H, W,
+                      &res, s));
+    if (res != g->lab_a) std::swap(g->lab_a, g->lab_b);  // labels live in lab_a
+    SP_TRY(dist2(g->lab_a, g->sy, g->sx, nullptr, g->dmax, H, W, (int)g->m, s));
+  }
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   unsigned long long d2 = ((unsigned long long*)g->h_small)[0];

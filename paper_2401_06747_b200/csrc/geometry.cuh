@@ -12,6 +12,7 @@ struct Geo {
   int *lab_a = nullptr, *lab_b = nullptr;  // labels live in lab_a after geo_voronoi
   int *sy = nullptr, *sx = nullptr;        // seed coordinates (row-major order)
   int* idx = nullptr;
+  int* rank = nullptr;                     // seed index at each seed pixel
   uint8_t* flags = nullptr;
   unsigned long long* keys = nullptr;
   unsigned long long* nkeys = nullptr;

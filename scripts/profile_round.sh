@@ -15,5 +15,12 @@ L=$(python -c "import json;print(json.loads(open('gpurun_out/bench_$TAG.json').r
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3 * L)) -c $L --csv \
     --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-strips > gpurun_out/launches_bench_$TAG.log 2>&1
-bash scripts/ncu_kernels.sh $TAG k_oras_rows k_resid_tma k_oras_blend k_prolong_tma:4
+bash scripts/ncu_kernels.sh $TAG k_oras_warp k_resid_tma k_oras_blend k_prolong_tma:4
+
+# fused RAS block kernels (tilesolve.cu) on the 4K block set
+for K in k_tv_down k_tv_close; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
+    -o gpurun_out/prof_${K}_$TAG -f python scripts/probe_tiles.py 2160,3840,3 1 \
+    > gpurun_out/ncu_${K}_$TAG.log 2>&1
+done
 ls -la gpurun_out
