@@ -312,15 +312,19 @@ def run_ours(args):
     # ---- end-to-end through the public API with host buffers --------------
     h2d = f_pinned.numel() * f_pinned.element_size()
     d2h = 0
+
+    def step_e2e():
+        m_e, st_e, _, _ = sp.run_pipeline(sp.Image(f_pinned), cfg, solver=solver)
+        mask_h = m_e.indicator          # D2H: mask (u8)
+        g_h = st_e.g.data               # D2H: stored values (dense f32 image)
+        return mask_h.nbytes + g_h.nbytes
+
+    step_e2e()  # untimed warm-up of the host path (page-locked staging blocks)
     _barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        m_e, st_e, _, _ = sp.run_pipeline(sp.Image(f_pinned), cfg, solver=solver)
-        mask_h = m_e.indicator          # D2H: mask
-        g_h = st_e.g.data               # D2H: stored values (moved sparsely:
-        n_st = int(mask_h.sum())        # indices + values of the stored pixels)
-        d2h = mask_h.nbytes + n_st * (8 + C * g_h.itemsize)
+        d2h = step_e2e()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.steps
     e2e_s = _max_over_ranks(e2e_s, world)

@@ -43,7 +43,7 @@ __device__ int g_stats_on;
 // stencil, 3 = persistent k_oras_rows_p with cp.async prefetch of the next
 // job (it removes the load stalls but issues 32% more instructions and
 // loses: 1.80 vs 1.58 ms per 4K V-cycle, profiles/oras_ab_r01j.txt)
-static int oras_kernel = 4;
+static int oras_kernel = 6;
 int oras_variant(int v) {
   if (v >= 0) oras_kernel = v;
   return oras_kernel;
@@ -488,8 +488,8 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
 // ---------------------------------------------------------------------------
 constexpr int WJ = 4;  // jobs (warps) per CTA
 
-template <bool UNIT_H, bool FULLH>
-__global__ void __launch_bounds__(WJ * 32, 3) k_oras_warp(
+template <bool UNIT_H, bool FULLH, int WJ>
+__global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
     const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
@@ -555,167 +555,6 @@ __global__ void __launch_bounds__(WJ * 32, 3) k_oras_warp(
       if (FULLH || s < bh) out[s * bw + j] = wb[s * bw + j] * v[s];
   }
   if (j == 0 && g_stats_on) {
-    atomicAdd(&g_oras_stats[0], 1ull);
-    atomicAdd(&g_oras_stats[1], (unsigned long long)it);
-    if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
-    atomicMax(&g_oras_stats[3], (unsigned long long)it);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Patch layout (sp_oras_variant 5, full 32x32 blocks): one warp per job as in
-// k_oras_warp, but lane l owns the 8 x 4 patch of block rows 8*(l/8) .. +7
-// and columns 4*(l%8) .. +3.  Three of a pixel's four stencil neighbours
-// are then usually in the lane's own registers: a CG step exchanges only
-// the patch edges (4 + 4 + 8 + 8 = 24 shuffles instead of 64), and the
-// stencil adds in-patch neighbours without the lane-edge factors.
-// Dots: float per lane (4 chains), summed over the 8 lanes of a row group
-// by an xor butterfly, the 4 group sums added in double.  Same operator and
-// CG recurrence as k_oras_warp; the dot summation order differs, so the
-// iterates agree with variant 4 to rounding (tests/test_solver_gpu.py).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ float sum_lane4(const float (&a)[4]) {
-  return ((a[0] + a[1]) + a[2]) + a[3];
-}
-// lane partial -> sum over the warp: 8-lane groups in float, groups in double
-__device__ __forceinline__ double patch_dot(float lane_sum) {
-  float g = lane_sum;
-  g += __shfl_xor_sync(0xFFFFFFFFu, g, 1);
-  g += __shfl_xor_sync(0xFFFFFFFFu, g, 2);
-  g += __shfl_xor_sync(0xFFFFFFFFu, g, 4);
-  double t = 0.0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) t += (double)__shfl_sync(0xFFFFFFFFu, g, 8 * q);
-  return t;
-}
-
-template <bool UNIT_H>
-__global__ void __launch_bounds__(WJ * 32, 3) k_oras_patch(
-    const float* __restrict__ r, const uint8_t* __restrict__ m,
-    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
-    const int* __restrict__ xs, int nbx, int nbl, int H, int W, int stride, float closure,
-    long cap, float inv_h2, const float* __restrict__ weights, float* __restrict__ corr,
-    const int* __restrict__ active, int corr_nb, size_t ps) {
-  constexpr int BS = 32, NP = 32;  // block side, pixels per lane
-  const int l = threadIdx.x & 31, px = l & 7, py = l >> 3;
-  const int bi = blockIdx.x * WJ + (threadIdx.x >> 5), ch = blockIdx.y, C = gridDim.y;
-  const int tile = blockIdx.z;
-  if (bi >= nbl) return;
-  if (active && !active[tile]) return;
-  const int nb = corr_nb > 0 ? corr_nb : nbl;
-  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
-  const int y0 = stride > 0 ? block_start(kyb, stride, H, BS) : ys[kyb];
-  const int x0 = stride > 0 ? block_start(kxb, stride, W, BS) : xs[kxb];
-  const float* rc = r + ((size_t)tile * C + ch) * ps + (size_t)(y0 + 8 * py) * W + x0 + 4 * px;
-  const uint8_t* mt = m + (size_t)tile * ps + (size_t)(y0 + 8 * py) * W + x0 + 4 * px;
-  float res[NP];
-  uint8_t mk[NP];
-#pragma unroll
-  for (int rr = 0; rr < 8; ++rr)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      res[rr * 4 + c] = rc[(size_t)rr * W + c];
-      mk[rr * 4 + c] = mt[(size_t)rr * W + c];
-    }
-  uint32_t off = 0;
-#pragma unroll
-  for (int k = 0; k < NP; ++k)
-    if (mk[k]) off |= 1u << k;
-  // Robin-closed diagonal (k_oras_rows' addition order) of the 3 x 3 pixel
-  // classes: first / interior / last row and column of the patch
-  const int gxl = x0 + 4 * px, gyt = y0 + 8 * py;
-  auto diag = [&](int i, int j) {
-    const int gy = y0 + i, gx = x0 + j;
-    float d = 0.0f;
-    if (gy > 0) d += i > 0 ? 1.0f : closure;
-    if (gy < H - 1) d += i < BS - 1 ? 1.0f : closure;
-    if (gx > 0) d += j > 0 ? 1.0f : closure;
-    if (gx < W - 1) d += j < BS - 1 ? 1.0f : closure;
-    return d * inv_h2;
-  };
-  (void)gxl; (void)gyt;
-  float dg[3][3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      dg[a][b] = diag(8 * py + (a == 0 ? 0 : a == 1 ? 1 : 7), 4 * px + (b == 0 ? 0 : b == 1 ? 1 : 3));
-  const float fu = py > 0 ? 1.0f : 0.0f, fd = py < 3 ? 1.0f : 0.0f;
-  const float fl = px > 0 ? 1.0f : 0.0f, fr = px < 7 ? 1.0f : 0.0f;
-  const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
-
-  float p[NP], v[NP], ap[NP];
-  float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    p[k] = res[k];
-    v[k] = 0.0f;
-    a4[k >> 3] = __fmaf_rn(res[k], res[k], a4[k >> 3]);
-  }
-  double rs = patch_dot(sum_lane4(a4));
-  long it = 0;
-  while (rs > tau && it < cap) {
-    float q[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) q[k] = ((off >> k) & 1u) ? 0.0f : p[k];
-    float qu[4], qd[4], ql[8], qr[8];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      qu[c] = __shfl_up_sync(0xFFFFFFFFu, q[28 + c], 8) * fu;
-      qd[c] = __shfl_down_sync(0xFFFFFFFFu, q[c], 8) * fd;
-    }
-#pragma unroll
-    for (int rr = 0; rr < 8; ++rr) {
-      ql[rr] = __shfl_up_sync(0xFFFFFFFFu, q[rr * 4 + 3], 1) * fl;
-      qr[rr] = __shfl_down_sync(0xFFFFFFFFu, q[rr * 4], 1) * fr;
-    }
-#pragma unroll
-    for (int g = 0; g < 4; ++g) a4[g] = 0.0f;
-#pragma unroll
-    for (int rr = 0; rr < 8; ++rr)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int k = rr * 4 + c;
-        const float up = rr > 0 ? q[k - 4] : qu[c];
-        const float dn = rr < 7 ? q[k + 4] : qd[c];
-        const float lf = c > 0 ? q[k - 1] : ql[rr];
-        const float rt = c < 3 ? q[k + 1] : qr[rr];
-        const float acc = ((up + dn) + lf) + rt;
-        const float d = dg[rr == 0 ? 0 : (rr == 7 ? 2 : 1)][c == 0 ? 0 : (c == 3 ? 2 : 1)];
-        const float a = __fmaf_rn(d, p[k], UNIT_H ? -acc : -(acc * inv_h2));
-        ap[k] = ((off >> k) & 1u) ? p[k] : a;
-        a4[k >> 3] = __fmaf_rn(p[k], ap[k], a4[k >> 3]);
-      }
-    const double pap = patch_dot(sum_lane4(a4));
-    if (pap <= 0.0) break;
-    const float alpha = (float)rs / (float)pap;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) a4[g] = 0.0f;
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      v[k] = __fmaf_rn(alpha, p[k], v[k]);
-      res[k] = __fmaf_rn(-alpha, ap[k], res[k]);
-      a4[k >> 3] = __fmaf_rn(res[k], res[k], a4[k >> 3]);
-    }
-    const double rsn = patch_dot(sum_lane4(a4));
-    const float beta = (float)rsn / (float)rs;
-    rs = rsn;
-#pragma unroll
-    for (int k = 0; k < NP; ++k) p[k] = __fmaf_rn(beta, p[k], res[k]);
-    ++it;
-  }
-  // corr = T(w) * v, 16-byte rows (block planes are 4 KB aligned)
-  float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(BS * BS);
-  const float* wb = weights + (size_t)bi * BS * BS;
-#pragma unroll
-  for (int rr = 0; rr < 8; ++rr) {
-    const int o = (8 * py + rr) * BS + 4 * px;
-    const float4 w4 = *reinterpret_cast<const float4*>(wb + o);
-    *reinterpret_cast<float4*>(out + o) =
-        make_float4(w4.x * v[rr * 4], w4.y * v[rr * 4 + 1], w4.z * v[rr * 4 + 2],
-                    w4.w * v[rr * 4 + 3]);
-  }
-  if (l == 0 && g_stats_on) {
     atomicAdd(&g_oras_stats[0], 1ull);
     atomicAdd(&g_oras_stats[1], (unsigned long long)it);
     if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
@@ -1184,7 +1023,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   const int npx = bh * bw;
   if (ps && ps != (size_t)H * W &&
       !(sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
-        (oras_kernel == 0 || oras_kernel == 2 || oras_kernel == 4 || oras_kernel == 5))) {
+        (oras_kernel == 0 || oras_kernel == 2 || oras_kernel == 4 || oras_kernel == 6))) {
     set_error("plane-strided ORAS launches need the float 32x32 4-warp kernel");
     return -2;
   }
@@ -1209,21 +1048,19 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                                      nby * nbx, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
                                      (float)inv_h2, (const float*)weights, (float*)corr, active,
                                      corr_nb, C, njobs);
-  } else if (sizeof(T) == 4 && bw == 32 && bh == 32 && oras_kernel == 5 &&
-             ((uintptr_t)weights & 15) == 0 && ((uintptr_t)corr & 15) == 0) {
+  } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && (oras_kernel == 4 || oras_kernel == 6)) {
     const int nbl = nby * nbx;
-    dim3 g5(cdiv(nbl, WJ), C, ntile);
-    auto kern = inv_h2 == 1.0 ? k_oras_patch<true> : k_oras_patch<false>;
-    kern<<<g5, WJ * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, H, W,
-                                stride, (float)(1.0 - gamma), cap, (float)inv_h2,
-                                (const float*)weights, (float*)corr, active, corr_nb, ps);
-  } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && (oras_kernel == 4 || oras_kernel == 5)) {
-    const int nbl = nby * nbx;
-    dim3 g4(cdiv(nbl, WJ), C, ntile);
     const bool unit = inv_h2 == 1.0, full = bh == 32;
-    auto kern = unit ? (full ? k_oras_warp<true, true> : k_oras_warp<true, false>)
-                     : (full ? k_oras_warp<false, true> : k_oras_warp<false, false>);
-    kern<<<g4, WJ * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
+    // 4: four jobs per CTA; 6: one job per CTA (a finished job frees its
+    // slot at once instead of waiting for the CTA's slowest job)
+    const int wj = oras_kernel == 6 ? 1 : WJ;
+    dim3 g4(cdiv(nbl, wj), C, ntile);
+#define SP_WARP(WJN)                                                                          \
+  (unit ? (full ? k_oras_warp<true, true, WJN> : k_oras_warp<true, false, WJN>)               \
+        : (full ? k_oras_warp<false, true, WJN> : k_oras_warp<false, false, WJN>))
+    auto kern = wj == 1 ? SP_WARP(1) : SP_WARP(WJ);
+#undef SP_WARP
+    kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
                                 bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
                                 (const float*)weights, (float*)corr, active, corr_nb, ps);
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {

@@ -42,9 +42,17 @@ DEFAULT_STENCIL = StencilSpec()
 
 
 def _to_host(t: torch.Tensor) -> np.ndarray:
-    """Device -> host numpy (a pageable copy: a fresh pinned buffer per call
-    costs more in page-locking than it saves in bandwidth, measured)."""
-    return t.cpu().numpy()
+    """Device -> host numpy through a page-locked block of torch's caching
+    host allocator: a 4K RGB f32 image comes back in 1.8 ms at ~55 GB/s
+    once the block is cached, vs 46 ms for a pageable copy and 18 ms for a
+    sparse copy scattered into host zeros (scripts/probe_d2h.py).  The
+    array shares the block's storage; the block returns to the cache when
+    the array is released."""
+    if not t.is_cuda:
+        return t.numpy()
+    out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
 
 
 class Image:
@@ -77,8 +85,9 @@ class Image:
     @classmethod
     def sparse(cls, t: torch.Tensor, support: torch.Tensor) -> "Image":
         """A device image that is zero outside `support` (H, W) -- e.g. the
-        stored tonal values g: the host copy moves only the supported
-        values (5% of the pixels) and scatters them into zeros."""
+        stored tonal values g.  The support is recorded for callers; the
+        host copy is the dense image (a pinned dense copy beats moving the
+        5% support and scattering it into host zeros, see _to_host)."""
         img = cls(t)
         img._support = support
         return img
@@ -87,17 +96,7 @@ class Image:
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            sup = getattr(self, "_support", None)
-            if sup is not None and self._dev.is_cuda:
-                C = self._dev.shape[0]
-                idx = torch.nonzero(sup.reshape(-1)).squeeze(1)
-                vals = self._dev.reshape(C, -1)[:, idx]
-                npdt = np.float32 if self._dev.dtype == torch.float32 else np.float64
-                out = np.zeros(tuple(self._dev.shape), dtype=npdt)
-                out.reshape(C, -1)[:, _to_host(idx)] = _to_host(vals)
-                self._host = out
-            else:
-                self._host = _to_host(self._dev)
+            self._host = _to_host(self._dev)
             self._dev = None
             self._support = None
         return self._host
