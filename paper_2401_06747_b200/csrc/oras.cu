@@ -495,7 +495,13 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
     float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps) {
+  // FULLH: a full 32 x 32 block (bh == bw == 32): compile-time row / column
+  // offsets in the job's loads and stores
   constexpr int R = 32;
+  if (FULLH) {
+    bh = 32;
+    bw = 32;
+  }
   const int j = threadIdx.x & 31;
   const int bi = blockIdx.x * WJ + (threadIdx.x >> 5), ch = blockIdx.y, C = gridDim.y;
   const int tile = blockIdx.z;
@@ -505,10 +511,11 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
   const int kyb = bi / nbx, kxb = bi - kyb * nbx;
   const int y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
   const int x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
-  const float* rc = r + ((size_t)tile * C + ch) * ps;
-  const uint8_t* mt = m + (size_t)tile * ps;
-  const bool lane_ok = j < bw;
+  const bool lane_ok = FULLH || j < bw;
   const int jc = lane_ok ? j : bw - 1, gx = x0 + j;
+  // the lane's column in row 0 of the block; rows follow at stride W
+  const float* rp = r + ((size_t)tile * C + ch) * ps + (size_t)y0 * W + (x0 + jc);
+  const uint8_t* mp = m + (size_t)tile * ps + (size_t)y0 * W + (x0 + jc);
 
   // ---- load the job (branch-free, clamped addresses; invalid zeroed)
   float res[R];
@@ -516,9 +523,8 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int ic = FULLH ? s : min(s, bh - 1);
-    const size_t g = (size_t)(y0 + ic) * W + (x0 + jc);
-    res[s] = rc[g];
-    mk[s] = mt[g];
+    res[s] = rp[ic * W];
+    mk[s] = mp[ic * W];
   }
   // off: bit s set where row s is masked or outside the block (q = 0 there,
   // and A p = p, which is 0 outside the block)
@@ -547,12 +553,12 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
   float v[R];
   const long it = warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh,
                                            tau, cap, j);
-  float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
-  const float* wb = weights + (size_t)bi * bh * bw;
+  float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw) + j;
+  const float* wb = weights + (size_t)bi * bh * bw + j;
   if (lane_ok) {
 #pragma unroll
     for (int s = 0; s < R; ++s)
-      if (FULLH || s < bh) out[s * bw + j] = wb[s * bw + j] * v[s];
+      if (FULLH || s < bh) out[s * bw] = wb[s * bw] * v[s];
   }
   if (j == 0 && g_stats_on) {
     atomicAdd(&g_oras_stats[0], 1ull);
@@ -1050,7 +1056,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                                      corr_nb, C, njobs);
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && (oras_kernel == 4 || oras_kernel == 6)) {
     const int nbl = nby * nbx;
-    const bool unit = inv_h2 == 1.0, full = bh == 32;
+    const bool unit = inv_h2 == 1.0, full = bh == 32 && bw == 32;
     // 4: four jobs per CTA; 6: one job per CTA (a finished job frees its
     // slot at once instead of waiting for the CTA's slowest job)
     const int wj = oras_kernel == 6 ? 1 : WJ;
