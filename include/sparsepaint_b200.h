@@ -278,6 +278,11 @@ int sp_oras_variant(int v);
  * hierarchy qualifies (float, two levels, <= 64x64): 1 = on (default),
  * 0 = the batched V-cycle path; v < 0 queries.  A/B aid. */
 int sp_tile_fused(int v);
+/* V-cycle graphs of multi-channel hierarchies captured afterwards run the C
+ * channels as parallel graph branches (solver.cu run_vcycle): 1 = on,
+ * 0 = one sequential chain (default, measured faster); v < 0 queries.
+ * Results are identical either way.  A/B aid. */
+int sp_channel_parallel(int v);
 /* Default sweep kernels of hierarchies created afterwards (all bit-identical
  * per element): 2 = TMA-staged residual sweeps on wide float levels
  * (mgtma.cu, default), 1 = row-marching register kernels (mgfast.cu), 0 =

@@ -59,6 +59,10 @@ static int dalloc(void** p, size_t bytes) {
 }
 
 Hier::~Hier() {
+  if (!owner) return;  // a channel view: the buffers belong to its parent
+  for (Hier* v : chv) delete v;
+  for (cudaStream_t st : ch_streams) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : ch_events) cudaEventDestroy(ev);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (cap_stream) cudaStreamDestroy(cap_stream);
   for (auto& L : lv) {
@@ -309,6 +313,85 @@ int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
   return 0;
 }
 
+// Channel-parallel V-cycles.  The C channels of an image are C independent
+// systems through a whole V-cycle (shared mask, per-channel norms and ORAS
+// thresholds; only the solve's tolerance test sums them), so the captured
+// graph runs them as C parallel branches: the compute-bound ORAS local CG of
+// one channel overlaps the HBM-bound sweeps of another, and the
+// launch-latency-bound coarse levels of the channels run side by side.
+// Every kernel is launched on a one-channel view that aliases the parent's
+// buffers at the channel's offset (results are identical: the kernels are
+// per plane and the per-plane reduction partials keep their slots).
+// Measured slower on the 4K RGB pipeline (335 vs 305 ms): the one-channel
+// launches lose the channel-fused kernels' amortised index work (the blend
+// gathers each pixel's covering blocks once for all C channels) and the
+// branches' ORAS launches mostly collide rather than interleave.  Off by
+// default (sp_channel_parallel), kept as a measured A/B option.
+static int channel_parallel_on = 0;
+int channel_parallel(int v) {
+  if (v >= 0) channel_parallel_on = v;
+  return channel_parallel_on;
+}
+
+static int make_channel_views(Hier* h) {
+  const size_t es = h->dtype == SP_F64 ? 8 : 4;
+  for (int c = 0; c < h->C; ++c) {
+    Hier* v = new Hier();
+    v->owner = false;
+    v->dtype = h->dtype;
+    v->C = 1;
+    v->ntile = 1;
+    v->cfg = h->cfg;
+    v->gamma = h->gamma;
+    v->has_values = h->has_values;
+    v->use_graphs = false;
+    v->sweep = h->sweep;
+    v->h_norms = h->h_norms;
+    v->h_active = h->h_active;
+    v->d_active = h->d_active;
+    v->d_scratch = h->d_scratch;
+    for (const Level& P : h->lv) {
+      Level L = P;
+      const size_t plane = (size_t)P.H * P.W, nbp = (size_t)P.nby * P.nbx * P.bh * P.bw;
+      auto off = [&](void* p, size_t n) { return p ? (void*)((char*)p + c * n * es) : p; };
+      L.u = off(P.u, plane);
+      L.b = off(P.b, plane);
+      L.r = off(P.r, plane);
+      L.values = off(P.values, plane);
+      L.corr = off(P.corr, nbp);
+      L.partial = P.partial + (size_t)c * P.npart;
+      L.counter = P.counter + c;
+      L.norms = P.norms + c;
+      v->lv.push_back(L);
+    }
+    h->chv.push_back(v);
+    cudaStream_t st;
+    cudaEvent_t ev;
+    SP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    SP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    h->ch_streams.push_back(st);
+    h->ch_events.push_back(ev);
+  }
+  cudaEvent_t fork;
+  SP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  h->ch_events.push_back(fork);  // the last event forks the branches
+  return 0;
+}
+
+template <typename T>
+static int vcycle_channels(Hier* h, cudaStream_t cap) {
+  if (h->chv.empty()) SP_TRY(make_channel_views(h));
+  cudaEvent_t fork = h->ch_events.back();
+  SP_CUDA(cudaEventRecord(fork, cap));
+  for (int c = 0; c < h->C; ++c) {
+    SP_CUDA(cudaStreamWaitEvent(h->ch_streams[c], fork, 0));
+    SP_TRY(vcycle_lv<T>(h->chv[c], 0, true, h->ch_streams[c]));
+    SP_CUDA(cudaEventRecord(h->ch_events[c], h->ch_streams[c]));
+    SP_CUDA(cudaStreamWaitEvent(cap, h->ch_events[c], 0));
+  }
+  return 0;
+}
+
 template <typename T>
 static int run_vcycle(Hier* h, cudaStream_t s) {
   // precondition: level-0 r/norms are current (residual_lv(0) ran)
@@ -319,7 +402,8 @@ static int run_vcycle(Hier* h, cudaStream_t s) {
     if (!h->cap_stream) SP_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t g;
     SP_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
-    int rc = vcycle_lv<T>(h, 0, true, h->cap_stream);
+    const bool par = channel_parallel_on && h->C > 1 && h->ntile == 1 && h->C <= 8;
+    int rc = par ? vcycle_channels<T>(h, h->cap_stream) : vcycle_lv<T>(h, 0, true, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc) { if (e == cudaSuccess) cudaGraphDestroy(g); return rc; }
     SP_CUDA(e);

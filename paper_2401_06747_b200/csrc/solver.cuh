@@ -41,6 +41,12 @@ struct Hier {
   int* h_active = nullptr;     // pinned [ntile]
   int* d_active = nullptr;     // [ntile] read by every V-cycle kernel
   void* d_scratch = nullptr;   // reduction partials
+  // channel-parallel V-cycle (solver.cu run_vcycle): C non-owning one-channel
+  // views of this hierarchy and the streams their graph branches run on
+  bool owner = true;
+  std::vector<Hier*> chv;
+  std::vector<cudaStream_t> ch_streams;
+  std::vector<cudaEvent_t> ch_events;
   ~Hier();
 };
 

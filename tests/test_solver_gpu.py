@@ -174,3 +174,29 @@ def test_oras_warp_kernel_bit_identical_ras():
     assert ma == mb
     assert np.array_equal(ga, gb)
 
+
+
+@pytest.mark.parametrize("shape", [(3, 301, 512), (3, 2160 // 4, 3840 // 4), (2, 100, 150)])
+def test_channel_parallel_vcycle_bit_identical(shape):
+    """V-cycle graphs with the C channels as parallel branches on one-channel
+    views (solver.cu run_vcycle) vs one sequential chain: bitwise equal."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 5)
+    mask = (np.random.default_rng(6).random((h, w)) < 0.05).astype(np.uint8)
+    prev = lib.sp_channel_parallel(-1)
+    outs = []
+    try:
+        for on in (0, 1):
+            lib.sp_channel_parallel(on)
+            _POOL.clear()
+            u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=1e-6))
+            outs.append((u.data, rep.iterations, rep.residuals))
+    finally:
+        lib.sp_channel_parallel(prev)
+        _POOL.clear()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
