@@ -144,6 +144,14 @@ int sp_hier_level_mask(void* hier, int level, uint8_t* out, void* stream);
  * V-cycles.  Synchronizes the stream once per V-cycle in tolerance mode. */
 int sp_hier_solve(void* hier, const void* bsym, void* u, int init_mode, double tol,
                   int cycles, int max_cycles, sp_solve_report* rep, void* stream);
+/* sp_hier_solve with separate start and result buffers (no copy of the
+ * caller's warm start) and, for src_mode 1, the right-hand side formed from
+ * stored values: src = x, b~ = sym_rhs(where(mask, x, 0)) (solver.py:501-502,
+ * tonal.py:136-137) written straight into the hierarchy.  src_mode 0: src is
+ * b~.  u_in is read for init_mode 1 only (NULL = u_out holds the start). */
+int sp_hier_solve_ex(void* hier, const void* src, int src_mode, const void* u_in, void* u_out,
+                     int init_mode, double tol, int cycles, int max_cycles,
+                     sp_solve_report* rep, void* stream);
 int sp_hier_vcycle(void* hier, const void* bsym, void* u, void* stream);
 /* batched solve_sym: active_h (HOST int[ntile], NULL = all) selects the tiles
  * to solve; iters_h / conv_h (HOST int[ntile], may be NULL) receive the

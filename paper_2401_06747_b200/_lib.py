@@ -51,6 +51,7 @@ _SIGS = {
     "sp_hier_set_mask": [P, P, P, P],
     "sp_hier_level_mask": [P, c_int, P, P],
     "sp_hier_solve": [P, P, P, c_int, c_double, c_int, c_int, P, P],
+    "sp_hier_solve_ex": [P, P, c_int, P, P, c_int, c_double, c_int, c_int, P, P],
     "sp_hier_vcycle": [P, P, P, P],
     "sp_hier_solve_tiles": [P, P, P, c_int, c_double, c_int, c_int, P, P, P, P],
     "sp_nccl_unique_id": [P],

@@ -309,6 +309,14 @@ int sp_hier_solve(void* h, const void* bsym, void* u, int init_mode, double tol,
                     nullptr, nullptr, nullptr, (SolveReport*)rep);
 }
 
+int sp_hier_solve_ex(void* h, const void* src, int src_mode, const void* u_in, void* u_out,
+                     int init_mode, double tol, int cycles, int max_cycles, sp_solve_report* rep,
+                     void* s) {
+  if (src_mode != 0 && src_mode != 1) { sp::set_error("bad src_mode %d", src_mode); return -3; }
+  return hier_solve((Hier*)h, src, u_out, init_mode, tol, cycles, max_cycles, STREAM(s),
+                    nullptr, nullptr, nullptr, (SolveReport*)rep, u_in, src_mode);
+}
+
 int sp_hier_solve_tiles(void* h, const void* bsym, void* u, int init_mode, double tol,
                         int cycles, int max_cycles, const int* active_h, int* iters_h,
                         int* conv_h, void* s) {

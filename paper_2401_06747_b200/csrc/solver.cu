@@ -450,10 +450,11 @@ static int upload_active(Hier* h, cudaStream_t s) {
 template <typename T>
 static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, int cycles,
                    int max_cycles, cudaStream_t s, const int* active_in, int* iters,
-                   int* conv, SolveReport* rep) {
+                   int* conv, SolveReport* rep, const T* u_in = nullptr, int src_mode = 0) {
   // batched cold tile solves to a tolerance (RAS block-local products): the
   // fused on-chip kernel when the hierarchy qualifies (tilesolve.cu)
-  if (sizeof(T) == 4 && active_in && !rep && init_mode == 0 && tol >= 0 && tile_fused_ok(h))
+  if (sizeof(T) == 4 && active_in && !rep && init_mode == 0 && tol >= 0 && src_mode == 0 &&
+      tile_fused_ok(h))
     return tile_solve_fused(h, (const float*)bsym, (float*)u_io, tol, max_cycles, s, active_in,
                             iters, conv);
   Level& L0 = h->lv[0];
@@ -465,7 +466,8 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
   for (int t = 0; t < nt; ++t) h->h_active[t] = active_in ? (active_in[t] != 0) : 1;
   SP_TRY(upload_active(h, s));
   if (init_mode == 1) {
-    SP_CUDA(cudaMemcpyAsync(L0.u, u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(L0.u, u_in ? u_in : u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice,
+                            s));
   } else if (init_mode == 2 && h->lv.size() > 1) {
     if (!h->has_values) {
       set_error("hierarchy was built without stored values");
@@ -475,7 +477,10 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
   } else {
     SP_CUDA(cudaMemsetAsync(L0.u, 0, sizeof(T) * n, s));
   }
-  SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  if (src_mode == 1)  // b~ = sym_rhs(where(mask, x, 0)) straight into level 0
+    SP_TRY(masked_sym_rhs<T>(bsym, L0.mask, (T*)L0.b, C, L0.H, L0.W, s, nt, h->d_active));
+  else
+    SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
   SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s, nt, h->d_active));
   std::vector<int> done(nt, 0), cv(nt, 0);
   if (tol < 0) {
@@ -534,12 +539,14 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
 
 int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
                int cycles, int max_cycles, cudaStream_t s, const int* active_in, int* iters,
-               int* conv, SolveReport* rep) {
+               int* conv, SolveReport* rep, const void* u_in, int src_mode) {
   if (h->dtype == SP_F64)
     return solve_t<double>(h, (const double*)bsym, (double*)u_io, init_mode, tol, cycles,
-                           max_cycles, s, active_in, iters, conv, rep);
+                           max_cycles, s, active_in, iters, conv, rep, (const double*)u_in,
+                           src_mode);
   return solve_t<float>(h, (const float*)bsym, (float*)u_io, init_mode, tol, cycles,
-                        max_cycles, s, active_in, iters, conv, rep);
+                        max_cycles, s, active_in, iters, conv, rep, (const float*)u_in,
+                        src_mode);
 }
 
 template <typename T>

@@ -62,9 +62,12 @@ struct SolveReport {
 int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
                 int with_values, int ntile = 1);
 int hier_set_mask(Hier* h, const uint8_t* mask, const void* values, cudaStream_t s);
+// u_in (optional): the start iterate for init_mode 1 (default: u_io itself);
+// src_mode 1: `bsym` holds stored values x and b~ = C~ (mask ? x : 0) is
+// formed directly in the hierarchy's level-0 right-hand side
 int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
                int cycles, int max_cycles, cudaStream_t s, const int* active_in, int* iters,
-               int* conv, SolveReport* rep);
+               int* conv, SolveReport* rep, const void* u_in = nullptr, int src_mode = 0);
 int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s);
 
 // tilesolve.cu: fused on-chip cold solve of a batch of small tiles

@@ -341,6 +341,14 @@ __global__ void __launch_bounds__(PT, 4) k_tv_up(TV a) {
   const int H1 = TH1 ? TH1 : a.H1, W1 = TW1 ? TW1 : a.W1;
   (void)H1; (void)W1; (void)H0; (void)W0;
   const int n0 = H0 * W0, n1 = H1 * W1;
+  // the bilinear axis weights of every fine row / column, once per CTA
+  __shared__ int ay0[TMAX], ay1[TMAX], ax0[TMAX], ax1[TMAX];
+  __shared__ double awy[TMAX], awx[TMAX];
+  if (threadIdx.x < H0) paxis(threadIdx.x, H1, ay0[threadIdx.x], ay1[threadIdx.x], awy[threadIdx.x]);
+  if (threadIdx.x >= 64 && threadIdx.x - 64 < W0) {
+    const int x = threadIdx.x - 64;
+    paxis(x, W1, ax0[x], ax1[x], awx[x]);
+  }
   load_mask(M, a.m0 + (size_t)tile * n0, n0);
   for (int c = 0; c < a.C; ++c) {
     const size_t o = ((size_t)tile * a.C + c) * n0, o1 = ((size_t)tile * a.C + c) * n1;
@@ -354,10 +362,8 @@ __global__ void __launch_bounds__(PT, 4) k_tv_up(TV a) {
         v = a.b0[o + k];
       } else {
         const int y = k / W0, x = k - y * W0;
-        int y0, y1, x0, x1;
-        double wy, wx;
-        paxis(y, H1, y0, y1, wy);
-        paxis(x, W1, x0, x1, wx);
+        const int y0 = ay0[y], y1 = ay1[y], x0 = ax0[x], x1 = ax1[x];
+        const double wy = awy[y], wx = awx[x];
         const double e = (1.0 - wy) * ((1.0 - wx) * (double)U1[y0 * W1 + x0] +
                                        wx * (double)U1[y0 * W1 + x1]) +
                          wy * ((1.0 - wx) * (double)U1[y1 * W1 + x0] +

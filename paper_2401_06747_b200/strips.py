@@ -232,6 +232,7 @@ class StripHierarchy:
     def __init__(self, owner: "StripSolver", mask_t, values_t):
         self.owner = owner
         H, W = mask_t.shape
+        self.mask_t = mask_t
         self.channels = owner.channels
         self.height, self.width = H, W
         self.cfg = owner.cfg
@@ -257,10 +258,12 @@ class StripHierarchy:
         return n.value
 
     def solve_sym(self, bsym, init=None, tol=None, cycles=None, max_cycles=None,
-                  cascade=False):
+                  cascade=False, values=False):
         cfg = self.cfg
         t0 = time.perf_counter()
         b = bsym.to(torch.float32).contiguous()
+        if values:  # stored values x -> b~ = sym_rhs(where(mask, x, 0))
+            b = _masked_rhs(b, self.mask_t)
         if init is not None:
             u = init.to(torch.float32).clone()
             mode = 1

@@ -120,7 +120,7 @@ class _TonalSystem:
         self.dtype = solver.cfg.torch_dtype
         self.solves = 0
 
-    def _solve(self, bsym, warm, tol=None, cycles=None):
+    def _solve(self, bsym, warm, tol=None, cycles=None, values=False):
         self.solves += 1
         if tol is None:
             if self.inner_tol is not None:
@@ -129,12 +129,12 @@ class _TonalSystem:
                 tol = self.cold_tol
         u, _ = self.hier.solve_sym(bsym, init=warm, tol=tol,
                                    cycles=self.inner_cycles if cycles is None else cycles,
-                                   max_cycles=self.cold_max_cycles)
+                                   max_cycles=self.cold_max_cycles, values=values)
         return u
 
     def apply_B(self, x, warm=None, tol=None, cycles=None):
-        bsym = _masked_rhs(x.to(self.dtype).contiguous(), self.mask)
-        return self._solve(bsym, warm, tol, cycles)
+        # B x = solve(A~, C~ (mask ? x : 0)): the rhs is formed in the hierarchy
+        return self._solve(x.to(self.dtype).contiguous(), warm, tol, cycles, values=True)
 
     def apply_Bt(self, y, warm=None, tol=None, cycles=None):
         w = self._solve(y.to(self.dtype).contiguous(), warm, tol, cycles)
@@ -185,8 +185,8 @@ def initial_state(f: Image, mask: Mask, solver: InpaintSolver | None = None,
 def _final_state(f64, mask_t, sys_: _TonalSystem, g_best, warm, history, iterations,
                  final_tol) -> TonalState:
     """tonal.py:183-195: tight reconstruction of the best values."""
-    bsym = _masked_rhs(g_best.to(sys_.dtype).contiguous(), mask_t)
-    u, rep = sys_.hier.solve_sym(bsym, init=warm, tol=final_tol)
+    u, rep = sys_.hier.solve_sym(g_best.to(sys_.dtype).contiguous(), init=warm, tol=final_tol,
+                                 values=True)
     sys_.solves += 1
     _enforce(u, g_best.to(u.dtype).contiguous(), mask_t)
     # g is zero off the mask by construction; make it exact and let the host
