@@ -22,5 +22,5 @@ for v, tf, cp in variants * 2:
         mask, st, hist, _ = sp.run_pipeline(sp.Image(f), cfg)
     e1.record()
     torch.cuda.synchronize()
-    print(f"oras variant {v} tile_fused {tf} chan_par {cp}: {e0.elapsed_time(e1) / 2:.1f} ms/pipeline  mse={st.mse:.9f} "
+    print(f"oras {v} tile_fused {tf} chan_par {cp}: {e0.elapsed_time(e1) / 2:.1f} ms/pipeline  mse={st.mse:.9f} "
           f"dd_mse={hist[-1][2]:.9f} count={mask.count}", flush=True)
