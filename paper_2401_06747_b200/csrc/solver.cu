@@ -63,6 +63,7 @@ Hier::~Hier() {
   for (Hier* v : chv) delete v;
   for (cudaStream_t st : ch_streams) cudaStreamDestroy(st);
   for (cudaEvent_t ev : ch_events) cudaEventDestroy(ev);
+  if (up_ev) cudaEventDestroy(up_ev);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (cap_stream) cudaStreamDestroy(cap_stream);
   for (auto& L : lv) {
@@ -441,9 +442,17 @@ static int cascade_t(Hier* h, cudaStream_t s) {
   return 0;
 }
 
-static int upload_active(Hier* h, cudaStream_t s) {
+int upload_active(Hier* h, cudaStream_t s) {
+  if (!h->up_ev) SP_CUDA(cudaEventCreateWithFlags(&h->up_ev, cudaEventDisableTiming));
   SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * h->ntile,
                           cudaMemcpyHostToDevice, s));
+  SP_CUDA(cudaEventRecord(h->up_ev, s));
+  return 0;
+}
+
+// waits for the last upload from h_active only, not for all queued work
+int active_host_ready(Hier* h) {
+  if (h->up_ev) SP_CUDA(cudaEventSynchronize(h->up_ev));
   return 0;
 }
 
@@ -462,7 +471,7 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
   size_t per = (size_t)C * L0.H * L0.W, n = per * nt;
   if (rep) { rep->iterations = 0; rep->nres = 0; rep->converged = 0; }
   // the pinned flag buffer may still feed an earlier async upload
-  SP_CUDA(cudaStreamSynchronize(s));
+  SP_TRY(active_host_ready(h));
   for (int t = 0; t < nt; ++t) h->h_active[t] = active_in ? (active_in[t] != 0) : 1;
   SP_TRY(upload_active(h, s));
   if (init_mode == 1) {
@@ -514,18 +523,21 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
                               cudaMemcpyDeviceToHost, s));
       SP_CUDA(cudaStreamSynchronize(s));
       int live = 0;
+      bool changed = false;
       for (int t = 0; t < nt; ++t) {
         if (!h->h_active[t]) continue;
         double tot = 0.0;
         for (int c = 0; c < C; ++c) tot += h->h_norms[(size_t)t * C + c];
         double rel = std::sqrt(tot) / scale[t];
         if (t == 0 && rep && rep->nres < SP_MAX_RES) rep->residuals[rep->nres++] = rel;
-        if (rel <= tol) { cv[t] = 1; h->h_active[t] = 0; continue; }
-        if (done[t] >= max_cycles) { h->h_active[t] = 0; continue; }
+        if (rel <= tol) { cv[t] = 1; h->h_active[t] = 0; changed = true; continue; }
+        if (done[t] >= max_cycles) { h->h_active[t] = 0; changed = true; continue; }
         ++live;
       }
       if (!live) break;
-      SP_TRY(upload_active(h, s));
+      // the device flags already match unless a tile stopped (one image:
+      // never), so the common V-cycle goes straight to the graph launch
+      if (changed) SP_TRY(upload_active(h, s));
       SP_TRY(run_vcycle<T>(h, s));
       for (int t = 0; t < nt; ++t) done[t] += h->h_active[t];
     }
@@ -553,7 +565,7 @@ template <typename T>
 static int vcycle_once_t(Hier* h, const T* bsym, T* u_io, cudaStream_t s) {
   Level& L0 = h->lv[0];
   size_t n = (size_t)h->C * L0.H * L0.W * h->ntile;
-  SP_CUDA(cudaStreamSynchronize(s));
+  SP_TRY(active_host_ready(h));
   for (int t = 0; t < h->ntile; ++t) h->h_active[t] = 1;
   SP_TRY(upload_active(h, s));
   SP_CUDA(cudaMemcpyAsync(L0.u, u_io, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
@@ -592,8 +604,9 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
     case 3: *bytes = (double)(2 * es * vec + plane * nt + es * vec / 4); break;    // u, b, mask, rc
     default: set_error("unknown kernel id %d", which); return -2;
   }
+  SP_TRY(active_host_ready(h));
   for (int t = 0; t < nt; ++t) h->h_active[t] = 1;
-  SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * nt, cudaMemcpyHostToDevice, s));
+  SP_TRY(upload_active(h, s));
   Level* G = h->lv.size() > 1 ? &h->lv[1] : nullptr;
   auto launch = [&]() -> int {
     switch (which) {
@@ -641,9 +654,9 @@ template <typename T>
 static int residual_out_t(Hier* h, int lv, void* r_out, double* norms_out, cudaStream_t s) {
   if (lv < 0 || lv >= (int)h->lv.size()) { set_error("no level %d", lv); return -2; }
   Level& L = h->lv[lv];
+  SP_TRY(active_host_ready(h));
   for (int t = 0; t < h->ntile; ++t) h->h_active[t] = 1;
-  SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * h->ntile,
-                          cudaMemcpyHostToDevice, s));
+  SP_TRY(upload_active(h, s));
   SP_TRY(residual_lv<T>(h, lv, true, s));
   const size_t n = (size_t)h->C * L.H * L.W * h->ntile;
   SP_CUDA(cudaMemcpyAsync(r_out, L.r, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));

@@ -44,6 +44,7 @@ struct Hier {
   // channel-parallel V-cycle (solver.cu run_vcycle): C non-owning one-channel
   // views of this hierarchy and the streams their graph branches run on
   bool owner = true;
+  cudaEvent_t up_ev = nullptr;  // recorded after each h_active upload
   std::vector<Hier*> chv;
   std::vector<cudaStream_t> ch_streams;
   std::vector<cudaEvent_t> ch_events;
@@ -69,6 +70,9 @@ int hier_solve(Hier* h, const void* bsym, void* u_io, int init_mode, double tol,
                int cycles, int max_cycles, cudaStream_t s, const int* active_in, int* iters,
                int* conv, SolveReport* rep, const void* u_in = nullptr, int src_mode = 0);
 int hier_vcycle(Hier* h, const void* bsym, void* u_io, cudaStream_t s);
+// h_active (pinned) may be rewritten once the last upload from it is done
+int active_host_ready(Hier* h);
+int upload_active(Hier* h, cudaStream_t s);
 
 // tilesolve.cu: fused on-chip cold solve of a batch of small tiles
 bool tile_fused_ok(const Hier* h);

@@ -431,9 +431,11 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
   Level& L0 = h->lv[0];
   Level& L1 = h->lv[1];
   const size_t n = (size_t)nt * C * L0.H * L0.W;
-  SP_CUDA(cudaStreamSynchronize(s));  // pinned buffers may feed an earlier copy
+  // the pinned flags may still feed an earlier upload (waits for that copy
+  // only, not for the caller's queued work)
+  SP_TRY(active_host_ready(h));
   for (int t = 0; t < nt; ++t) h->h_active[t] = active_in ? (active_in[t] != 0) : 1;
-  SP_CUDA(cudaMemcpyAsync(h->d_active, h->h_active, sizeof(int) * nt, cudaMemcpyHostToDevice, s));
+  SP_TRY(upload_active(h, s));
   SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
   double* scale = (double*)h->d_scratch;
   int* done = (int*)(scale + nt);
@@ -468,23 +470,32 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
                                     (long)L.bh * L.bw, 1.0, (const float*)L.weights,
                                     (float*)L.corr, s, nt, h->d_active, stride);
   };
+  // V-cycles run in batches between reads of the live-block count: a block
+  // that stops inside a batch is skipped by every later launch (each kernel
+  // tests `active`), so batching changes no result, only the number of host
+  // round trips.  The local products converge in 3 V-cycles (4K RAS), so the
+  // first batch is 3, then one V-cycle per read.
+  int batch = 3;
   while (true) {
+    for (int b = 0; b < batch; ++b) {
+      SP_CUDA(cudaMemsetAsync(live, 0, sizeof(int), s));
+      SP_TRY(oras(L0));                     // pre-smoothing, level 0
+      k_down<<<nt, PT, 0, s>>>(a);
+      SP_CHECK_LAUNCH();
+      SP_TRY(oras(L1));                     // coarsest, sweep 1
+      k_coarse<<<nt, PT, 0, s>>>(a);
+      SP_CHECK_LAUNCH();
+      SP_TRY(oras(L1));                     // coarsest, sweep 2
+      k_up<<<nt, PT, 0, s>>>(a);
+      SP_CHECK_LAUNCH();
+      SP_TRY(oras(L0));                     // post-smoothing, level 0
+      k_close<<<nt, PT, 0, s>>>(a);
+      SP_CHECK_LAUNCH();
+    }
     SP_CUDA(cudaMemcpyAsync(hl, live, sizeof(int), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     if (hl[0] == 0) break;
-    SP_CUDA(cudaMemsetAsync(live, 0, sizeof(int), s));
-    SP_TRY(oras(L0));                       // pre-smoothing, level 0
-    k_down<<<nt, PT, 0, s>>>(a);
-    SP_CHECK_LAUNCH();
-    SP_TRY(oras(L1));                       // coarsest, sweep 1
-    k_coarse<<<nt, PT, 0, s>>>(a);
-    SP_CHECK_LAUNCH();
-    SP_TRY(oras(L1));                       // coarsest, sweep 2
-    k_up<<<nt, PT, 0, s>>>(a);
-    SP_CHECK_LAUNCH();
-    SP_TRY(oras(L0));                       // post-smoothing, level 0
-    k_close<<<nt, PT, 0, s>>>(a);
-    SP_CHECK_LAUNCH();
+    batch = 1;
   }
   SP_CUDA(cudaMemcpyAsync(u_out, L0.u, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
   SP_CUDA(cudaMemcpyAsync(hl, done, sizeof(int) * 2 * nt, cudaMemcpyDeviceToHost, s));
