@@ -94,6 +94,7 @@ _SIGS = {
     "sp_march_variant": [c_int],
     "sp_tile_fused": [c_int],
     "sp_channel_parallel": [c_int],
+    "sp_graph_loop": [c_int],
     "sp_hier_residual": [P, c_int, P, P, P],
     "sp_geo_export": [P, P, P, P, P, P, P, P, c_long, P],
 }

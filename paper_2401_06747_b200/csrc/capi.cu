@@ -478,9 +478,10 @@ namespace sp {
 int march_default(int v);
 }
 extern "C" int sp_march_variant(int v) { return sp::march_default(v); }
-namespace sp { int tile_fused(int v); int channel_parallel(int v); }
+namespace sp { int tile_fused(int v); int channel_parallel(int v); int graph_loop(int v); }
 extern "C" int sp_tile_fused(int v) { return sp::tile_fused(v); }
 extern "C" int sp_channel_parallel(int v) { return sp::channel_parallel(v); }
+extern "C" int sp_graph_loop(int v) { return sp::graph_loop(v); }
 
 // ---- dithered initial mask (spatial.py:107-148) -------------------------------
 namespace sp {

@@ -64,6 +64,9 @@ Hier::~Hier() {
   for (cudaStream_t st : ch_streams) cudaStreamDestroy(st);
   for (cudaEvent_t ev : ch_events) cudaEventDestroy(ev);
   if (up_ev) cudaEventDestroy(up_ev);
+  if (loop_exec) cudaGraphExecDestroy(loop_exec);
+  if (loop_ctl) cudaFree(loop_ctl);
+  if (h_loop) cudaFreeHost(h_loop);
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   if (cap_stream) cudaStreamDestroy(cap_stream);
   for (auto& L : lv) {
@@ -180,6 +183,7 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
   size_t scratch = sizeof(double) * (1024 + 8) * (size_t)ntile + 256;
   if (cudaMallocHost((void**)&h->h_norms, sizeof(double) * ntc) != cudaSuccess ||
       cudaMallocHost((void**)&h->h_active, sizeof(int) * ntile) != cudaSuccess ||
+      cudaMallocHost(&h->h_loop, 4096) != cudaSuccess ||
       cudaMalloc((void**)&h->d_active, sizeof(int) * ntile) != cudaSuccess ||
       cudaMalloc(&h->d_scratch, scratch) != cudaSuccess) {
     set_error("hierarchy bookkeeping alloc failed");
@@ -456,6 +460,147 @@ int active_host_ready(Hier* h) {
   return 0;
 }
 
+// ---- device-driven tolerance loop --------------------------------------------
+// solver.py:351-369 without a host round trip per V-cycle: the stop test
+// (relative residual over the channels, tolerance, cycle cap) runs in a
+// one-thread kernel that sets the conditions of a WHILE node (continue the
+// loop) and of an IF node (run the V-cycle + residual of this iteration).
+// The whole solve is one graph launch; the host reads the iteration record
+// (count, converged flag, relative residual history) once at the end.
+static int graph_loop_on = 1;
+int graph_loop(int v) {
+  if (v >= 0) graph_loop_on = v;
+  return graph_loop_on;
+}
+
+struct LoopCtl {  // <= 4096 bytes (h_loop)
+  double tol;
+  double scale;
+  int max_cycles;
+  int done;
+  int conv;
+  int nres;
+  double res[SP_MAX_RES];
+};
+
+__global__ void k_loop_init(LoopCtl* c, double tol, int max_cycles, const double* bn) {
+  const double b = sqrt(bn[0]);
+  c->tol = tol;
+  c->scale = b > 0 ? b : 1.0;
+  c->max_cycles = max_cycles;
+  c->done = 0;
+  c->conv = 0;
+  c->nres = 0;
+}
+
+__global__ void k_loop_check(LoopCtl* c, const double* norms, int C,
+                             cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
+  double tot = 0.0;
+  for (int ch = 0; ch < C; ++ch) tot += norms[ch];
+  const double rel = sqrt(tot) / c->scale;
+  if (c->nres < SP_MAX_RES) c->res[c->nres++] = rel;
+  unsigned go = 0;
+  if (rel <= c->tol) c->conv = 1;
+  else if (c->done < c->max_cycles) { go = 1; c->done += 1; }
+  cudaGraphSetConditional(hw, go);
+  cudaGraphSetConditional(hi, go);
+}
+
+template <typename T>
+static int build_loop_graph(Hier* h) {
+  Level& L0 = h->lv[0];
+  if (!h->cap_stream) SP_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  if (!h->loop_ctl) SP_CUDA(cudaMalloc(&h->loop_ctl, sizeof(LoopCtl)));
+  cudaGraph_t g;
+  SP_CUDA(cudaGraphCreate(&g, 0));
+  int rc = 0;
+  cudaGraphConditionalHandle hw, hi;
+  cudaGraphNode_t wnode, cnode, inode;
+  cudaGraphNodeParams wp = {};
+  cudaGraphNodeParams ip = {};
+  cudaGraph_t body, ifbody;
+  size_t nn = 0;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
+  if (e == cudaSuccess) {
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    e = cudaGraphAddNode(&wnode, g, nullptr, 0, &wp);
+  }
+  if (e == cudaSuccess) {
+    body = wp.conditional.phGraph_out[0];
+    e = cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault);
+  }
+  if (e == cudaSuccess) {
+    // the stop test (captured: a kernel node of the WHILE body)
+    e = cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      k_loop_check<<<1, 1, 0, h->cap_stream>>>((LoopCtl*)h->loop_ctl, L0.norms, h->C, hw, hi);
+      cudaError_t le = cudaGetLastError();
+      e = cudaStreamEndCapture(h->cap_stream, &body);
+      if (e == cudaSuccess) e = le;
+    }
+  }
+  if (e == cudaSuccess) {
+    size_t nb = 1;
+    e = cudaGraphGetNodes(body, &cnode, &nb);
+  }
+  if (e == cudaSuccess) {
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    e = cudaGraphAddNode(&inode, body, &cnode, 1, &ip);
+  }
+  if (e == cudaSuccess) {
+    ifbody = ip.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(h->cap_stream, ifbody, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      // precondition of vcycle_lv: level-0 r/norms current (the previous
+      // iteration's residual, or the one launched before the graph)
+      rc = vcycle_lv<T>(h, 0, true, h->cap_stream);
+      if (!rc) rc = residual_lv<T>(h, 0, true, h->cap_stream);
+      e = cudaStreamEndCapture(h->cap_stream, &ifbody);
+    }
+  }
+  if (e == cudaSuccess && !rc) {
+    cudaGraphGetNodes(ifbody, nullptr, &nn);
+    h->loop_nodes = (long long)nn;
+    e = cudaGraphInstantiate(&h->loop_exec, g, 0);
+  }
+  cudaGraphDestroy(g);
+  if (rc) return rc;
+  SP_CUDA(e);
+  return 0;
+}
+
+// tolerance mode of solve_t for one image: L0.u / L0.b set and enforced;
+// bn = ||b~||^2 on the device.  Fills done[0] / cv[0] and the report.
+template <typename T>
+static int solve_loop_t(Hier* h, double tol, int max_cycles, const double* bn, cudaStream_t s,
+                        int* done, int* cv, SolveReport* rep) {
+  if (!h->loop_exec) SP_TRY(build_loop_graph<T>(h));
+  LoopCtl* c = (LoopCtl*)h->loop_ctl;
+  k_loop_init<<<1, 1, 0, s>>>(c, tol, max_cycles, bn);
+  SP_CHECK_LAUNCH();
+  SP_TRY(residual_lv<T>(h, 0, true, s));
+  SP_CUDA(cudaGraphLaunch(h->loop_exec, s));
+  LoopCtl* hc = (LoopCtl*)h->h_loop;
+  SP_CUDA(cudaMemcpyAsync(hc, c, sizeof(LoopCtl), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  count_launches(2 + (long long)hc->done * h->loop_nodes);
+  done[0] = hc->done;
+  cv[0] = hc->conv;
+  if (rep) {
+    rep->nres = 0;
+    for (int i = 0; i < hc->nres && i < SP_MAX_RES; ++i) rep->residuals[rep->nres++] = hc->res[i];
+  }
+  return 0;
+}
+
 template <typename T>
 static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, int cycles,
                    int max_cycles, cudaStream_t s, const int* active_in, int* iters,
@@ -510,6 +655,14 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
     unsigned* counter = (unsigned*)(bn + nt);
     SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
     SP_TRY(chan_reduce<T>(0, (const T*)L0.b, nullptr, nullptr, per, nt, part, counter, bn, s));
+    if (nt == 1 && h->use_graphs && graph_loop_on && h->h_loop) {
+      SP_TRY(solve_loop_t<T>(h, tol, max_cycles, bn, s, done.data(), cv.data(), rep));
+      if (rep) { rep->iterations = done[0]; rep->converged = cv[0]; }
+      if (iters) iters[0] = done[0];
+      if (conv) conv[0] = cv[0];
+      SP_CUDA(cudaMemcpyAsync(u_io, L0.u, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+      return 0;
+    }
     std::vector<double> scale(nt);
     SP_CUDA(cudaMemcpyAsync(h->h_norms, bn, sizeof(double) * nt, cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));

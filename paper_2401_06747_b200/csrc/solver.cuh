@@ -45,6 +45,13 @@ struct Hier {
   // views of this hierarchy and the streams their graph branches run on
   bool owner = true;
   cudaEvent_t up_ev = nullptr;  // recorded after each h_active upload
+  // device-driven tolerance loop (solver.cu solve_loop_t): one graph launch
+  // per solve, a WHILE conditional node around {stop test; IF{V-cycle;
+  // residual}}; loop_ctl holds the test's inputs and the iteration record
+  cudaGraphExec_t loop_exec = nullptr;
+  void* loop_ctl = nullptr;
+  void* h_loop = nullptr;       // pinned copy of loop_ctl (read back once)
+  long long loop_nodes = 0;
   std::vector<Hier*> chv;
   std::vector<cudaStream_t> ch_streams;
   std::vector<cudaEvent_t> ch_events;

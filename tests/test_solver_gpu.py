@@ -200,3 +200,36 @@ def test_channel_parallel_vcycle_bit_identical(shape):
         _POOL.clear()
     assert np.array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
+
+
+@pytest.mark.parametrize("shape,tol", [((3, 301, 512), 1e-6), ((1, 256, 256), 1e-4),
+                                       ((3, 540, 960), 1e-4)])
+def test_device_driven_solve_loop_identical(shape, tol):
+    """Tolerance solves as one graph launch (WHILE / IF conditional nodes,
+    stop test on the device) vs the host-driven loop: same iterate, same
+    V-cycle count, same relative-residual history; and the cycle cap."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 7)
+    mask = (np.random.default_rng(8).random((h, w)) < 0.05).astype(np.uint8)
+    prev = lib.sp_graph_loop(-1)
+    outs = []
+    try:
+        for on in (0, 1):
+            lib.sp_graph_loop(on)
+            _POOL.clear()
+            u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=tol))
+            u2, rep2 = sp.inpaint(sp.Image(f), sp.Mask(mask),
+                                  sp.MultigridConfig(tol=1e-12, max_cycles=2), init=u)
+            outs.append((u.data, rep.iterations, rep.residuals, rep.converged,
+                         u2.data, rep2.iterations, rep2.converged))
+    finally:
+        lib.sp_graph_loop(prev)
+        _POOL.clear()
+    a, b = outs
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[4], b[4])
+    assert a[1:4] == b[1:4] and a[5:] == b[5:]
+    assert b[5] == 2 and not b[6]
