@@ -294,8 +294,9 @@ int sp_channel_parallel(int v);
 /* Tolerance-mode solves of one image as ONE graph launch: a WHILE
  * conditional node around {stop test kernel; IF{V-cycle; residual}}, the
  * stop test (solver.py:358-368) on the device, no host round trip per
- * V-cycle: 1 = on (default), 0 = host-driven loop; v < 0 queries.  Results,
- * iteration counts and residual histories are identical. */
+ * V-cycle: 1 = on, 0 = host-driven loop (default: equal speed, and the
+ * host-driven form keeps every kernel visible to CUPTI profilers); v < 0
+ * queries.  Results, iteration counts and residual histories are identical. */
 int sp_graph_loop(int v);
 /* Default sweep kernels of hierarchies created afterwards (all bit-identical
  * per element): 2 = TMA-staged residual sweeps on wide float levels

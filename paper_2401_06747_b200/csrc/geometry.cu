@@ -161,6 +161,46 @@ __global__ void k_jfa_pass_key(const unsigned* __restrict__ cur, unsigned* __res
   nxt[(size_t)y * W + x] = best;
 }
 
+// four pixels per thread for steps that are multiples of 4 (W % 4 == 0): the
+// quad x0..x0+3 and each of its 3x3 candidate quads start on a multiple of
+// 4, so every candidate row is one 16-byte load and the four pixels share
+// the bounds tests; per pixel the candidates are visited in the same order
+// with the same rule, so the labels are those of k_jfa_pass_key
+__global__ void k_jfa_pass_key4(const unsigned* __restrict__ cur, unsigned* __restrict__ nxt,
+                                int step, int H, int W) {
+  const int x0 = (blockIdx.x * BX + threadIdx.x) * 4, y = blockIdx.y * BY + threadIdx.y;
+  if (x0 >= W || y >= H) return;
+  const uint4 self = *reinterpret_cast<const uint4*>(cur + (size_t)y * W + x0);
+  unsigned best[4] = {self.x, self.y, self.z, self.w};
+  int bd[4];
+  const int big = 4 * (H * H + W * W);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bd[i] = best[i] != KNONE ? key_d2(best[i], y, x0 + i) : big;
+#pragma unroll
+  for (int oy = -1; oy <= 1; ++oy) {
+    const int ny = y + oy * step;
+    if (ny < 0 || ny >= H) continue;
+#pragma unroll
+    for (int ox = -1; ox <= 1; ++ox) {
+      if (oy == 0 && ox == 0) continue;
+      const int nx = x0 + ox * step;
+      if (nx < 0 || nx >= W) continue;
+      const uint4 q = *reinterpret_cast<const uint4*>(cur + (size_t)ny * W + nx);
+      const unsigned cand[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (cand[i] == KNONE) continue;
+        const int cd = key_d2(cand[i], y, x0 + i);
+        if (cd < bd[i] || (cd == bd[i] && best[i] != KNONE && cand[i] < best[i])) {
+          bd[i] = cd;
+          best[i] = cand[i];
+        }
+      }
+    }
+  }
+  *reinterpret_cast<uint4*>(nxt + (size_t)y * W + x0) = make_uint4(best[0], best[1], best[2], best[3]);
+}
+
 // keys -> seed indices (rank of the seed pixel), in place; fused with the
 // max squared distance of jfa_dist2 (unlabelled pixels: numba's seeds[-1])
 __global__ void k_jfa_key_finish(unsigned* __restrict__ lab, const int* __restrict__ rank,
@@ -710,7 +750,10 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
     k_jfa_key_init<<<grid2(W, H), dim3(BX, BY), 0, s>>>(mask, cur, H, W);
     SP_CHECK_LAUNCH();
     for (size_t i = 0; i < steps.size(); ++i) {
-      k_jfa_pass_key<<<grid2(W, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
+      if (steps[i] % 4 == 0 && W % 4 == 0)
+        k_jfa_pass_key4<<<grid2(W / 4, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
+      else
+        k_jfa_pass_key<<<grid2(W, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
       SP_CHECK_LAUNCH();
       std::swap(cur, nxt);
     }
