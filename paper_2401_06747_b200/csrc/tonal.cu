@@ -123,6 +123,31 @@ __global__ void k_plane_axpy(T* yout, const T* x, const T* z, const double* __re
   yout[i] = sign > 0 ? (T)(x[i] + prod) : (T)(x[i] - prod);
 }
 
+// float planes of a multiple of 4 elements (16-byte aligned): one CTA per
+// plane, the plane's active flag and coefficient read once, float4 traffic
+// (the per-element kernel above pays a 64-bit division per element)
+__global__ void __launch_bounds__(256) k_plane_axpy4(float* yout, const float* x, const float* z,
+                                                     const double* __restrict__ coef,
+                                                     double sign, int len4, int C,
+                                                     const int* __restrict__ active) {
+  const long pl = blockIdx.x;
+  if (active && !active[pl / C]) return;
+  const float a = (float)coef[pl];
+  const float4* x4 = reinterpret_cast<const float4*>(x) + pl * len4;
+  const float4* z4 = reinterpret_cast<const float4*>(z) + pl * len4;
+  float4* y4 = reinterpret_cast<float4*>(yout) + pl * len4;
+  for (int i = threadIdx.x; i < len4; i += blockDim.x) {
+    const float4 xv = x4[i], zv = z4[i];
+    float4 o;
+    if (sign > 0) {
+      o.x = xv.x + a * zv.x; o.y = xv.y + a * zv.y; o.z = xv.z + a * zv.z; o.w = xv.w + a * zv.w;
+    } else {
+      o.x = xv.x - a * zv.x; o.y = xv.y - a * zv.y; o.z = xv.z - a * zv.z; o.w = xv.w - a * zv.w;
+    }
+    y4[i] = o;
+  }
+}
+
 // rhs tiles [tile][C][bh][bw] from the image (C, H, W) at block origins
 template <typename T>
 __global__ void k_gather_tiles(const T* __restrict__ img, const int* __restrict__ oy,
@@ -261,6 +286,15 @@ int plane_axpy(T* yout, const T* x, const T* z, const double* coef, double sign,
                long nplanes, int C, const int* active, cudaStream_t s) {
   size_t n = len * nplanes;
   if (!n) return 0;
+  if (sizeof(T) == 4 && len % 4 == 0 && len / 4 < (1u << 30) &&
+      ((((uintptr_t)yout) | ((uintptr_t)x) | ((uintptr_t)z)) & 15) == 0) {
+    // same operations per element: a = T(coef), x +- a * z (no contraction)
+    k_plane_axpy4<<<(unsigned)nplanes, 256, 0, s>>>((float*)yout, (const float*)x,
+                                                    (const float*)z, coef, sign, (int)(len / 4),
+                                                    C, active);
+    SP_CHECK_LAUNCH();
+    return 0;
+  }
   k_plane_axpy<T><<<cdiv(n, 256), 256, 0, s>>>(yout, x, z, coef, sign, len, nplanes, C, active);
   SP_CHECK_LAUNCH();
   return 0;
