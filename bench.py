@@ -61,12 +61,17 @@ def _ncu_traffic(kernel):
     if not files:
         return None
     tot = 0.0
+    issue = None
     for line in open(files[-1]):
         m = re.match(r"dram__bytes_(read|write)\.sum\s+([\d.]+)\s+(\w+)", line)
         if m:
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(3), 1)
             tot += float(m.group(2)) * scale
-    return {"bytes": tot, "source": os.path.relpath(files[-1], ROOT)} if tot else None
+        m = re.match(r"sm__inst_issued\.avg\.pct_of_peak_sustained_active\s+([\d.]+)", line)
+        if m:
+            issue = float(m.group(1)) / 100.0
+    return ({"bytes": tot, "issue": issue, "source": os.path.relpath(files[-1], ROOT)}
+            if tot else None)
 
 
 def _peaks():
@@ -355,7 +360,9 @@ def run_ours(args):
             "traffic": tr["bytes"] if tr else None,
             "traffic_source": tr["source"] if tr else None,
             "peak_kind": peak_kind,
-            "note": "dominant kernel = ORAS local CG (on-chip, latency bound); "
+            "issue_utilization": tr.get("issue") if tr else None,
+            "note": "dominant kernel = ORAS local CG (on-chip, latency bound: HBM frac is low "
+                    "by nature, issue_utilization = ncu sm__inst_issued of the same capture); "
                     "stencil sweep roofline in `stencil_roofline`"}
     sten = names[0]
     trs = _ncu_traffic("k_resid_tma")
