@@ -346,10 +346,10 @@ __global__ void k_decode_tris(const unsigned long long* __restrict__ keys, long 
 template <typename V>
 __global__ void k_assign_tris(const V* __restrict__ tris, long T, const V* __restrict__ vy,
                               const V* __restrict__ vx, int H, int W, int* __restrict__ assign) {
-  // one 8-lane group per triangle (Delaunay triangles cover ~20-40 box
-  // pixels): four triangles in flight per warp, so the per-triangle vertex
+  // one 4-lane group per triangle (Delaunay triangles cover ~20-40 box
+  // pixels): eight triangles in flight per warp, so the per-triangle vertex
   // gathers overlap instead of serialising a warp's whole triangle list
-  constexpr int G = 8;
+  constexpr int G = 4;
   long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) / G;
   int lane = threadIdx.x & (G - 1);
   long nwarps = ((long)gridDim.x * blockDim.x) / G;
