@@ -167,7 +167,8 @@ class Mask:
         if isinstance(indicator, torch.Tensor):
             if indicator.dim() != 2:
                 raise ValueError("mask must be 2-D")
-            self._dev = (indicator != 0).to(torch.uint8).contiguous()
+            # bool and uint8 share the byte layout: binarise in one pass
+            self._dev = (indicator != 0).contiguous().view(torch.uint8)
             self._host = None
         else:
             arr = np.asarray(indicator)
