@@ -144,8 +144,9 @@ class GeoWorkspace:
         seeds = np.asarray(seeds).reshape(-1, 2)
         sy = _lib.to_dev(seeds[:, 0].astype(np.int32))
         sx = _lib.to_dev(seeds[:, 1].astype(np.int32))
-        call("sp_geo_load", self._g, ptr(lab_t.to(torch.int32).contiguous()), ptr(sy), ptr(sx),
-             int(seeds.shape[0]), stream())
+        lab_c = lab_t.to(torch.int32).contiguous()   # alive until the launch is queued
+        call("sp_geo_load", self._g, ptr(lab_c), ptr(sy), ptr(sx), int(seeds.shape[0]),
+             stream())
         self.m = int(seeds.shape[0])
         self.ntris = 0
 

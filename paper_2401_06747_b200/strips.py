@@ -195,30 +195,37 @@ def _cfg_of(key):
 
 
 class _GroupPool:
-    """Free strip groups per geometry key (a group owns P full-size
-    hierarchies, so they are reused across solves and pipeline runs)."""
+    """Free strip groups, least-recently released first out (a group owns P
+    full-size hierarchies, so they are reused across solves and pipeline
+    runs).  At most `keep` per key and `max_total` overall stay resident;
+    `clear()` returns them all to the device."""
 
-    def __init__(self, keep=2):
+    def __init__(self, keep=2, max_total=4):
         self.keep = keep
-        self.free = {}
+        self.max_total = max_total
+        self.free = []                      # oldest first
 
     def acquire(self, key, comm):
-        lst = self.free.get(key)
-        if lst:
-            return lst.pop()
+        for i in range(len(self.free) - 1, -1, -1):
+            if self.free[i].key == key:
+                return self.free.pop(i)
         return _StripGroup(key, comm)
 
     def release(self, g):
-        lst = self.free.setdefault(g.key, [])
-        if len(lst) < self.keep:
-            lst.append(g)
-        else:
-            g.destroy()
+        same = [x for x in self.free if x.key == g.key]
+        if len(same) >= self.keep:
+            self.free.remove(same[0])
+            same[0].destroy()
+        self.free.append(g)
+        while len(self.free) > self.max_total:
+            self.free.pop(0).destroy()
+
+    def __len__(self):
+        return len(self.free)
 
     def clear(self):
-        for lst in self.free.values():
-            for g in lst:
-                g.destroy()
+        for g in self.free:
+            g.destroy()
         self.free.clear()
 
 

@@ -398,9 +398,9 @@ class _RasBlocks:
         return out.view(self.nt, self.C)
 
     def axpy(self, yout, x, z, coef, sign, active_d):
-        call("sp_plane_axpy", dcode(x), ptr(yout), ptr(x), ptr(z), ptr(coef.contiguous()),
-             float(sign), self.bh * self.bw, self.nt * self.C, self.C, ptr(active_d),
-             stream())
+        coef_c = coef.contiguous()
+        call("sp_plane_axpy", dcode(x), ptr(yout), ptr(x), ptr(z), ptr(coef_c), float(sign),
+             self.bh * self.bw, self.nt * self.C, self.C, ptr(active_d), stream())
 
     def normal_cg(self, rhs, cap, tol):
         """tonal.py:267-294 for every tile at once (per-tile stopping)."""
@@ -535,8 +535,9 @@ def _voronoi_weights_t(lab_t, seeds_t, idx: _CellIndex, scheme="inverse-log"):
 
 def _cell_sum(idx: _CellIndex, vals):
     out = torch.empty(idx.m, dtype=torch.float64, device=vals.device)
-    call("sp_cell_sum", ptr(idx.perm), ptr(idx.start), ptr(idx.end),
-         ptr(vals.to(torch.float64).contiguous()), idx.m, ptr(out), stream())
+    vals_c = vals.to(torch.float64).contiguous()
+    call("sp_cell_sum", ptr(idx.perm), ptr(idx.start), ptr(idx.end), ptr(vals_c), idx.m,
+         ptr(out), stream())
     return out
 
 

@@ -16,9 +16,12 @@ def chan_reduce(mode, x, y=None, z=None, channels=None):
         y = y.to(x.dtype)
     if z is not None and z.dtype != torch.float64:
         z = z.to(torch.float64)
-    call("sp_chan_reduce", dcode(x), mode, ptr(x.contiguous()),
-         ptr(None if y is None else y.contiguous()),
-         ptr(None if z is None else z.contiguous()), n, C, ptr(out), stream())
+    # bind the contiguous copies so they outlive the (asynchronous) launch
+    xc = x.contiguous()
+    yc = None if y is None else y.contiguous()
+    zc = None if z is None else z.contiguous()
+    call("sp_chan_reduce", dcode(xc), mode, ptr(xc), ptr(yc), ptr(zc), n, C, ptr(out),
+         stream())
     return out
 
 
