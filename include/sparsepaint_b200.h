@@ -266,6 +266,11 @@ int sp_ras_scatter(int dtype, void* g, const void* v, const int32_t* tile_of,
                    int bh, int bw, int C, int H, int W, void* stream);
 int sp_where_mask(int dtype, const void* x, const uint8_t* mask, void* out, int C, int H, int W,
                   void* stream);
+/* neighbor_balance_init (tonal.py:389-414, scipy.ndimage.correlate with a
+ * 3x3 ones kernel, mode="constant"): g = T(u + box(f - u) / box(1)) on the
+ * mask, 0 elsewhere.  f is the f64 image [C,H,W]; u, g are [C,H,W] of dtype. */
+int sp_neighbor_balance(int dtype, const double* f, const void* u, const uint8_t* mask, void* g,
+                        int C, int H, int W, void* stream);
 int sp_masked_sym_rhs_tiles(int dtype, const void* x, const uint8_t* mask, void* out, int C,
                             int H, int W, int ntile, const int32_t* active, void* stream);
 int sp_ct_apply_tiles(int dtype, const void* w, const uint8_t* mask, void* out, int C, int H,

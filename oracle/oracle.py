@@ -978,6 +978,29 @@ def ras_tonal(f, mask, init=None, cfg=None, block=64, overlap=6, local_iters=30,
     return st
 
 
+def neighbor_balance_values(f, u, mask):
+    """tonal.py:389-410 stored values: u + correlate(f - u, ones(3,3),
+    mode="constant") / correlate(ones, ones(3,3)), cast to u's dtype, zero
+    off the mask.  scipy's NI_Correlate sums the footprint in row-major
+    offset order; an out-of-image tap adds cval * 1 = 0.0."""
+    f = np.asarray(f, np.float64)
+    u = np.asarray(u)
+    diff = f - u.astype(np.float64)
+    C, H, W = diff.shape
+    pad = np.zeros((C, H + 2, W + 2))
+    pad[:, 1:-1, 1:-1] = diff
+    one = np.zeros((H + 2, W + 2))
+    one[1:-1, 1:-1] = 1.0
+    s = np.zeros((C, H, W))
+    cnt = np.zeros((H, W))
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            s = s + pad[:, 1 + dy:1 + dy + H, 1 + dx:1 + dx + W]
+            cnt = cnt + one[1 + dy:1 + dy + H, 1 + dx:1 + dx + W]
+    vals = u.astype(np.float64) + s / cnt
+    return np.where(np.asarray(mask)[None] > 0, vals.astype(u.dtype), np.zeros((), u.dtype))
+
+
 def cgnr_tonal(f, mask, init=None, cfg=None, rel_improvement=1e-3, max_iters=100,
                inner_cycles=1, inner_tol=None, cold_tol=1e-4, final_tol=1e-6):
     """tonal.py:198-264."""

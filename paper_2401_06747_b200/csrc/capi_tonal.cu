@@ -31,6 +31,9 @@ int ras_scatter(T* g, const T* v, const int* tile_of, const int* ys, const int* 
                 int nbx, int bh, int bw, int C, int H, int W, cudaStream_t s);
 template <typename T>
 int where_mask(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s);
+template <typename T>
+int neighbor_balance(const double* f, const T* u, const uint8_t* m, T* g, int C, int H, int W,
+                     cudaStream_t s);
 }  // namespace sp
 
 using namespace sp;
@@ -118,6 +121,13 @@ int sp_where_mask(int dtype, const void* x, const uint8_t* m, void* out, int C, 
                   void* s) {
   DISPATCH(dtype, where_mask<float>((const float*)x, m, (float*)out, C, H, W, STREAM(s)),
            where_mask<double>((const double*)x, m, (double*)out, C, H, W, STREAM(s)));
+}
+
+int sp_neighbor_balance(int dtype, const double* f, const void* u, const uint8_t* m, void* g,
+                        int C, int H, int W, void* s) {
+  DISPATCH(dtype,
+           neighbor_balance<float>(f, (const float*)u, m, (float*)g, C, H, W, STREAM(s)),
+           neighbor_balance<double>(f, (const double*)u, m, (double*)g, C, H, W, STREAM(s)));
 }
 
 int sp_masked_sym_rhs_tiles(int dtype, const void* x, const uint8_t* m, void* out, int C, int H,

@@ -213,7 +213,53 @@ __global__ void k_where_mask(const T* __restrict__ x, const uint8_t* __restrict_
   out[i] = m[i % n] ? x[i] : (T)0;
 }
 
+// neighbor_balance_init (tonal.py:389-414): g = T(u + s / cnt) on the mask,
+// 0 elsewhere, with s = correlate(f - u, ones(3, 3), mode="constant") and
+// cnt = correlate(ones, ones(3, 3)) summed in scipy's footprint order
+// (row-major offsets (-1,-1) .. (1,1)); an out-of-image offset adds
+// cval * weight = +0.0, which leaves every sum unchanged.  f is the f64 image.
+template <typename T>
+__global__ void k_neighbor_balance(const double* __restrict__ f, const T* __restrict__ u,
+                                   const uint8_t* __restrict__ m, T* __restrict__ g, int C,
+                                   int H, int W) {
+  const size_t n = (size_t)H * W;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * C) return;
+  const size_t p = i % n;
+  if (!m[p]) {
+    g[i] = (T)0;
+    return;
+  }
+  const int y = (int)(p / W), x = (int)(p - (size_t)y * W);
+  const double* fc = f + (i - p);
+  const T* uc = u + (i - p);
+  double s = 0.0, cnt = 0.0;
+  for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int yy = y + dy, xx = x + dx;
+      if (yy < 0 || yy >= H || xx < 0 || xx >= W) {
+        s = __dadd_rn(s, 0.0);
+        cnt = __dadd_rn(cnt, 0.0);
+        continue;
+      }
+      const size_t q = (size_t)yy * W + xx;
+      s = __dadd_rn(s, __dsub_rn(fc[q], (double)uc[q]));
+      cnt = __dadd_rn(cnt, 1.0);
+    }
+  g[i] = (T)__dadd_rn((double)u[i], __ddiv_rn(s, cnt));
+}
+
 }  // namespace
+
+template <typename T>
+int neighbor_balance(const double* f, const T* u, const uint8_t* m, T* g, int C, int H, int W,
+                     cudaStream_t s) {
+  const size_t n = (size_t)H * W * C;
+  if (!n) return 0;
+  k_neighbor_balance<T><<<cdiv(n, 256), 256, 0, s>>>(f, u, m, g, C, H, W);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
 
 // ---- cell index ----------------------------------------------------------------
 int cell_index(const int* lab, int H, int W, long m, int* perm, int* start, int* end,
@@ -351,7 +397,9 @@ int where_mask(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaSt
   template int ras_scatter<T>(T*, const T*, const int*, const int*, const int*, const int*,   \
                               const int*, const int*, const int*, int, int, int, int, int,    \
                               int, cudaStream_t);                                             \
-  template int where_mask<T>(const T*, const uint8_t*, T*, int, int, int, cudaStream_t);
+  template int where_mask<T>(const T*, const uint8_t*, T*, int, int, int, cudaStream_t);     \
+  template int neighbor_balance<T>(const double*, const T*, const uint8_t*, T*, int, int, int, \
+                                   cudaStream_t);
 INST(float)
 INST(double)
 

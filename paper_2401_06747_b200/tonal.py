@@ -603,16 +603,19 @@ def voronoi_richardson_init(f: Image, mask: Mask, cfg: InitConfig | None = None,
 def neighbor_balance_init(f: Image, u: Image, mask: Mask, solver: InpaintSolver | None = None,
                           final_tol: float = 1e-6) -> TonalState:
     """tonal.py:389-414: 3x3 (border-clipped) mean signed error added to the
-    stored values (device box filter via conv2d)."""
+    stored values, one CUDA pass (sp_neighbor_balance, scipy `correlate`
+    summation order, bit-exact)."""
     f64 = f.tensor(torch.float64)
     u_t = u.tensor()
-    diff = (f64 - u_t.to(torch.float64))[:, None]
-    kern = torch.ones((1, 1, 3, 3), dtype=torch.float64, device=f64.device)
-    s = torch.nn.functional.conv2d(diff, kern, padding=1)[:, 0]
-    cnt = torch.nn.functional.conv2d(torch.ones_like(diff[:1]), kern, padding=1)[0, 0]
-    vals = u_t.to(torch.float64) + s / cnt
+    if u_t.dtype not in (torch.float32, torch.float64):
+        u_t = u_t.to(torch.float64)
     m_t = mask.tensor()
-    g = torch.where(m_t.bool()[None], vals.to(u_t.dtype), torch.zeros_like(u_t))
+    C, H, W = u_t.shape
+    if tuple(f64.shape) != (C, H, W) or tuple(m_t.shape) != (H, W):
+        raise ValueError("image, reconstruction and mask dimensions disagree")
+    g = torch.empty_like(u_t)
+    call("sp_neighbor_balance", dcode(u_t), ptr(f64), ptr(u_t), ptr(m_t), ptr(g), C, H, W,
+         stream())
     if solver is None:
         unew = u.copy()
         return TonalState(g=Image(g), u=unew, mse=mse_t(f64, unew.tensor()))

@@ -143,3 +143,11 @@ def test_recorded_reference_runs(textured64, key):
             st = O.ras_tonal(f, mask, init=st, cfg=cfg)
         mse = st["mse"]
     assert abs(mse - rec["mse"]) <= 5e-7 * rec["mse"]
+
+
+def test_neighbor_balance_oracle_matches_reference():
+    """tonal.py:389-414 stored values vs the reference's own output
+    (tests/golden/large_f34.npz, scipy.ndimage.correlate)."""
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "large_f34.npz"))
+    g = O.neighbor_balance_values(G["t64_pgm"], G["balance_u_in"], G["aa_mask"])
+    assert np.array_equal(g, G["balance_g_nosolver"])
