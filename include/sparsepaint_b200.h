@@ -321,6 +321,20 @@ long long sp_launch_count(int reset);
 int sp_hier_bench(void* hier, int which, int reps, double* ms_h, double* bytes_h,
                   void* stream);
 
+/* ---- PNM wire formats, encoded on the device (pnm.py:40-127) ------------ */
+/* P4 body of write_mask (pnm.py:78-84): np.packbits(mask != 0, axis=1), i.e.
+ * H rows of ceil(W/8) bytes, MSB first; out holds H * ceil(W/8) bytes */
+int sp_pack_mask_bits(const uint8_t* mask, int H, int W, uint8_t* out, void* stream);
+/* inverse of the above (read_mask, pnm.py:87-95): mask u8 0/1 [H,W] */
+int sp_unpack_mask_bits(const uint8_t* bits, int H, int W, uint8_t* mask, void* stream);
+/* PGM/PPM body of values [C,H,W] (dtype code) as interleaved [H,W,C]:
+ * wide = 0: clip(rint(v), 0, 255) u8 (write_image / 8-bit write_tonal,
+ * grid.py:216-218); wide = 1: big-endian u16 clip(rint((v+256)*64), 0,
+ * 65535) (pnm.py:106-117).  mask != NULL applies where(mask, v, 0) first
+ * (write_tonal).  out holds H*W*C*(1 + wide) bytes. */
+int sp_encode_pnm(int dtype, const void* values, const uint8_t* mask, int C, int H, int W,
+                  int wide, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

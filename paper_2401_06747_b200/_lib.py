@@ -84,6 +84,10 @@ _SIGS = {
     "sp_ras_scatter": [c_int, P, P, P, P, P, P, P, P, P, c_int, c_int, c_int, c_int, c_int,
                        c_int, P],
     "sp_where_mask": [c_int, P, P, P, c_int, c_int, c_int, P],
+    "sp_neighbor_balance": [c_int, P, P, P, P, c_int, c_int, c_int, P],
+    "sp_pack_mask_bits": [P, c_int, c_int, P, P],
+    "sp_unpack_mask_bits": [P, c_int, c_int, P, P],
+    "sp_encode_pnm": [c_int, P, P, c_int, c_int, c_int, c_int, P, P],
     "sp_masked_sym_rhs_tiles": [c_int, P, P, P, c_int, c_int, c_int, c_int, P, P],
     "sp_ct_apply_tiles": [c_int, P, P, P, c_int, c_int, c_int, c_int, P, P],
     "sp_density_map": [P, c_int, c_int, c_int, c_double, P, c_int, P, P, P],

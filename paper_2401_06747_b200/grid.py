@@ -105,6 +105,11 @@ class Image:
     def data(self, value):
         self.__init__(value)
 
+    @property
+    def on_device(self) -> bool:
+        """True while the data lives only on the device (no host copy yet)."""
+        return self._host is None and self._dev is not None and self._dev.is_cuda
+
     def tensor(self, dtype=None) -> torch.Tensor:
         """Device tensor (C, H, W); uploads host data when host-sourced."""
         if self._dev is not None:
@@ -187,6 +192,11 @@ class Mask:
     @indicator.setter
     def indicator(self, value):
         self.__init__(value)
+
+    @property
+    def on_device(self) -> bool:
+        """True while the indicator lives only on the device."""
+        return self._host is None and self._dev is not None and self._dev.is_cuda
 
     def tensor(self) -> torch.Tensor:
         if self._dev is not None:
