@@ -317,7 +317,7 @@ int sp_hier_residual(void* hier, int lv, void* r_out, double* norms_out, void* s
 /* kernels launched by the library since the last reset */
 long long sp_launch_count(int reset);
 /* CUDA-event timing of a finest-level kernel (0 residual, 1 ORAS local CG,
- * 2 blend, 3 residual+restrict): mean ms and algorithmic bytes per launch */
+ * 2 blend, 3 residual+restrict, 4 prolongation+add+enforce): mean ms and algorithmic bytes per launch */
 int sp_hier_bench(void* hier, int which, int reps, double* ms_h, double* bytes_h,
                   void* stream);
 

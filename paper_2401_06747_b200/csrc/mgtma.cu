@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
   __shared__ uint64_t bars[NS];
   __shared__ double wsum[CR];
   __shared__ bool am_last;
-  __shared__ float rrow[MODE == 1 ? CR : 1][MODE == 1 ? TC + 4 : 1];
+  __shared__ __align__(16) float rrow[MODE == 1 ? 2 : 1][MODE == 1 ? CR : 1][MODE == 1 ? TC + 4 : 1];
   const int z = blockIdx.z, tile = z / C;
   if (active && !active[tile]) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
         }
       }
     }
-    if (MODE == 1) *reinterpret_cast<float4*>(&rrow[w][4 * lane]) = rr;
+    if (MODE == 1) *reinterpret_cast<float4*>(&rrow[k & 1][w][4 * lane]) = rr;
     if (MODE == 0 && NORMS && bandcol && ((k & 1) || k == nck - 1)) {
       // row-band partials for the strip-partitioned solve (strips.cu): the
       // CTA's sum over each 16-row band (2 chunks), one double per (plane,
@@ -212,27 +212,26 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
     if (threadIdx.x == 0 && k + NS < nck)
       issue_chunk(mp, sm, bars, st, x0, y0 + (k + NS) * CR, z, tile);
     if (MODE == 1) {
-      // restrict_values (numba_impl.py:266-284): warps 0..3 combine the row
-      // pairs of the chunk, 2 coarse pixels per lane, ((a + b) + c) + d
-      if (w < CR / 2) {
-        const int yf = y0 + k * CR + 2 * w;
-        if (yf < H && xq < W) {
-          const float4 a = *reinterpret_cast<const float4*>(&rrow[2 * w][4 * lane]);
-          float2 o;
-          if (yf + 1 < H) {
-            const float4 b2 = *reinterpret_cast<const float4*>(&rrow[2 * w + 1][4 * lane]);
-            o.x = (float)(((((double)a.x + (double)a.y) + (double)b2.x) + (double)b2.y) / 4.0);
-            o.y = (float)(((((double)a.z + (double)a.w) + (double)b2.z) + (double)b2.w) / 4.0);
-          } else {
-            o.x = (float)(((double)a.x + (double)a.y) / 2.0);
-            o.y = (float)(((double)a.z + (double)a.w) / 2.0);
-          }
-          const int cw = W / 2;
-          *reinterpret_cast<float2*>(rcoarse + (size_t)z * cps + (size_t)(yf >> 1) * cw +
-                                     (xq >> 1)) = o;
+      // restrict_values (numba_impl.py:266-284): all 8 warps, one coarse
+      // pixel per lane -- warp w takes coarse row w/2 of the chunk and the
+      // 32-column half w&1, ((a + b) + c) + d in double.  rrow is double
+      // buffered, so the next chunk's rows never overwrite rows still being
+      // restricted (no second barrier per chunk).
+      const int yf = y0 + k * CR + 2 * (w >> 1);
+      const int xc = (x0 >> 1) + 32 * (w & 1) + lane;
+      const int cw = W / 2;
+      if (yf < H && xc < cw) {
+        const float* ra = &rrow[k & 1][2 * (w >> 1)][2 * (32 * (w & 1) + lane)];
+        const float2 a = *reinterpret_cast<const float2*>(ra);
+        float o;
+        if (yf + 1 < H) {
+          const float2 b2 = *reinterpret_cast<const float2*>(ra + (TC + 4));
+          o = (float)(((((double)a.x + (double)a.y) + (double)b2.x) + (double)b2.y) / 4.0);
+        } else {
+          o = (float)(((double)a.x + (double)a.y) / 2.0);
         }
+        rcoarse[(size_t)z * cps + (size_t)(yf >> 1) * cw + xc] = o;
       }
-      __syncthreads();  // rrow reused by the next chunk
     }
   }
   if (MODE != 0 || !NORMS || bandcol) return;
@@ -329,8 +328,8 @@ int launch(const float* u, const float* b, const uint8_t* m, float* r, double* p
 // u = (add ? u : 0) + P e on unmasked pixels, u = b~ on masked pixels.  A
 // chunk is 8 fine rows x 128 columns: TMA brings the u rows (add only), the
 // mask rows and the 6 x 72 coarse rows / columns the bilinear stencil of
-// the chunk touches; b~ is read directly, and only for quads holding a
-// stored pixel (5% density).  The interpolation is the reference's double
+// the chunk touches; the overwrite form (FMG cascade) reads b~ directly for
+// quads holding a stored pixel, the add form never reads it (see below).  The interpolation is the reference's double
 // expression with its clamped, cell-centred indices, one rounding.
 constexpr int EW = TC / 2 + 8;     // coarse columns per chunk (4-column halo)
 constexpr int EH = CR / 2 + 2;     // coarse rows per chunk
@@ -404,9 +403,16 @@ __global__ void __launch_bounds__(CR * 32) k_prolong_tma(
       const uint32_t mw = *reinterpret_cast<const uint32_t*>(base + PM_OFF + w * TC + 4 * lane);
       const float4 uu = ADD ? *reinterpret_cast<const float4*>(base + PU_OFF + (w * TC + 4 * lane) * 4)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 bb = mw ? *reinterpret_cast<const float4*>(b + (size_t)z * plane +
-                                                               (size_t)y * W + xq)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      // masked pixels take b~.  With ADD the V-cycle invariant u == b~ on
+      // the mask holds on entry (solver.py:293-296 enforces before every
+      // smoothing sweep, and ORAS corrections vanish on masked pixels: the
+      // local residual, and hence p and v, are exactly 0 there), so the
+      // TMA-staged u already holds b~ and b~ is never read; the FMG
+      // cascade's overwrite (ADD false) reads it.
+      const float4 bb = ADD ? uu
+                            : (mw ? *reinterpret_cast<const float4*>(b + (size_t)z * plane +
+                                                                      (size_t)y * W + xq)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f));
       int ya, yb;
       double wy;
       paxis_d(y, chh, ya, yb, wy);

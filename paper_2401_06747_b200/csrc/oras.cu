@@ -38,12 +38,14 @@ __device__ unsigned long long g_oras_stats[4];
 __device__ int g_stats_on;
 
 // kernel choice for float blocks <= 32x32 (sp_oras_variant, A/B runs):
-// 0 = register-resident 4-warp job kernel, one job per CTA (k_oras_rows,
-// default), 1 = the 256-thread CTA kernel with the reference's double
-// stencil, 3 = persistent k_oras_rows_p with cp.async prefetch of the next
-// job (it removes the load stalls but issues 32% more instructions and
-// loses: 1.80 vs 1.58 ms per 4K V-cycle, profiles/oras_ab_r01j.txt)
-static int oras_kernel = 6;
+// 7 = one warp per job, lean local CG (k_oras_warp<FAST>, the default);
+// 6 = one warp per job, the reference-ordered CG (bit-identical to 0 and 4);
+// 4 = k_oras_warp with four jobs per CTA; 0 = the register-resident 4-warp
+// job kernel (k_oras_rows); 1 = the 256-thread CTA kernel with the
+// reference's double stencil.  (A persistent cp.async-prefetch variant
+// measured slower -- 1.80 vs 1.58 ms per 4K V-cycle, profiles/
+// oras_ab_r01j.txt -- and was removed.)
+static int oras_kernel = 7;
 int oras_variant(int v) {
   if (v >= 0) oras_kernel = v;
   return oras_kernel;
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
 // ---------------------------------------------------------------------------
 constexpr int WJ = 4;  // jobs (warps) per CTA
 
-template <bool UNIT_H, bool FULLH, int WJ>
+template <bool UNIT_H, bool FULLH, int WJ, bool FAST = false>
 __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
@@ -532,7 +534,9 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const bool ok = (FULLH || s < bh) && lane_ok;
-    res[s] = ok ? res[s] : 0.0f;
+    // FAST: the residual is 0 on masked pixels anyway (u = b~ there, so
+    // r = b~ - u = 0); zeroing it makes p = q exact for warp_cg32_fast
+    res[s] = (FAST ? ok && !mk[s] : ok) ? res[s] : 0.0f;
     if (!ok || mk[s]) off |= 1u << s;
   }
   // Robin-closed diagonal of the three row classes (k_oras_rows' float
@@ -551,8 +555,11 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
   const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
 
   float v[R];
-  const long it = warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh,
-                                           tau, cap, j);
+  const long it =
+      FAST ? warp_cg32_fast<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh,
+                                           tau, cap)
+           : warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh, tau,
+                                      cap, j);
   float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw) + j;
   const float* wb = weights + (size_t)bi * bh * bw + j;
   if (lane_ok) {
@@ -566,123 +573,6 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
     atomicMax(&g_oras_stats[3], (unsigned long long)it);
   }
-}
-
-// Persistent variant of k_oras_rows (sp_oras_variant 3, measured slower):
-// a resident CTA walks jobs job, job + gridDim.x, ... and prefetches the
-// NEXT job's residual block, blend weights and mask words into a second
-// shared-memory buffer with cp.async (LDGSTS) while the current job's CG
-// runs.  It hides the per-job DRAM latency (the top stall of the one-job-
-// per-CTA kernel) but the prefetch bookkeeping costs more issue slots than
-// the latency it hides in this issue-bound kernel.  Needs W % 4 == 0.
-constexpr int MWR = 9;  // mask words per block row (32 bytes + misalignment)
-
-__device__ __forceinline__ void job_origin(long job, int nb, int C, int nbx, int bh, int bw,
-                                           int H, int W, int stride, const int* ys,
-                                           const int* xs, int& bi, int& ch, int& tile, int& y0,
-                                           int& x0) {
-  bi = (int)(job % nb);
-  const long rest = job / nb;
-  ch = (int)(rest % C);
-  tile = (int)(rest / C);
-  const int kyb = bi / nbx, kxb = bi - kyb * nbx;
-  y0 = stride > 0 ? block_start(kyb, stride, H, bh) : ys[kyb];
-  x0 = stride > 0 ? block_start(kxb, stride, W, bw) : xs[kxb];
-}
-
-template <bool UNIT_H>
-__global__ void __launch_bounds__(NTJ, 7) k_oras_rows_p(
-    const float* __restrict__ r, const uint8_t* __restrict__ m,
-    const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
-    const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
-    float closure, long cap, float inv_h2, const float* __restrict__ weights,
-    float* __restrict__ corr, const int* __restrict__ active, int corr_nb, int C, long njobs) {
-  __shared__ float er_top[NWJ][32], er_bot[NWJ][32];
-  __shared__ double red_a[NWJ], red_b[NWJ];
-  __shared__ __align__(16) float sr[2][32 * 32];
-  __shared__ __align__(16) float sw[2][32 * 32];
-  __shared__ __align__(16) uint32_t smw[2][32 * MWR];
-  const int nb = corr_nb > 0 ? corr_nb : nbl;
-  const int j = threadIdx.x & 31, w = threadIdx.x >> 5, i0 = w * RW;
-  const size_t plane = (size_t)H * W;
-  auto prefetch = [&](long job, int b) {
-    int bi, ch, tile, y0, x0;
-    job_origin(job, nbl, C, nbx, bh, bw, H, W, stride, ys, xs, bi, ch, tile, y0, x0);
-    if (active && !active[tile]) return;
-    const float* rc = r + ((size_t)tile * C + ch) * plane;
-    const float* wb = weights + (size_t)bi * bh * bw;
-    if (j < bw) {
-#pragma unroll
-      for (int s = 0; s < RW; ++s) {
-        const int i = i0 + s;
-        if (i < bh) {
-          __pipeline_memcpy_async(&sr[b][i * 32 + j], rc + (size_t)(y0 + i) * W + x0 + j, 4);
-          __pipeline_memcpy_async(&sw[b][i * 32 + j], wb + i * bw + j, 4);
-        }
-      }
-    }
-    const uint8_t* mt = m + (size_t)tile * plane;
-    const int wx0 = x0 >> 2, nwr = ((x0 + bw - 1) >> 2) - wx0 + 1;
-    for (int q = threadIdx.x; q < bh * nwr; q += NTJ) {
-      const int i = q / nwr, k = q - i * nwr;
-      __pipeline_memcpy_async(&smw[b][i * MWR + k],
-                              mt + (size_t)(y0 + i) * W + (size_t)(wx0 + k) * 4, 4);
-    }
-  };
-  int buf = 0;
-  long job = blockIdx.x;
-  if (job < njobs) prefetch(job, buf);
-  __pipeline_commit();
-  for (; job < njobs; job += gridDim.x) {
-    const long nxt = job + gridDim.x;
-    if (nxt < njobs) prefetch(nxt, buf ^ 1);
-    __pipeline_commit();
-    __pipeline_wait_prior(1);  // this thread's copies of the current job landed
-    __syncthreads();           // ... and every other thread's
-    int bi, ch, tile, y0, x0;
-    job_origin(job, nbl, C, nbx, bh, bw, H, W, stride, ys, xs, bi, ch, tile, y0, x0);
-    if (!(active && !active[tile])) {
-      const unsigned char* mrow0 = reinterpret_cast<const unsigned char*>(smw[buf]) + (x0 & 3);
-      auto mbyte = [&](int i) { return mrow0[i * MWR * 4 + j]; };
-      const bool lane_ok = j < bw;
-      float res[RW];
-      uint32_t mb = 0, vb = 0;
-#pragma unroll
-      for (int s = 0; s < RW; ++s) {
-        const int i = i0 + s;
-        res[s] = 0.0f;
-        if (i < bh && lane_ok) {
-          res[s] = sr[buf][i * 32 + j];
-          if (mbyte(i)) mb |= 1u << s;
-          vb |= 1u << s;
-        }
-      }
-      const bool has_up = i0 > 0 && i0 - 1 < bh && lane_ok;
-      const bool has_dn = i0 + RW < bh && lane_ok;
-      const float fm_up = has_up && !mbyte(i0 - 1) ? 1.0f : 0.0f;
-      const float fm_dn = has_dn && !mbyte(i0 + RW) ? 1.0f : 0.0f;
-      const double tau = tau_scale * tau_src[(size_t)tile * C + ch];
-      float v[RW];
-      const long it = cg_rows<UNIT_H>(res, v, mb, vb, fm_up, fm_dn, y0, x0, bh, bw, H, W,
-                                      closure, inv_h2, tau, cap, j, w, er_top, er_bot, red_a,
-                                      red_b);
-      float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw);
-#pragma unroll
-      for (int s = 0; s < RW; ++s) {
-        const int i = i0 + s;
-        if ((vb >> s) & 1u) out[i * bw + j] = sw[buf][i * 32 + j] * v[s];
-      }
-      if (threadIdx.x == 0 && g_stats_on) {
-        atomicAdd(&g_oras_stats[0], 1ull);
-        atomicAdd(&g_oras_stats[1], (unsigned long long)it);
-        if (it == 0) atomicAdd(&g_oras_stats[2], 1ull);
-        atomicMax(&g_oras_stats[3], (unsigned long long)it);
-      }
-    }
-    __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
-    buf ^= 1;
-  }
-  __pipeline_wait_prior(0);
 }
 
 template <typename T, int PPT>
@@ -1129,7 +1019,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   const int npx = bh * bw;
   if (ps && ps != (size_t)H * W &&
       !(sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
-        (oras_kernel == 0 || oras_kernel == 2 || oras_kernel == 4 || oras_kernel == 6))) {
+        (oras_kernel == 0 || oras_kernel == 2 || oras_kernel == 4 || oras_kernel >= 6))) {
     set_error("plane-strided ORAS launches need the float 32x32 4-warp kernel");
     return -2;
   }
@@ -1140,31 +1030,20 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   }
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
-  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel == 3 && W % 4 == 0 &&
-      ((uintptr_t)m & 3) == 0 && ps == (size_t)H * W) {
-    const long njobs = (long)nby * nbx * C * ntile;
-    static int occ = 0;
-    if (!occ) {
-      SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_oras_rows_p<true>, NTJ, 0));
-      if (occ < 1) occ = 1;
-    }
-    const long g = std::min<long>(njobs, (long)num_sms() * occ);
-    auto kern = inv_h2 == 1.0 ? k_oras_rows_p<true> : k_oras_rows_p<false>;
-    kern<<<(unsigned)g, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx,
-                                     nby * nbx, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
-                                     (float)inv_h2, (const float*)weights, (float*)corr, active,
-                                     corr_nb, C, njobs);
-  } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && (oras_kernel == 4 || oras_kernel == 6)) {
+  if (sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
+      (oras_kernel == 4 || oras_kernel == 6 || oras_kernel == 7)) {
     const int nbl = nby * nbx;
     const bool unit = inv_h2 == 1.0, full = bh == 32 && bw == 32;
     // 4: four jobs per CTA; 6: one job per CTA (a finished job frees its
-    // slot at once instead of waiting for the CTA's slowest job)
-    const int wj = oras_kernel == 6 ? 1 : WJ;
+    // slot at once instead of waiting for the CTA's slowest job); 7: 6 with
+    // the lean local CG (warp_cg32_fast)
+    const int wj = oras_kernel == 4 ? WJ : 1;
     dim3 g4(cdiv(nbl, wj), C, ntile);
-#define SP_WARP(WJN)                                                                          \
-  (unit ? (full ? k_oras_warp<true, true, WJN> : k_oras_warp<true, false, WJN>)               \
-        : (full ? k_oras_warp<false, true, WJN> : k_oras_warp<false, false, WJN>))
-    auto kern = wj == 1 ? SP_WARP(1) : SP_WARP(WJ);
+#define SP_WARP(WJN, F)                                                                   \
+  (unit ? (full ? k_oras_warp<true, true, WJN, F> : k_oras_warp<true, false, WJN, F>)     \
+        : (full ? k_oras_warp<false, true, WJN, F> : k_oras_warp<false, false, WJN, F>))
+    auto kern = oras_kernel == 7 ? SP_WARP(1, true) : (wj == 1 ? SP_WARP(1, false)
+                                                               : SP_WARP(WJ, false));
 #undef SP_WARP
     kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
                                 bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,

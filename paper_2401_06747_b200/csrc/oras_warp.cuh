@@ -100,4 +100,86 @@ __device__ __forceinline__ long warp_cg32(float (&res)[32], float (&v)[32], uint
   return it;
 }
 
+// sum of a0..a3 over the warp, in every lane: ((a0 + a1) + (a2 + a3)), then
+// one xor butterfly in float.  The closing broadcast of lane 0 makes the
+// result provably warp-uniform, so the CG loop's exit tests stay uniform
+// branches (without it the compiler wraps every shuffle of the loop in
+// WARPSYNC / collective fix-up code).
+__device__ __forceinline__ float warp_sum_f(float a0, float a1, float a2, float a3) {
+  float x = (a0 + a1) + (a2 + a3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+  return __shfl_sync(0xFFFFFFFFu, x, 0);
+}
+
+// The same local CG with a leaner instruction stream (the default kernel,
+// sp_oras_variant 7).  Differences from warp_cg32, all below the float
+// rounding of the vectors themselves:
+//   - q = p: the caller zeroes the residual on `off` rows (masked or outside
+//     the block), so p, v and the residual stay exactly 0 there and only the
+//     operator row needs the select (A p = p = 0 on those rows);
+//   - dots: four interleaved float accumulators per lane (rows s mod 4),
+//     combined pairwise, one float xor butterfly, compared in double;
+//   - alpha = rs / pap and beta = rs' / rs by the fast float division (the
+//     reference rounds both to the vector dtype, numba_impl.py:234-247).
+// Stop rule, cap, breakdown test and the update order are warp_cg32's.
+template <bool UNIT_H, bool FULLH>
+__device__ __forceinline__ long warp_cg32_fast(float (&res)[32], float (&v)[32], uint32_t off,
+                                               float dtop, float dmid, float dbot, float lf,
+                                               float rt, float inv_h2, int bh, double tau,
+                                               long cap) {
+  constexpr int R = 32;
+  float p[R], ap[R];
+  float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+#pragma unroll
+  for (int s = 0; s < R; s += 4) {
+    v[s] = v[s + 1] = v[s + 2] = v[s + 3] = 0.0f;
+    p[s] = res[s];
+    p[s + 1] = res[s + 1];
+    p[s + 2] = res[s + 2];
+    p[s + 3] = res[s + 3];
+    a0 = __fmaf_rn(res[s], res[s], a0);
+    a1 = __fmaf_rn(res[s + 1], res[s + 1], a1);
+    a2 = __fmaf_rn(res[s + 2], res[s + 2], a2);
+    a3 = __fmaf_rn(res[s + 3], res[s + 3], a3);
+  }
+  float rs = warp_sum_f(a0, a1, a2, a3);
+  long it = 0;
+  while ((double)rs > tau && it < cap) {
+    float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const float ql = __shfl_up_sync(0xFFFFFFFFu, p[s], 1);
+      const float qr = __shfl_down_sync(0xFFFFFFFFu, p[s], 1);
+      const float up = s > 0 ? p[s - 1] : 0.0f;
+      const float dn = s < R - 1 ? p[s + 1] : 0.0f;
+      const float acc = __fmaf_rn(qr, rt, __fmaf_rn(ql, lf, up + dn));
+      float dg;
+      if (FULLH) dg = s == 0 ? dtop : (s == R - 1 ? dbot : dmid);
+      else dg = s == 0 ? dtop : (s == bh - 1 ? dbot : dmid);
+      const float a = __fmaf_rn(dg, p[s], UNIT_H ? -acc : -(acc * inv_h2));
+      ap[s] = ((off >> s) & 1u) ? 0.0f : a;
+      acc4[s & 3] = __fmaf_rn(p[s], ap[s], acc4[s & 3]);
+    }
+    const float pap = warp_sum_f(acc4[0], acc4[1], acc4[2], acc4[3]);
+    if (pap <= 0.0f) break;
+    const float alpha = __fdividef(rs, pap);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc4[g] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      v[s] = __fmaf_rn(alpha, p[s], v[s]);
+      res[s] = __fmaf_rn(-alpha, ap[s], res[s]);
+      acc4[s & 3] = __fmaf_rn(res[s], res[s], acc4[s & 3]);
+    }
+    const float rsn = warp_sum_f(acc4[0], acc4[1], acc4[2], acc4[3]);
+    const float beta = __fdividef(rsn, rs);
+    rs = rsn;
+#pragma unroll
+    for (int s = 0; s < R; ++s) p[s] = __fmaf_rn(beta, p[s], res[s]);
+    ++it;
+  }
+  return it;
+}
+
 }  // namespace sp

@@ -744,8 +744,8 @@ namespace sp {
 
 // ---- per-kernel timing on the finest level (bench.py roofline) ---------------
 // which: 0 = residual + norms sweep, 1 = ORAS local CG, 2 = ORAS blend,
-// 3 = fused residual + restriction.  Runs `reps` launches on the current
-// level-0 state (after a solve) between CUDA events on `s`; returns the mean
+// 3 = fused residual + restriction, 4 = prolongation + add + enforce.  Runs
+// `reps` launches on the current level-0 state (after a solve) between CUDA events on `s`; returns the mean
 // milliseconds per launch and the algorithmic bytes per launch.
 template <typename T>
 static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes) {
@@ -759,6 +759,7 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
     case 1: *bytes = (double)(es * C * nb * npx * nt * 3 + nb * npx * nt); break;  // r, w, corr + mask
     case 2: *bytes = (double)(es * C * nb * npx * nt + 2 * es * vec); break;       // corr + u rw
     case 3: *bytes = (double)(2 * es * vec + plane * nt + es * vec / 4); break;    // u, b, mask, rc
+    case 4: *bytes = (double)(2 * es * vec + plane * nt + es * vec / 4); break;    // u rw, mask, e
     default: set_error("unknown kernel id %d", which); return -2;
   }
   SP_TRY(active_host_ready(h));
@@ -780,9 +781,19 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
                                     L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
                                     s, h->ntile, h->d_active);
       }
-      default:
+      case 3:
         if (!G) { set_error("single-level hierarchy"); return -2; }
         return residual_restrict_lv<T>(h, 0, s);
+      default: {
+        // u += P e, u = b~ on the mask, into the r buffer (scratch) so the
+        // solver state is not disturbed
+        if (!G) { set_error("single-level hierarchy"); return -2; }
+        if (sizeof(T) == 4 && h->sweep == 2 && tma_prolong_ok(L.H, L.W) && aligned_level<T>(L))
+          return prolong_tma((const float*)G->u, (float*)L.r, (const float*)L.b, L.mask, h->C,
+                             G->H, G->W, L.H, L.W, 1, s, h->ntile, h->d_active);
+        return prolong_enforce<T>((const T*)G->u, (T*)L.r, (const T*)L.b, L.mask, h->C, G->H,
+                                  G->W, L.H, L.W, 1, s, h->ntile, h->d_active);
+      }
     }
   };
   // the ORAS local kernel needs current r/norms
