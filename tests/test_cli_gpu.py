@@ -110,7 +110,8 @@ def test_device_pnm_bodies_equal_host_encoders(sp, tmp_path, dtype, c, h, w):
     back = sp.read_tonal(str(tmp_path / "tonal16_d"), wide=True).data
     enc = np.where(m[None] > 0, v, 0).astype(np.float64)
     inside = (enc > -256) & (enc < 767.98)
-    assert np.all(np.abs(back - enc)[inside] <= 1 / 128 + 1e-9)
+    # half a 1/64 step, plus the float32 rounding of (v + 256) * 64
+    assert np.all(np.abs(back - enc)[inside] <= 1 / 128 + 1e-4)
 
 
 def test_synth_roundtrip_via_cli_eval(sp, tmp_path, capsys):
