@@ -44,10 +44,6 @@ if ROOT not in sys.path:
 H, W, C = 2160, 3840, 3
 METRIC = "4K RGB 5% mask: spatial+tonal opt wall time (s); solver HBM GB/s vs peak"
 WORKLOAD = "3840x2160 RGB synthetic, 5% density, dd (20 iters) + ras+vi (PipelineConfig defaults)"
-REF_SAMPLE = (128, 128, 3)
-# runtime exponent of the reference pipeline in pixel count, recorded by the
-# reference's own scaling test (pkg/test_output.txt:35, slope 0.789)
-REF_SLOPE = 0.789
 
 
 def _ncu_traffic(kernel):
@@ -163,59 +159,81 @@ def _barrier(world):
         dist.barrier()
 
 
+def _cpu_sampled(steps, warmup, threads_one=True):
+    """The oracle port timed on a bounded sample of the 4K workload's own
+    work units (oracle/sampled.py): returns (estimate dict, per-step s)."""
+    from oracle import sampled
+    smp = sampled.Sampler()
+    nthr = os.cpu_count() or 1
+    sampled.set_threads(nthr)
+    step_s = []
+    for i in range(warmup + steps):
+        dt = smp.step("init" if i % 2 == 0 else "final")
+        if i >= warmup:
+            step_s.append(dt)
+        if i == warmup - 1:
+            smp.reset()
+    est = smp.estimate()
+    est["threads"] = sampled.get_threads()
+    if threads_one:
+        smp.reset()
+        sampled.set_threads(1)
+        for which in ("init", "final"):
+            smp.step(which)
+        est["estimate_1thread_s"] = smp.estimate()["estimate_s"]
+        sampled.set_threads(nthr)
+    est["cpu_model"] = sampled.cpu_model()
+    est["cpu_count"] = os.cpu_count()
+    est["reference_note"] = smp.reference_note()
+    return est, step_s
+
+
+def _cpu_line(est, step_s):
+    return {"value": est["estimate_s"], "unit": "s", "cores": est["threads"], "kind": "port",
+            "sample": (f"oracle port (C kernels, OpenMP x{est['threads']}) timed on the 4K "
+                       f"workload's own work units -- finest V-cycles on the initial and final "
+                       f"masks, 64x64 RAS block V-cycles, JFA / Delaunay / accumulate passes; "
+                       f"{len(step_s)} step(s) of {statistics.mean(step_s):.1f} s -- weighted by "
+                       f"the unit census of the reference's measured 4K run "
+                       f"(units cover {est['covered']:.0%} of its time; "
+                       f"oracle/sampled.py)"),
+            "estimate_1thread_s": est.get("estimate_1thread_s"),
+            "cpu_model": est["cpu_model"], "cpu_count": est["cpu_count"],
+            "unit_means_s": est["unit_means_s"], "counts": est["counts"],
+            "reference_measured": est["reference_note"]}
+
+
 def run_reference(args):
-    """CPU arm: the oracle port on the host cores, bounded sample."""
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """CPU arm: the oracle port on the host cores, one bounded 4K work-unit
+    sample per step (oracle/sampled.py); value = the full-run estimate."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import oracle as O
-    O.build()
-    h, w, c = REF_SAMPLE
-    f = O.synth(h, w, c, 0)
-    O.run_pipeline(O.synth(32, 32, c, 1), iterations=2)  # warm libraries
-    times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        O.run_pipeline(f)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
-    t_sample = statistics.mean(times)
-    scale = ((H * W) / (h * w)) ** REF_SLOPE
-    value = t_sample * scale
-    cores = os.cpu_count()
+    est, step_s = _cpu_sampled(args.steps, args.warmup)
+    value = est["estimate_s"]
+    cpu = _cpu_line(est, step_s)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample": f"{h}x{w}x{c}",
-                   "extrapolation": f"(pixels ratio)^{REF_SLOPE} = x{scale:.1f}"},
-        "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": f"oracle run_pipeline on {h}x{w}x{c} synth "
-                                   f"({t_sample:.2f} s/step, OpenMP over {cores} threads), "
-                                   f"x{scale:.1f} = (pixel ratio)^{REF_SLOPE} to 3840x2160"},
+        "ms_per_step": statistics.mean(step_s) * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config(args, args.gpus, False),
+        "sample": ("each step = one bounded sample of the 4K workload (ms_per_step is the "
+                   "sample's time); value = the full-run estimate from the sampled unit "
+                   "costs x the reference's unit census (cpu_baseline.sample)"),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def _cpu_baseline_sample():
-    from oracle import oracle as O
-    O.build()
-    h, w, c = REF_SAMPLE
-    f = O.synth(h, w, c, 0)
-    O.run_pipeline(O.synth(32, 32, c, 1), iterations=2)
-    t0 = time.perf_counter()
-    O.run_pipeline(f)
-    dt = time.perf_counter() - t0
-    scale = ((H * W) / (h * w)) ** REF_SLOPE
-    return {"value": dt * scale, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle run_pipeline on {h}x{w}x{c} synth ({dt:.2f} s), "
-                      f"extrapolated x{scale:.1f} = (pixel ratio)^{REF_SLOPE} (reference "
-                      f"runtime slope, test_output.txt:35) to 3840x2160"}
+def _config(args, world, strips_mode):
+    return {"workload": WORKLOAD, "H": H, "W": W, "C": C, "density": 0.05,
+            "parallelism": (f"row strips x{world} (one image; solves on strips, "
+                            "geometry replicated, RAS blocks sharded)"
+                            if strips_mode else f"replicas x{world} (one image per GPU)"),
+            "l2": "working set (>1 GB per step) exceeds the 126 MB L2"}
 
 
 S5 = (4320, 7680, 3)  # BASELINE.json configs[4]: 8K RGB, row strips over the ranks
@@ -302,6 +320,8 @@ def run_ours(args):
     _barrier(world)
     torch.cuda.synchronize()
     lib.sp_launch_count(1)
+    lib.sp_work_count(0, 1)
+    lib.sp_work_count(1, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         e0.record(stream)
@@ -310,6 +330,8 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
     launches = lib.sp_launch_count(0) // max(1, args.steps)
+    work_img = lib.sp_work_count(0, 0) / max(1, args.steps)
+    work_blk = lib.sp_work_count(1, 0) / max(1, args.steps)
     _barrier(world)
     ms = e0.elapsed_time(e1) / args.steps
     ms = _max_over_ranks(ms, world)
@@ -345,8 +367,9 @@ def run_ours(args):
     hier.solve_sym(bsym, tol=1e-4, cascade=True)
     import ctypes
     names = {0: "k_resid_tma (sym_residual sweep)", 1: "k_oras_warp (ORAS local CG)",
-             2: "k_oras_blend", 3: "k_resid_tma<1> (residual + restriction)"}
-    for which in (0, 1, 2, 3):
+             2: "k_oras_blend", 3: "k_resid_tma<1> (residual + restriction)",
+             4: "k_prolong_tma (prolongation + add + enforce)"}
+    for which in (0, 1, 2, 3, 4):
         t_ms, nbytes = ctypes.c_double(), ctypes.c_double()
         _lib.call("sp_hier_bench", hier._h, which, 20, ctypes.byref(t_ms), ctypes.byref(nbytes),
                   _lib.stream())
@@ -371,11 +394,39 @@ def run_ours(args):
                         "traffic": trs["bytes"] if trs else None,
                         "traffic_source": trs["source"] if trs else None}
 
+    # solver level: a warm finest V-cycle of the same hierarchy against the
+    # SURVEY.md 8(d) algorithmic V-cycle traffic (68 B per finest px.ch:
+    # (4/3) x (two fused smoothing sweeps + residual + restriction +
+    # prolongation))
+    u_w, _ = hier.solve_sym(bsym, tol=1e-4, cascade=True)
+    nvc = 20
+    hier.solve_sym(bsym, init=u_w, tol=None, cycles=2)
+    torch.cuda.synchronize()
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record(stream)
+    hier.solve_sym(bsym, init=u_w, tol=None, cycles=nvc)
+    v1.record(stream)
+    torch.cuda.synchronize()
+    vc_ms = v0.elapsed_time(v1) / nvc
+    vc_bytes = 68.0 * H * W * C
+    solver = {"vcycle_ms": vc_ms, "alg_bytes": vc_bytes,
+              "gbs": vc_bytes / (vc_ms * 1e-3) / 1e9,
+              "frac_measured_peak": vc_bytes / (vc_ms * 1e-3) / 1e9 / peak,
+              "frac_8tbs": vc_bytes / (vc_ms * 1e-3) / 1e9 / 8000.0,
+              "note": "warm 4K RGB V-cycle (solver.py:283-300) incl. the solve's copies; "
+                      "bytes = SURVEY.md 8(d) 68 B per finest px.ch"}
+    pipe_work = {"image_px_vcycles": work_img, "block_px_vcycles": work_blk,
+                 "mpix_iter_per_s": work_img / (ms * 1e-3) / 1e6,
+                 "mpix_iter_per_s_incl_blocks": (work_img + work_blk) / (ms * 1e-3) / 1e6,
+                 "note": "finest-level pixels x V-cycles per step (image solves; RAS 64x64 "
+                         "block solves separately) / device step time"}
+
     strips = None if args.no_strips else run_strips(world, rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = _cpu_baseline_sample()
+        est, step_s = _cpu_sampled(steps=2, warmup=0, threads_one=False)
+        cpu = _cpu_line(est, step_s)
 
     # Mpixel-iterations/s: pixels x finest V-cycles of the step (dd + tonal)
     if rank == 0:
@@ -384,15 +435,11 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "strong" if strips_mode else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "H": H, "W": W, "C": C, "density": 0.05,
-                       "parallelism": (f"row strips x{world} (one image; solves on strips, "
-                                       "geometry replicated, RAS blocks sharded)"
-                                       if strips_mode else
-                                       f"replicas x{world} (one image per GPU)"),
-                       "l2": "working set (>1 GB per step) exceeds the 126 MB L2",
-                       "final_mse": st.mse, "dd_mse": hist[-1][2], "mask_count": mask.count,
+            "config": _config(args, world, strips_mode),
+            "result": {"final_mse": st.mse, "dd_mse": hist[-1][2], "mask_count": mask.count,
                        "images_per_s": (1 if strips_mode else world) / (ms / 1e3)},
             "roofline": roof, "stencil_roofline": stencil_roofline, "kernels": kern,
+            "solver": solver, "throughput": pipe_work,
             "strips": strips,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,

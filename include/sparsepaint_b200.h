@@ -200,6 +200,11 @@ int sp_geo_voronoi(void* geo, const uint8_t* mask, double start_hint, long* m,
 int sp_geo_delaunay(void* geo, long* ntris, void* stream); /* syncs */
 /* err: device double (H, W); voronoi != 0 buckets by cell instead of triangle */
 int sp_geo_accumulate(void* geo, const double* err, int voronoi, void* stream);
+/* implementation of sp_geo_accumulate (partition "delaunay"): 1 = tile-binned
+ * rasteriser with shared-memory minima + per-triangle bounding-box walk
+ * (default), 0 = global atomicMin rasteriser + pixel radix sort; both are
+ * bit-identical to numba_impl.py:442-498.  v < 0 only reads the setting. */
+int sp_geo_accumulate_mode(int v);
 /* marks the argmax pixels of the `want` best eligible buckets in mask */
 int sp_geo_select(void* geo, uint8_t* mask, long nbuckets, long want, long* picked,
                   void* stream);
@@ -316,6 +321,10 @@ int sp_march_variant(int v);
 int sp_hier_residual(void* hier, int lv, void* r_out, double* norms_out, void* stream);
 /* kernels launched by the library since the last reset */
 long long sp_launch_count(int reset);
+/* finest-level pixel x V-cycle work of the solves since the last reset
+ * (Mpixel-iterations of the metric): kind 0 = image-level solves, kind 1 =
+ * batched block-local (RAS) solves */
+long long sp_work_count(int kind, int reset);
 /* CUDA-event timing of a finest-level kernel (0 residual, 1 ORAS local CG,
  * 2 blend, 3 residual+restrict, 4 prolongation+add+enforce): mean ms and algorithmic bytes per launch */
 int sp_hier_bench(void* hier, int which, int reps, double* ms_h, double* bytes_h,

@@ -21,6 +21,7 @@
  * reduction runs in the reference's sequential order.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -433,3 +434,7 @@ void ora_reduce_cells(const int32_t *assign, const double *err, long ntris,
       if (e > amax_val[t]) { amax_val[t] = e; amax_idx[t] = (int64_t)y * W + x; }
     }
 }
+
+/* thread control for the CPU baseline timings (bench.py reference arm) */
+void ora_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }
+int ora_get_threads(void) { return omp_get_max_threads(); }

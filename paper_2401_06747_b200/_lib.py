@@ -68,6 +68,7 @@ _SIGS = {
     "sp_geo_voronoi": [P, P, c_double, P, P, P, P],
     "sp_geo_delaunay": [P, P, P],
     "sp_geo_accumulate": [P, P, c_int, P],
+    "sp_geo_accumulate_mode": [c_int],
     "sp_geo_select": [P, P, c_long, c_long, P, P],
     "sp_geo_fill_highest_error": [P, P, P, c_long, P],
     "sp_geo_load": [P, P, P, P, c_long, P],
@@ -126,6 +127,8 @@ def load(require_cuda: bool = True):
             fn.restype = c_int
         lib.sp_launch_count.restype = ctypes.c_longlong
         lib.sp_launch_count.argtypes = [c_int]
+        lib.sp_work_count.restype = ctypes.c_longlong
+        lib.sp_work_count.argtypes = [c_int, c_int]
         lib.sp_last_error.restype = ctypes.c_char_p
         lib.sp_last_error.argtypes = []
         _lib = lib
@@ -136,7 +139,7 @@ def load(require_cuda: bool = True):
 
 
 def exported_symbols():
-    return list(_SIGS) + ["sp_last_error", "sp_launch_count"]
+    return list(_SIGS) + ["sp_last_error", "sp_launch_count", "sp_work_count"]
 
 
 def call(name, *args):

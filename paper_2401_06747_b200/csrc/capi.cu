@@ -404,6 +404,10 @@ int sp_geo_delaunay(void* g, long* ntris, void* s) {
   return geo_delaunay((Geo*)g, ntris, STREAM(s));
 }
 
+// accumulate implementation (A/B and tests): 1 = tile-binned rasteriser +
+// bbox-order reduction (default), 0 = global atomics + pixel sort; v < 0 reads
+int sp_geo_accumulate_mode(int v) { return sp::geo_accumulate_mode(v); }
+
 int sp_geo_accumulate(void* g, const double* err, int voronoi, void* s) {
   return geo_accumulate((Geo*)g, err, voronoi, STREAM(s));
 }
@@ -577,6 +581,11 @@ int sp_strip_levels(void* g, int* nlev, int* dims, int cap) {
 namespace sp {
 static std::atomic<long long> g_launches{0};
 void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// finest-level pixel x V-cycle work of every solve (Mpixel-iterations)
+static std::atomic<long long> g_work[2]{{0}, {0}};
+void count_work(int kind, long long px_cycles) {
+  g_work[kind & 1].fetch_add(px_cycles, std::memory_order_relaxed);
+}
 int hier_bench(Hier* h, int which, int reps, cudaStream_t s, double* ms, double* bytes);
 int hier_residual_out(Hier* h, int lv, void* r_out, double* norms_out, cudaStream_t s);
 }  // namespace sp
@@ -586,6 +595,15 @@ extern "C" {
 long long sp_launch_count(int reset) {
   long long v = sp::g_launches.load();
   if (reset) sp::g_launches.store(0);
+  return v;
+}
+
+// finest-level pixel-V-cycles of the solves since the last reset: kind 0 =
+// image-level solves (one hierarchy per image / strip group), kind 1 =
+// batched block-local solves (RAS 64x64 products)
+long long sp_work_count(int kind, int reset) {
+  long long v = sp::g_work[kind & 1].load();
+  if (reset) sp::g_work[kind & 1].store(0);
   return v;
 }
 

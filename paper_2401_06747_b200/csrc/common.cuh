@@ -29,6 +29,7 @@ const char* last_error();
 // kernels launched by this library (direct launches; graph replays add their
 // node count) -- reported by bench.py as gpu_launches
 void count_launches(long long n);
+void count_work(int kind, long long px_cycles);
 
 #define SP_CHECK_LAUNCH()                                                      \
   do {                                                                         \

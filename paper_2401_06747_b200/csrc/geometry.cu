@@ -451,6 +451,388 @@ __global__ void k_reduce_segments(const int* __restrict__ start, const int* __re
   if (amax_val) amax_val[t] = best;
 }
 
+
+// ---- tile-binned rasterisation + bbox-order reduction (B2 path) ----------
+// The same three results as assign_triangles -> fallback_assign ->
+// reduce_cells (numba_impl.py:442-498), without a global atomic per covered
+// pixel and without sorting the 8.3 M pixels by triangle:
+//  1. bin: every triangle is listed in the 64 x 32 screen tiles its clamped
+//     bounding box overlaps (count, scan, scatter; order inside a tile's
+//     list is irrelevant because the winner is the minimum index);
+//  2. raster: one CTA per tile takes the minimum containing triangle per
+//     pixel in shared memory (inclusive edge test, exact 32-bit integer
+//     edge functions: |coordinates| < 2^15), then the fallback for
+//     uncovered pixels (seed's lowest incident triangle, else 0).  Fallback
+//     pixels are stored with the sign bit set and listed as (t, pixel) keys;
+//  3. reduce: one thread per triangle walks its bounding box in row-major
+//     order and takes the pixels rasterised to it, merged in pixel order
+//     with its (sorted) fallback pixels -- exactly the row-major sequence
+//     reduce_cells visits, so the double sums and the first strict maxima
+//     are bit-identical.
+constexpr int RTW = 64, RTH = 32, RTN = RTW * RTH;
+
+__device__ __forceinline__ bool tri_box(const int* __restrict__ tris, long t,
+                                        const int* __restrict__ vy, const int* __restrict__ vx,
+                                        int H, int W, int4& v, int2& c, int4& box) {
+  const int a = tris[3 * t], b = tris[3 * t + 1], cc = tris[3 * t + 2];
+  v = make_int4(vy[a], vx[a], vy[b], vx[b]);
+  c = make_int2(vy[cc], vx[cc]);
+  box.x = max(0, min(v.x, min(v.z, c.x)));          // ylo
+  box.z = min(H - 1, max(v.x, max(v.z, c.x)));      // yhi
+  box.y = max(0, min(v.y, min(v.w, c.y)));          // xlo
+  box.w = min(W - 1, max(v.y, max(v.w, c.y)));      // xhi
+  return box.x <= box.z && box.y <= box.w;
+}
+
+__global__ void k_bin_count(const int* __restrict__ tris, long T, const int* __restrict__ vy,
+                            const int* __restrict__ vx, int H, int W, int ntx,
+                            int4* __restrict__ tv, int2* __restrict__ tc,
+                            int4* __restrict__ tbox, unsigned* __restrict__ cnt) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int4 v, box;
+  int2 c;
+  const bool ok = tri_box(tris, t, vy, vx, H, W, v, c, box);
+  tv[t] = v;
+  tc[t] = c;
+  if (!ok) box = make_int4(1, 1, 0, 0);
+  tbox[t] = box;
+  if (!ok) return;
+  for (int ty = box.x / RTH; ty <= box.z / RTH; ++ty)
+    for (int tx = box.y / RTW; tx <= box.w / RTW; ++tx) atomicAdd(&cnt[ty * ntx + tx], 1u);
+}
+
+__global__ void k_bin_scatter(const int4* __restrict__ tbox, long T, int ntx,
+                              const unsigned* __restrict__ off, unsigned* __restrict__ fill,
+                              int* __restrict__ list) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int4 box = tbox[t];
+  if (box.x > box.z) return;
+  for (int ty = box.x / RTH; ty <= box.z / RTH; ++ty)
+    for (int tx = box.y / RTW; tx <= box.w / RTW; ++tx) {
+      const int tile = ty * ntx + tx;
+      list[off[tile] + atomicAdd(&fill[tile], 1u)] = (int)t;
+    }
+}
+
+// The pixels of row y inside triangle (v, c) under the reference's
+// inclusive test (numba_impl.py:456-462) form one run [x0, x1] (empty when
+// x0 > x1): each edge function is affine in x, e_i = K_i - B_i x, and with
+// D = e0 + e1 + e2 (twice the signed area, constant) the test is "all
+// e_i >= 0" for D >= 0 (for D == 0 that is "all e_i == 0", the same set as
+// "all <= 0") and "all e_i <= 0" for D < 0.  Each half-line bound is an
+// exact integer floor / ceil, so the run equals the per-pixel test.
+__device__ __forceinline__ int fdiv_floor(int a, int b) {  // b > 0
+  return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+// |K_i| <= 2 (H - 1)(W - 1) < 2^31 for H, W < 32768 (the caller's bound)
+__device__ __forceinline__ void tri_span(int y, const int4& v, const int2& c, int lo, int hi,
+                                         int& x0, int& x1) {
+  const int ay = v.x, ax = v.y, by = v.z, bx = v.w, cy = c.x, cx = c.y;
+  int B[3] = {by - ay, cy - by, ay - cy};
+  int K[3] = {(bx - ax) * (y - ay) + (by - ay) * ax, (cx - bx) * (y - by) + (cy - by) * bx,
+              (ax - cx) * (y - cy) + (ay - cy) * cx};
+  // D = e0 + e1 + e2 = K0 + K1 + K2 (the B_i sum to 0): twice the signed area
+  const long long D = (long long)K[0] + K[1] + K[2];
+  int l = lo, h = hi;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int k = K[i], b = B[i];
+    if (D < 0) { k = -k; b = -b; }
+    // k - b x >= 0
+    if (b == 0) {
+      if (k < 0) { l = 1; h = 0; }
+    } else if (b > 0) {
+      h = min(h, fdiv_floor(k, b));
+    } else {
+      l = max(l, -fdiv_floor(k, -b));  // ceil(k / b) for b < 0
+    }
+  }
+  x0 = max(l, lo);
+  x1 = min(h, hi);
+}
+
+__global__ void __launch_bounds__(256) k_raster_tiles(
+    const unsigned* __restrict__ off, const unsigned* __restrict__ cnt,
+    const int* __restrict__ list, const int4* __restrict__ tv, const int2* __restrict__ tc,
+    const int4* __restrict__ tbox, const int* __restrict__ lab, const int* __restrict__ smt,
+    int H, int W, int ntx, int* __restrict__ assign, unsigned long long* __restrict__ fb,
+    unsigned long long* __restrict__ nfb) {
+  __shared__ int best[RTN];
+  __shared__ unsigned wcount[8];
+  __shared__ unsigned long long cbase;
+  const int tile = blockIdx.x, ty0 = (tile / ntx) * RTH, tx0 = (tile % ntx) * RTW;
+  for (int i = threadIdx.x; i < RTN; i += 256) best[i] = INT_MAX;
+  __syncthreads();
+  // 4 lanes per triangle, 8 triangles per warp in flight.  Rows of the
+  // clipped box: wide rows take the exact run (tri_span, three integer
+  // divisions per row), narrow rows test their few pixels directly (the
+  // reference's inclusive edge functions, exact in 32 bits)
+  const int grp = threadIdx.x >> 2, sub = threadIdx.x & 3;
+  const unsigned n = cnt[tile], o = off[tile];
+  // few (large) triangles: (triangle, row) items so all 64 groups work
+  const bool by_row = n < 64;
+  const unsigned nitems = by_row ? n * RTH : n;
+  for (unsigned item = grp; item < nitems; item += 64) {
+    const unsigned i = by_row ? item / RTH : item;
+    const int t = list[o + i];
+    const int4 v = tv[t];
+    const int2 c = tc[t];
+    const int4 box = tbox[t];
+    int ylo = max(box.x, ty0), yhi = min(box.z, ty0 + RTH - 1);
+    if (by_row) {
+      const int yr = ty0 + (int)(item % RTH);
+      if (yr < ylo || yr > yhi) continue;
+      ylo = yhi = yr;
+    }
+    const int xlo = max(box.y, tx0), xhi = min(box.w, tx0 + RTW - 1);
+    const int ay = v.x, ax = v.y, by = v.z, bx = v.w, cy = c.x, cx = c.y;
+    const bool wide = xhi - xlo >= 24;
+    for (int y = ylo; y <= yhi; ++y) {
+      int* row = best + (y - ty0) * RTW - tx0;
+      if (wide) {
+        int x0, x1;
+        tri_span(y, v, c, xlo, xhi, x0, x1);
+        for (int x = x0 + sub; x <= x1; x += 4) atomicMin(&row[x], t);
+      } else {
+        const int f0 = (bx - ax) * (y - ay), f1 = (cx - bx) * (y - by), f2 = (ax - cx) * (y - cy);
+        for (int x = xlo + sub; x <= xhi; x += 4) {
+          const int e0 = f0 - (by - ay) * (x - ax);
+          const int e1 = f1 - (cy - by) * (x - bx);
+          const int e2 = f2 - (ay - cy) * (x - cx);
+          if ((e0 >= 0 && e1 >= 0 && e2 >= 0) || (e0 <= 0 && e1 <= 0 && e2 <= 0))
+            atomicMin(&row[x], t);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i0 = 0; i0 < RTN; i0 += 256) {
+    const int i = i0 + threadIdx.x;
+    const int y = ty0 + i / RTW, x = tx0 + (i % RTW);
+    bool isfb = false;
+    int t = 0;
+    size_t p = 0;
+    if (y < H && x < W) {
+      p = (size_t)y * W + x;
+      t = best[i];
+      if (t == INT_MAX) {
+        t = smt[lab[p]];
+        if (t < 0 || t == INT_MAX) t = 0;
+        isfb = true;
+        assign[p] = (int)((unsigned)t | 0x80000000u);
+      } else {
+        assign[p] = t;
+      }
+    }
+    // CTA-aggregated append of the fallback pixels
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, isfb);
+    if (lane == 0) wcount[w] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned acc = 0;
+      for (int k = 0; k < 8; ++k) {
+        const unsigned c2 = wcount[k];
+        wcount[k] = acc;
+        acc += c2;
+      }
+      cbase = acc ? atomicAdd(nfb, (unsigned long long)acc) : 0ull;
+    }
+    __syncthreads();
+    if (isfb)
+      fb[cbase + wcount[w] + __popc(bal & ((1u << lane) - 1u))] =
+          ((unsigned long long)(unsigned)t << 32) | (unsigned long long)p;
+    __syncthreads();
+  }
+}
+
+__global__ void k_fb_bounds(const unsigned long long* __restrict__ keys, long n,
+                            int* __restrict__ start, int* __restrict__ end) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned t = (unsigned)(keys[i] >> 32);
+  if (i == 0 || (unsigned)(keys[i - 1] >> 32) != t) start[t] = (int)i;
+  if (i == n - 1 || (unsigned)(keys[i + 1] >> 32) != t) end[t] = (int)i + 1;
+}
+
+// one thread per triangle (dense triangulations: boxes of a few dozen
+// pixels): the box in row-major order, eight pixels per step with their
+// assign / err loads issued together, the triangle's fallback pixels merged
+// in pixel order
+__global__ void __launch_bounds__(128) k_reduce_tris_small(
+    const int4* __restrict__ tbox, long T, const int* __restrict__ assign,
+    const double* __restrict__ err, int W, const unsigned long long* __restrict__ fb,
+    const int* __restrict__ fs, const int* __restrict__ fe, double* __restrict__ sums,
+    long long* __restrict__ amax_idx, double* __restrict__ amax_val) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int4 box = tbox[t];
+  int fi = fs[t];
+  const int fend = fe[t];
+  long long nfp = fi < fend ? (long long)(fb[fi] & 0xFFFFFFFFull) : LLONG_MAX;
+  double s = 0.0, best = -1.0;
+  long long bi = -1;
+  for (int y = box.x; y <= box.z; ++y) {
+    const long long row = (long long)y * W;
+    for (int x0 = box.y; x0 <= box.w; x0 += 8) {
+      int a[8];
+      double e[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = x0 + k <= box.w ? assign[row + x0 + k] : -1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = a[k] == (int)t ? err[row + x0 + k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long p = row + x0 + k;
+        while (nfp < p) {
+          const double v = err[nfp];
+          s += v;
+          if (v > best) { best = v; bi = nfp; }
+          ++fi;
+          nfp = fi < fend ? (long long)(fb[fi] & 0xFFFFFFFFull) : LLONG_MAX;
+        }
+        if (a[k] == (int)t) {
+          s += e[k];
+          if (e[k] > best) { best = e[k]; bi = p; }
+        }
+      }
+    }
+  }
+  while (nfp != LLONG_MAX) {
+    const double v = err[nfp];
+    s += v;
+    if (v > best) { best = v; bi = nfp; }
+    ++fi;
+    nfp = fi < fend ? (long long)(fb[fi] & 0xFFFFFFFFull) : LLONG_MAX;
+  }
+  sums[t] = s;
+  amax_idx[t] = bi;
+  amax_val[t] = best;
+}
+
+// one warp per triangle: the run of each row of the triangle (tri_span) in
+// 32-pixel chunks -- lanes load assign / err coalesced, then lane 0 adds
+// the chunk's pixels of this triangle in pixel order from shared memory.
+// The triangle's fallback pixels (outside every triangle, hence never inside
+// one of its runs) are merged in pixel order between runs.
+__global__ void __launch_bounds__(256) k_reduce_tris(
+    const int4* __restrict__ tv, const int2* __restrict__ tc, const int4* __restrict__ tbox,
+    long T, const int* __restrict__ assign, const double* __restrict__ err, int W,
+    const unsigned long long* __restrict__ fb, const int* __restrict__ fs,
+    const int* __restrict__ fe, double* __restrict__ sums, long long* __restrict__ amax_idx,
+    double* __restrict__ amax_val, unsigned* __restrict__ next) {
+  constexpr int RB = 4;  // rows per batch
+  __shared__ double vals[8][RB * 32];
+  __shared__ double fv[8][32];
+  __shared__ long long qv[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // persistent warps take triangles from a work counter: a few large
+  // triangles must not hold a whole wave of CTAs
+  while (true) {
+    unsigned tt = 0;
+    if (lane == 0) tt = atomicAdd(next, 1u);
+    const long t = (long)__shfl_sync(0xFFFFFFFFu, tt, 0);
+    if (t >= T) break;
+    const int4 box = tbox[t];
+    const int4 v = tv[t];
+    const int2 c = tc[t];
+    int fi = fs[t];  // warp-uniform
+    const int fend = fe[t];
+    double s = 0.0, best = -1.0;  // meaningful in lane 0
+    long long bi = -1;
+    // all lanes: consume the fallback pixels below `lim`, 32 per step (the
+    // list is sorted, so the taken ones are a prefix), added by lane 0
+    auto drain = [&](long long lim) {
+      while (fi < fend) {
+        const int j = fi + lane;
+        const long long q = j < fend ? (long long)(fb[j] & 0xFFFFFFFFull) : LLONG_MAX;
+        const bool take = q < lim;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, take);
+        if (!bal) break;
+        fv[w][lane] = take ? err[q] : 0.0;
+        qv[w][lane] = q;
+        __syncwarp();
+        if (lane == 0) {
+          for (unsigned b = bal; b; b &= b - 1) {
+            const int k = __ffs(b) - 1;
+            const double ev = fv[w][k];
+            s += ev;
+            if (ev > best) { best = ev; bi = qv[w][k]; }
+          }
+        }
+        __syncwarp();
+        const int nt = __popc(bal);
+        fi += nt;
+        if (nt < 32) break;
+      }
+    };
+    // add the chunk of `row` starting at column xc (hits in `bal`, values
+    // staged in vals[w][slot]) in pixel order, after the earlier fallbacks
+    auto take = [&](long long row, int xc, unsigned bal, int slot) {
+      drain(row + xc);
+      if (lane == 0) {
+        for (unsigned b = bal; b; b &= b - 1) {
+          const int k = __ffs(b) - 1;
+          const double ev = vals[w][slot * 32 + k];
+          s += ev;
+          if (ev > best) { best = ev; bi = row + xc + k; }
+        }
+      }
+      __syncwarp();
+    };
+    for (int yb = box.x; yb <= box.z; yb += RB) {
+      int x0[RB], x1[RB];
+      bool narrow = true;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        x0[r] = 1;
+        x1[r] = 0;
+        if (yb + r <= box.z) tri_span(yb + r, v, c, box.y, box.w, x0[r], x1[r]);
+        narrow = narrow && x1[r] - x0[r] < 32;
+      }
+      if (narrow) {
+        // RB rows of at most one chunk each: all loads in flight together
+        bool hit[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int x = x0[r] + lane;
+          hit[r] = x <= x1[r] && assign[(long long)(yb + r) * W + x] == (int)t;
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          vals[w][r * 32 + lane] = hit[r] ? err[(long long)(yb + r) * W + x0[r] + lane] : 0.0;
+        unsigned bal[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) bal[r] = __ballot_sync(0xFFFFFFFFu, hit[r]);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (bal[r]) take((long long)(yb + r) * W, x0[r], bal[r], r);
+        continue;
+      }
+      for (int r = 0; r < RB && yb + r <= box.z; ++r) {
+        const long long row = (long long)(yb + r) * W;
+        for (int xc = x0[r]; xc <= x1[r]; xc += 32) {
+          const int x = xc + lane;
+          const bool h = x <= x1[r] && assign[row + x] == (int)t;
+          vals[w][lane] = h ? err[row + x] : 0.0;
+          const unsigned b = __ballot_sync(0xFFFFFFFFu, h);
+          __syncwarp();
+          if (b) take(row, xc, b, 0);
+        }
+      }
+    }
+    drain(LLONG_MAX);
+    if (lane == 0) {
+      sums[t] = s;
+      amax_idx[t] = bi;
+      amax_val[t] = best;
+    }
+  }
+}
+
 __global__ void k_fs_dither(const double* __restrict__ dens, double* __restrict__ buf,
                             uint8_t* __restrict__ out, int H, int W) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -823,6 +1205,96 @@ int geo_delaunay(Geo* g, long* T_out, cudaStream_t s) {
   return 0;
 }
 
+// B2 accumulate (geometry.py:197-223) through the tile-binned rasteriser and
+// the bbox-order reduction (see k_raster_tiles): bit-identical to the
+// assign_tris / fallback / reduce_cells sequence, which stays the kernel-table
+// (B1) path and the fallback for images of 2^15 pixels or more per side or
+// pixel counts that do not fit the 32-bit fallback keys.
+static int accumulate_tiled(Geo* g, const double* err, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  const long T = g->T;
+  const size_t n = (size_t)H * W;
+  const int ntx = cdiv(W, RTW), nty = cdiv(H, RTH), ntile = ntx * nty;
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const unsigned*)nullptr,
+                                (unsigned*)nullptr, ntile, s);
+  Scratch scr(s);
+  const size_t tb = sizeof(int4) * 2 * (size_t)T + sizeof(int2) * (size_t)T;
+  const size_t ub = sizeof(unsigned) * 3 * (size_t)ntile + 64;
+  SP_TRY(scr.alloc(tb + ub + scan_bytes + 256));
+  int4* tv = (int4*)scr.p;
+  int4* tbox = tv + T;
+  int2* tc = (int2*)(tbox + T);
+  unsigned* cnt = (unsigned*)(tc + T);
+  unsigned* off = cnt + ntile;
+  unsigned* fill = off + ntile;
+  void* scan_tmp = (void*)(((uintptr_t)(fill + ntile) + 255) & ~(uintptr_t)255);
+  SP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * ntile, s));
+  SP_CUDA(cudaMemsetAsync(fill, 0, sizeof(unsigned) * ntile, s));
+  k_bin_count<<<cdiv(T, 256), 256, 0, s>>>(g->tris, T, g->sy, g->sx, H, W, ntx, tv, tc, tbox,
+                                           cnt);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, off, ntile, s));
+  unsigned* hs = (unsigned*)g->h_small;
+  SP_CUDA(cudaMemcpyAsync(hs, off + ntile - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(hs + 1, cnt + ntile - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const size_t nlist = (size_t)hs[0] + hs[1];
+  Scratch lst(s);
+  SP_TRY(lst.alloc(sizeof(int) * (nlist + 1)));
+  k_bin_scatter<<<cdiv(T, 256), 256, 0, s>>>(tbox, T, ntx, off, fill, (int*)lst.p);
+  SP_CHECK_LAUNCH();
+  SP_TRY(seed_min_tri<int>(g->tris, T, g->smt, g->m, s));
+  unsigned long long* fbk = (unsigned long long*)g->keys;  // n <= key_cap scratch keys
+  SP_CUDA(cudaMemsetAsync(g->nkeys + 2, 0, sizeof(unsigned long long), s));
+  k_raster_tiles<<<ntile, 256, 0, s>>>(off, cnt, (const int*)lst.p, tv, tc, tbox, g->lab_a,
+                                       g->smt, H, W, ntx, g->assign, fbk, g->nkeys + 2);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys + 2, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const long nfb = (long)((unsigned long long*)g->h_small)[0];
+  // fallback pixels sorted by (triangle, pixel); per-triangle ranges
+  Scratch fbs(s);
+  size_t sort_bytes = 0;
+  if (nfb > 0)
+    cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                   (unsigned long long*)nullptr, (int)nfb, 0,
+                                   32 + bits_for(T), s);
+  SP_TRY(fbs.alloc(sizeof(unsigned long long) * (nfb + 1) + sizeof(int) * 2 * (size_t)T +
+                   sort_bytes + 512));
+  unsigned long long* fsorted = (unsigned long long*)fbs.p;
+  int* fs = (int*)(fsorted + nfb + 1);
+  int* fe = fs + T;
+  void* sort_tmp = (void*)(((uintptr_t)(fe + T) + 255) & ~(uintptr_t)255);
+  SP_CUDA(cudaMemsetAsync(fs, 0, sizeof(int) * 2 * (size_t)T, s));
+  if (nfb > 0) {
+    SP_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp, sort_bytes, fbk, fsorted, (int)nfb, 0,
+                                           32 + bits_for(T), s));
+    k_fb_bounds<<<cdiv(nfb, 256), 256, 0, s>>>(fsorted, nfb, fs, fe);
+    SP_CHECK_LAUNCH();
+  }
+  if ((double)T * 128.0 >= (double)n) {
+    // dense: boxes of a few dozen pixels, one thread per triangle
+    k_reduce_tris_small<<<cdiv(T, 128), 128, 0, s>>>(tbox, T, g->assign, err, W, fsorted, fs,
+                                                     fe, g->sums, g->amax, g->amax_val);
+  } else {
+    const long rblocks = std::min<long>(cdiv(T, 8), (long)num_sms() * 4);
+    SP_CUDA(cudaMemsetAsync(g->nkeys + 3, 0, sizeof(unsigned long long), s));
+    k_reduce_tris<<<rblocks, 256, 0, s>>>(tv, tc, tbox, T, g->assign, err, W, fsorted, fs, fe,
+                                          g->sums, g->amax, g->amax_val,
+                                          (unsigned*)(g->nkeys + 3));
+  }
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+static int accumulate_mode = 1;  // 1: tiled (default), 0: global atomics + pixel sort
+int geo_accumulate_mode(int v) {
+  if (v >= 0) accumulate_mode = v;
+  return accumulate_mode;
+}
+
 // geometry.py:197-223 (partition="delaunay") or :226-244 ("voronoi")
 int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s) {
   const int H = g->H, W = g->W;
@@ -831,6 +1303,9 @@ int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s) {
     return reduce_cells(g->lab_a, err, g->m, g->sums, g->amax, g->amax_val, H, W, s);
   }
   if (g->T == 0) return 0;
+  if (accumulate_mode == 1 && H < 32768 && W < 32768 && n < (1ull << 32) &&
+      n <= g->key_cap)
+    return accumulate_tiled(g, err, s);
   SP_TRY(assign_tris<int>(g->tris, g->T, g->sy, g->sx, H, W, g->assign, false, s));
   SP_TRY(seed_min_tri<int>(g->tris, g->T, g->smt, g->m, s));
   SP_TRY(fallback(g->assign, g->lab_a, g->smt, g->assign, n, s));

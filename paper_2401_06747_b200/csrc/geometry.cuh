@@ -33,6 +33,7 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
                 int* nsteps_out, cudaStream_t s);
 int geo_delaunay(Geo* g, long* T_out, cudaStream_t s);
 int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s);
+int geo_accumulate_mode(int v);
 int geo_select(Geo* g, uint8_t* mask, long nbuckets, long want, long* picked, cudaStream_t s);
 int fill_highest_error(Geo* g, const double* err, uint8_t* mask, long want, cudaStream_t s);
 

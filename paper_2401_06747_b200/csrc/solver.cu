@@ -661,6 +661,7 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
     SP_TRY(chan_reduce<T>(0, (const T*)L0.b, nullptr, nullptr, per, nt, part, counter, bn, s));
     if (nt == 1 && h->use_graphs && graph_loop_on && h->h_loop) {
       SP_TRY(solve_loop_t<T>(h, tol, max_cycles, bn, s, done.data(), cv.data(), rep));
+      count_work(0, (long long)done[0] * L0.H * L0.W);
       if (rep) { rep->iterations = done[0]; rep->converged = cv[0]; }
       if (iters) iters[0] = done[0];
       if (conv) conv[0] = cv[0];
@@ -702,6 +703,11 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
   }
   if (iters) for (int t = 0; t < nt; ++t) iters[t] = done[t];
   if (conv) for (int t = 0; t < nt; ++t) conv[t] = cv[t];
+  {
+    long long cyc = 0;
+    for (int t = 0; t < nt; ++t) cyc += done[t];
+    count_work(nt > 1 ? 1 : 0, cyc * (long long)L0.H * L0.W);
+  }
   SP_CUDA(cudaMemcpyAsync(u_io, L0.u, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
   return 0;
 }

@@ -676,6 +676,7 @@ int strip_solve(StripGroup* g, const float* bsym, float* u_io, int init_mode, do
     }
   }
   if (rep) { rep->iterations = done; rep->converged = cv; }
+  count_work(0, (long long)done * g->h[0]->lv[0].H * g->h[0]->lv[0].W);
   // gather the owned rows of the finest level into every strip
   std::vector<int> r0(g->P), r1(g->P);
   for (int q = 0; q < g->P; ++q) { r0[q] = g->o0[0][q]; r1[q] = g->o1[0][q]; }

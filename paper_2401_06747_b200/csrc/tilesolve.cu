@@ -500,10 +500,13 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
   SP_CUDA(cudaMemcpyAsync(u_out, L0.u, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
   SP_CUDA(cudaMemcpyAsync(hl, done, sizeof(int) * 2 * nt, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
+  long long cyc = 0;
   for (int t = 0; t < nt; ++t) {
     if (iters) iters[t] = hl[t];
     if (conv) conv[t] = hl[nt + t];
+    cyc += hl[t];
   }
+  count_work(1, cyc * (long long)L0.H * L0.W);
   return 0;
 }
 
