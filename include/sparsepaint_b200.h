@@ -185,6 +185,20 @@ int sp_strip_set_mask(void* group, const uint8_t* mask, const void* values, void
 int sp_strip_solve(void* group, const void* bsym, void* u, int init_mode, double tol,
                    int cycles, int max_cycles, sp_solve_report* rep, void* stream);
 int sp_strip_levels(void* group, int* nlev, int* dims, int cap);
+/* Host-staged transport for a strip group whose strips live on other ranks
+ * (instead of the NCCL communicator of sp_strip_create): halo rows, the
+ * band-sum all-reduce and the agglomeration broadcasts go through these
+ * callbacks on pinned host buffers, stream-synchronously, and the V-cycle is
+ * not graph-captured.  It runs the multi-rank protocol where NCCL cannot
+ * (several ranks sharing one GPU: the CI harness; a gloo world).
+ *   int sendrecv(void* user, int peer, const void* send, size_t send_bytes,
+ *                void* recv, size_t recv_bytes);
+ *   int allreduce_f64(void* user, double* buf, size_t n);      (sum)
+ *   int bcast(void* user, void* buf, size_t bytes, int root);
+ * Each returns 0 on success.  Replaces the NCCL path of csrc/strips.cu;
+ * reference counterpart: none (the reference is single-process). */
+int sp_strip_set_host_transport(void* group, void* sendrecv, void* allreduce_f64, void* bcast,
+                                void* user);
 
 /* ================ B2: densification geometry workspace ================== */
 /* One workspace per (H, W).  Replaces, per densification iteration,

@@ -63,6 +63,7 @@ _SIGS = {
     "sp_strip_set_mask": [P, P, P, P],
     "sp_strip_solve": [P, P, P, c_int, c_double, c_int, c_int, P, P],
     "sp_strip_levels": [P, P, P, c_int],
+    "sp_strip_set_host_transport": [P, P, P, P, P],
     "sp_geo_create": [P, c_int, c_int],
     "sp_geo_destroy": [P],
     "sp_geo_voronoi": [P, P, c_double, P, P, P, P],

@@ -533,6 +533,7 @@ int strip_set_mask(StripGroup* g, const uint8_t* mask, const float* values, cuda
 int strip_solve(StripGroup* g, const float* bsym, float* u_io, int init_mode, double tol,
                 int cycles, int max_cycles, cudaStream_t s, SolveReport* rep);
 int strip_levels(StripGroup* g, int* nlev, int* dims, int cap);
+int strip_set_host_transport(StripGroup* g, const HostTransport& t);
 int nccl_unique_id(uint8_t* out);
 int nccl_comm_create(void** comm, const uint8_t* id_bytes, int nranks, int rank);
 int nccl_comm_destroy(void* comm);
@@ -573,6 +574,15 @@ int sp_strip_solve(void* g, const void* bsym, void* u, int init_mode, double tol
 }
 int sp_strip_levels(void* g, int* nlev, int* dims, int cap) {
   return sp::strip_levels((sp::StripGroup*)g, nlev, dims, cap);
+}
+int sp_strip_set_host_transport(void* g, void* sendrecv, void* allreduce_f64, void* bcast,
+                                void* user) {
+  sp::HostTransport t;
+  t.sendrecv = (decltype(t.sendrecv))sendrecv;
+  t.allreduce_f64 = (decltype(t.allreduce_f64))allreduce_f64;
+  t.bcast = (decltype(t.bcast))bcast;
+  t.user = user;
+  return sp::strip_set_host_transport((sp::StripGroup*)g, t);
 }
 }  // extern "C"
 

@@ -9,6 +9,16 @@
 
 namespace sp {
 
+// host-staged strip transport (strips.cu): caller callbacks over pinned
+// host buffers; each returns 0 on success
+struct HostTransport {
+  int (*sendrecv)(void* user, int peer, const void* send, size_t send_bytes, void* recv,
+                  size_t recv_bytes) = nullptr;
+  int (*allreduce_f64)(void* user, double* buf, size_t n) = nullptr;
+  int (*bcast)(void* user, void* buf, size_t bytes, int root) = nullptr;
+  void* user = nullptr;
+};
+
 struct HierCfg {
   int block = 32, overlap = 6, levels = 0, pre = 1, post = 1;
   double alpha = 1.0, rho = 0.25;

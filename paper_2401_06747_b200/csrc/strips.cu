@@ -134,6 +134,14 @@ struct StripGroup {
   std::vector<std::vector<double*>> bandcol;  // [nloc][La] [C][nbt][ncg]
   std::vector<std::vector<double*>> bands;    // [nloc][La] [C][nbt]
   ncclComm_t comm = nullptr;                  // strips on other ranks (P > nloc)
+  // host-staged transport (sp_strip_set_host_transport): the same exchanges
+  // through caller callbacks on pinned host buffers, stream-synchronous and
+  // never graph-captured -- the harness that runs the multi-rank protocol
+  // where NCCL cannot (several ranks on one GPU)
+  HostTransport host{};
+  bool host_mode = false;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
   // the V-cycle (kernels, halo copies / NCCL calls) recorded once as a CUDA
   // graph on a private stream and replayed on the caller's stream
   cudaGraphExec_t graph = nullptr;
@@ -151,7 +159,9 @@ struct StripGroup {
     for (auto& vv : bands)
       for (double* p : vv) if (p) cudaFree(p);
     for (Hier* x : h) delete x;
+    if (stage) cudaFreeHost(stage);
   }
+  bool remote_ok() const { return comm != nullptr || host_mode; }
   bool local(int p) const { return p >= first && p < first + nloc; }
   int rank_of(int p) const { return p; }  // NCCL: one strip per rank, rank = strip
 };
@@ -198,6 +208,41 @@ int copy_rows(StripGroup& g, int lv, int which, int p, int q, int r0, int r1, cu
   return 0;
 }
 
+int stage_for(StripGroup& g, size_t bytes) {
+  if (g.stage_bytes >= bytes) return 0;
+  if (g.stage) cudaFreeHost(g.stage);
+  g.stage = nullptr;
+  g.stage_bytes = 0;
+  SP_CUDA(cudaMallocHost(&g.stage, bytes));
+  g.stage_bytes = bytes;
+  return 0;
+}
+
+// host transport: rows [s0, s1) of every channel to strip q, rows [r0, r1)
+// from it (pinned staging, stream-synchronous)
+int host_sendrecv(StripGroup& g, float* buf, const Level& L, int q, int s0, int s1, int r0,
+                  int r1, cudaStream_t s) {
+  const size_t rowb = sizeof(float) * L.W, pitch = sizeof(float) * L.H * L.W;
+  const size_t sb = (size_t)g.C * std::max(0, s1 - s0) * rowb;
+  const size_t rb = (size_t)g.C * std::max(0, r1 - r0) * rowb;
+  SP_TRY(stage_for(g, sb + rb + 16));
+  char* sh = (char*)g.stage;
+  char* rh = sh + sb;
+  if (sb)
+    SP_CUDA(cudaMemcpy2DAsync(sh, (s1 - s0) * rowb, rowp(buf, L, 0, s0), pitch, (s1 - s0) * rowb,
+                              g.C, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  if (g.host.sendrecv(g.host.user, g.rank_of(q), sh, sb, rh, rb)) {
+    set_error("host transport: send/recv with strip %d failed", q);
+    return -1;
+  }
+  if (rb)
+    SP_CUDA(cudaMemcpy2DAsync(rowp(buf, L, 0, r0), pitch, rh, (r1 - r0) * rowb, (r1 - r0) * rowb,
+                              g.C, cudaMemcpyHostToDevice, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
 // halo exchange of buffer `which` (0 u, 1 b, 2 r) at partitioned level lv
 int exchange(StripGroup& g, int lv, int which, cudaStream_t s) {
   if (g.P == 1) return 0;
@@ -218,12 +263,16 @@ int exchange(StripGroup& g, int lv, int which, cudaStream_t s) {
         SP_TRY(copy_rows(g, lv, which, p, q, rr0, rr1, s));
         continue;
       }
-      if (!g.comm || !n) { set_error("strip %d has no transport to strip %d", p, q); return -2; }
-      if (!grouped) { SP_NCCL(n->GroupStart()); grouped = true; }
       // what q needs from p
       const int qo0 = g.o0[lv][q], qo1 = g.o1[lv][q];
       const int qe0 = std::max(0, qo0 - g.halo), qe1 = std::min(L.H, qo1 + g.halo);
       const int s0 = side == 0 ? qo1 : qe0, s1 = side == 0 ? qe1 : qo0;
+      if (g.host_mode) {
+        SP_TRY(host_sendrecv(g, (float*)buf, L, q, s0, s1, rr0, rr1, s));
+        continue;
+      }
+      if (!g.comm || !n) { set_error("strip %d has no transport to strip %d", p, q); return -2; }
+      if (!grouped) { SP_NCCL(n->GroupStart()); grouped = true; }
       for (int c = 0; c < g.C; ++c) {
         if (s1 > s0)
           SP_NCCL(n->Send(rowp(buf, L, c, s0), (size_t)(s1 - s0) * L.W, ncclFloat32, g.rank_of(q),
@@ -249,9 +298,32 @@ int gather_rows(StripGroup& g, int lv, int which, const std::vector<int>& r0,
       if (q != g.first + i && g.local(q))
         SP_TRY(copy_rows(g, lv, which, g.first + i, q, r0[q], r1[q], s));
   if (g.nloc == g.P) return 0;
-  if (!g.comm || !n) { set_error("strip group spans ranks without a communicator"); return -2; }
   Level& L = g.h[0]->lv[lv];
   void* buf = which == 0 ? L.u : (which == 1 ? L.b : L.r);
+  if (g.host_mode) {
+    // one strip per rank: broadcast every strip's owned rows from its rank
+    const size_t rowb = sizeof(float) * L.W, pitch = sizeof(float) * L.H * L.W;
+    for (int q = 0; q < g.P; ++q) {
+      if (r1[q] <= r0[q]) continue;
+      const size_t nb = (size_t)g.C * (r1[q] - r0[q]) * rowb;
+      SP_TRY(stage_for(g, nb));
+      const bool root = g.local(q);
+      if (root)
+        SP_CUDA(cudaMemcpy2DAsync(g.stage, (r1[q] - r0[q]) * rowb, rowp(buf, L, 0, r0[q]), pitch,
+                                  (r1[q] - r0[q]) * rowb, g.C, cudaMemcpyDeviceToHost, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+      if (g.host.bcast(g.host.user, g.stage, nb, g.rank_of(q))) {
+        set_error("host transport: broadcast from strip %d failed", q);
+        return -1;
+      }
+      if (!root)
+        SP_CUDA(cudaMemcpy2DAsync(rowp(buf, L, 0, r0[q]), pitch, g.stage, (r1[q] - r0[q]) * rowb,
+                                  (r1[q] - r0[q]) * rowb, g.C, cudaMemcpyHostToDevice, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+    }
+    return 0;
+  }
+  if (!g.comm || !n) { set_error("strip group spans ranks without a communicator"); return -2; }
   SP_NCCL(n->GroupStart());
   for (int q = 0; q < g.P; ++q)
     for (int c = 0; c < g.C; ++c)
@@ -303,7 +375,18 @@ int residual_norms(StripGroup& g, int lv, bool exch, cudaStream_t s) {
                                   g.bands[j][lv] + b0, sizeof(double) * g.nbt[lv],
                                   sizeof(double) * (b1 - b0), g.C, cudaMemcpyDeviceToDevice, s));
       }
-    if (g.nloc < g.P) {
+    if (g.nloc < g.P && g.host_mode) {
+      const size_t nb = sizeof(double) * g.C * g.nbt[lv];
+      SP_TRY(stage_for(g, nb));
+      SP_CUDA(cudaMemcpyAsync(g.stage, g.bands[0][lv], nb, cudaMemcpyDeviceToHost, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+      if (g.host.allreduce_f64(g.host.user, (double*)g.stage, (size_t)g.C * g.nbt[lv])) {
+        set_error("host transport: all-reduce failed");
+        return -1;
+      }
+      SP_CUDA(cudaMemcpyAsync(g.bands[0][lv], g.stage, nb, cudaMemcpyHostToDevice, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+    } else if (g.nloc < g.P) {
       NcclApi* n = nccl();
       if (!g.comm || !n) { set_error("strip group spans ranks without a communicator"); return -2; }
       SP_NCCL(n->AllReduce(g.bands[0][lv], g.bands[0][lv], (size_t)g.C * g.nbt[lv],
@@ -465,10 +548,9 @@ int strip_create(StripGroup** out, int C, int H, int W, const HierCfg& cfg, int 
               halo);
     return -2;
   }
-  if (nloc < P && !comm) {
-    set_error("strips on other ranks need an NCCL communicator");
-    return -2;
-  }
+  // strips on other ranks need a transport: the NCCL communicator here, or a
+  // host transport installed right after creation (sp_strip_set_host_transport);
+  // an exchange without either fails with "no transport"
   if (tma_view_ok(128) && tma_prepare()) return -1;
   StripGroup* g = new StripGroup();
   g->P = P; g->nloc = nloc; g->first = first; g->La = La; g->halo = halo;
@@ -570,6 +652,20 @@ int strip_create(StripGroup** out, int C, int H, int W, const HierCfg& cfg, int 
 
 void strip_destroy(StripGroup* g) { delete g; }
 
+int strip_set_host_transport(StripGroup* g, const HostTransport& t) {
+  if (!t.sendrecv || !t.allreduce_f64 || !t.bcast) {
+    set_error("host transport needs send/recv, all-reduce and broadcast callbacks");
+    return -2;
+  }
+  if (g->graph) {
+    cudaGraphExecDestroy(g->graph);
+    g->graph = nullptr;
+  }
+  g->host = t;
+  g->host_mode = true;
+  return 0;
+}
+
 int strip_set_mask(StripGroup* g, const uint8_t* mask, const float* values, cudaStream_t s) {
   for (Hier* h : g->h) SP_TRY(hier_set_mask(h, mask, values, s));
   return 0;
@@ -615,6 +711,7 @@ int strip_solve(StripGroup* g, const float* bsym, float* u_io, int init_mode, do
   int done = 0, cv = 0;
   auto norms0 = [&](bool exch) -> int { return residual_norms(*g, 0, exch, s); };
   auto cycle = [&]() -> int {
+    if (g->host_mode) return vcycle(*g, 0, true, s);  // host callbacks: not capturable
     if (!g->graph) {
       if (!g->cap) SP_CUDA(cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking));
       // order the private capture stream after the work already queued on s

@@ -165,20 +165,93 @@ class NcclComm:
             pass
 
 
+_SENDRECV = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                             ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t)
+_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+_BCAST = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                          ctypes.c_int)
+
+
+def _host_view(addr, nbytes, dtype=torch.uint8):
+    """A CPU tensor over `nbytes` of (pinned) host memory at `addr`."""
+    if nbytes == 0:
+        return torch.empty(0, dtype=dtype)
+    buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+    return torch.frombuffer(buf, dtype=torch.uint8).view(dtype)
+
+
+class HostComm:
+    """Host-staged strip transport over the current ``torch.distributed``
+    group (any backend with CPU point-to-point, e.g. gloo): the library hands
+    pinned host buffers to these callbacks (sp_strip_set_host_transport).
+    It runs the multi-rank strip protocol where NCCL cannot -- several ranks
+    sharing one GPU (the CI harness) -- at host-copy speed; NcclComm is the
+    performance transport."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            raise RuntimeError("HostComm needs torch.distributed to be initialised")
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.calls = {"sendrecv": 0, "allreduce": 0, "bcast": 0}
+        self._cbs = (_SENDRECV(self._sendrecv), _ALLREDUCE(self._allreduce), _BCAST(self._bcast))
+
+    def _sendrecv(self, user, peer, sp_, sb, rp, rb):
+        try:
+            reqs = []
+            if sb:
+                reqs.append(self.dist.isend(_host_view(sp_, sb), peer))
+            if rb:
+                reqs.append(self.dist.irecv(_host_view(rp, rb), peer))
+            for q in reqs:
+                q.wait()
+            self.calls["sendrecv"] += 1
+            return 0
+        except Exception:
+            return -1
+
+    def _allreduce(self, user, p, n):
+        try:
+            self.dist.all_reduce(_host_view(p, 8 * n, torch.float64))
+            self.calls["allreduce"] += 1
+            return 0
+        except Exception:
+            return -1
+
+    def _bcast(self, user, p, nbytes, root):
+        try:
+            self.dist.broadcast(_host_view(p, nbytes), root)
+            self.calls["bcast"] += 1
+            return 0
+        except Exception:
+            return -1
+
+    def install(self, group_handle):
+        f = [ctypes.cast(cb, ctypes.c_void_p) for cb in self._cbs]
+        call("sp_strip_set_host_transport", group_handle, f[0], f[1], f[2], None)
+
+    def close(self):
+        pass
+
+
 class _StripGroup:
     """One native strip group (csrc/strips.cu): P strips of a (C, H, W)
     float32 hierarchy, the strips [first, first + nloc) held here."""
 
     def __init__(self, key, comm):
-        C, H, W, block, overlap, levels, pre, post, alpha, rho, P, La, nloc, first = key
+        C, H, W, block, overlap, levels, pre, post, alpha, rho, P, La, nloc, first = key[:14]
         self.key = key
         self.La, self.o0, self.o1 = strip_plan(H, W, P, La, _cfg_of(key))
         flat0 = np.array([v for row in self.o0 for v in row] or [0], np.int32)
         flat1 = np.array([v for row in self.o1 for v in row] or [0], np.int32)
         self.h = ctypes.c_void_p()
+        nccl = comm is not None and not isinstance(comm, HostComm)
         call("sp_strip_create", ctypes.byref(self.h), C, H, W, block, overlap, levels, pre,
              post, alpha, rho, P, nloc, first, self.La, HALO, ptr(flat0), ptr(flat1),
-             comm.handle if comm is not None else None)
+             comm.handle if nccl else None)
+        if isinstance(comm, HostComm):
+            comm.install(self.h)
         self.has_values = False
 
     def destroy(self):
@@ -316,12 +389,19 @@ class StripSolver:
         self._comm = _comm
         o = self.cfg.oras
         self._key = (channels, height, width, o.block, o.overlap, self.cfg.levels, self.cfg.pre,
-                     self.cfg.post, float(o.alpha), float(o.rho), strips, self.La, nloc, first)
+                     self.cfg.post, float(o.alpha), float(o.rho), strips, self.La, nloc, first,
+                     id(_comm) if _comm is not None else 0)
 
     @classmethod
-    def distributed(cls, height, width, channels, cfg=None, La=None):
+    def distributed(cls, height, width, channels, cfg=None, La=None, transport="nccl"):
+        """One strip per rank of the current ``torch.distributed`` job.
+        transport "nccl": the library's NCCL communicator (one GPU per rank);
+        "host": host-staged exchanges through torch.distributed (HostComm --
+        e.g. gloo ranks sharing one GPU)."""
         import torch.distributed as dist
-        comm = NcclComm()
+        if transport not in ("nccl", "host"):
+            raise ValueError("transport must be 'nccl' or 'host'")
+        comm = NcclComm() if transport == "nccl" else HostComm()
         return cls(height, width, channels, strips=dist.get_world_size(), cfg=cfg, La=La,
                    _rank=dist.get_rank(), _comm=comm)
 

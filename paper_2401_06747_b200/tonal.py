@@ -354,12 +354,15 @@ class _RasBlocks:
         if self.ranks == 1:
             return v
         import torch.distributed as dist
-        pad = torch.zeros((self.chunk,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+        # NCCL gathers device tensors; other backends (the host-transport
+        # harness, gloo) through host copies
+        dev = v.device if dist.get_backend() == "nccl" else torch.device("cpu")
+        pad = torch.zeros((self.chunk,) + tuple(v.shape[1:]), dtype=v.dtype, device=dev)
         pad[:self.nt] = v
         out = torch.empty((self.chunk * self.ranks,) + tuple(v.shape[1:]), dtype=v.dtype,
-                          device=v.device)
+                          device=dev)
         dist.all_gather_into_tensor(out, pad)
-        return out[:self.nt_all].contiguous()
+        return out[:self.nt_all].to(v.device).contiguous()
 
     def scatter_add(self, g, v):
         """g += sum_b T(1/cover) * v_b (tonal.py:375-380); v holds all blocks."""
