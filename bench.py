@@ -284,6 +284,38 @@ def run_strips(world, rank, steps=3):
             "scaling": "strong (fixed image, one strip per GPU)"}
 
 
+def run_strip_pipeline(world, steps):
+    """N > 1 beside the replicas: the same 4K pipeline on ONE image cut
+    into one row strip per rank (every solve on strips over NCCL, geometry
+    replicated, RAS blocks sharded) -- strong scaling of the metric's wall
+    time.  Device time with CUDA events, max over ranks."""
+    import torch
+
+    import paper_2401_06747_b200 as sp
+    from oracle.oracle import synth  # input generator only
+    from paper_2401_06747_b200.strips import StripSolver
+    try:
+        cfg = sp.PipelineConfig()
+        f = torch.from_numpy(synth(H, W, C, seed=0)).cuda()
+        solver = StripSolver.distributed(H, W, C, cfg=cfg.solver().cfg)
+        sp.run_pipeline(sp.Image(f), cfg, solver=solver)
+        torch.cuda.synchronize()
+        stream = torch.cuda.current_stream()
+        _barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            mask, st, hist, _ = sp.run_pipeline(sp.Image(f), cfg, solver=solver)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+        return {"value_s": ms / 1e3, "ms_per_step": ms, "n_strips": world,
+                "partitioned_levels": solver.La, "final_mse": st.mse,
+                "mask_count": mask.count, "scaling": "strong (one 4K image on N GPUs)"}
+    except Exception as e:  # reported, never fatal to the replica measurement
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -422,6 +454,9 @@ def run_ours(args):
                          "block solves separately) / device step time"}
 
     strips = None if args.no_strips else run_strips(world, rank)
+    strip_pipe = None
+    if world > 1 and not strips_mode and not args.no_strips:
+        strip_pipe = run_strip_pipeline(world, args.steps)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -441,6 +476,7 @@ def run_ours(args):
             "roofline": roof, "stencil_roofline": stencil_roofline, "kernels": kern,
             "solver": solver, "throughput": pipe_work,
             "strips": strips,
+            "strips_pipeline": strip_pipe,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
