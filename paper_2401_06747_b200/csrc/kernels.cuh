@@ -27,7 +27,13 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile = 1, const int* active = nullptr,
-                      int stride = 0, int corr_nb = 0, size_t ps = 0);
+                      int stride = 0, int corr_nb = 0, size_t ps = 0,
+                      const int* wdelta = nullptr);
+// wdelta[b] = c - b where block c holds weights identical to block b's
+// (interior blocks share one 32x32 pattern): the ORAS epilogue reads the
+// shared pattern (cache-resident) instead of every block's own weights
+int weight_aliases(const float* weights, int nby, int nbx, int bh, int bw, int* wdelta,
+                   cudaStream_t s);
 // u += weighted corrections of the covering blocks, in block order
 template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,

@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
     const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
-    float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps) {
+    float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps,
+    const int* __restrict__ wdelta) {
   // FULLH: a full 32 x 32 block (bh == bw == 32): compile-time row / column
   // offsets in the job's loads and stores
   constexpr int R = 32;
@@ -561,7 +562,9 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
            : warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh, tau,
                                       cap, j);
   float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw) + j;
-  const float* wb = weights + (size_t)bi * bh * bw + j;
+  // interior blocks read the one shared weight pattern (bit-identical values)
+  const long wb_i = (long)bi + (wdelta ? wdelta[bi] : 0);
+  const float* wb = weights + wb_i * bh * bw + j;
   if (lane_ok) {
 #pragma unroll
     for (int s = 0; s < R; ++s)
@@ -1015,7 +1018,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile, const int* active, int stride,
-                      int corr_nb, size_t ps) {
+                      int corr_nb, size_t ps, const int* wdelta) {
   const int npx = bh * bw;
   if (ps && ps != (size_t)H * W &&
       !(sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
@@ -1047,7 +1050,8 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
 #undef SP_WARP
     kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
                                 bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
-                                (const float*)weights, (float*)corr, active, corr_nb, ps);
+                                (const float*)weights, (float*)corr, active, corr_nb, ps,
+                                wdelta);
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
     kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
@@ -1104,6 +1108,31 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   return 0;
 }
 
+// wdelta[b] = cb - b when block b's weights equal block cb's bit for bit
+// (cb: the interior block (1, 1)), else 0
+__global__ void k_weight_alias(const float* __restrict__ w, int npx, int cb,
+                               int* __restrict__ wdelta) {
+  const int b = blockIdx.x;
+  __shared__ int diff;
+  if (threadIdx.x == 0) diff = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < npx; i += blockDim.x)
+    if (__float_as_uint(w[(size_t)b * npx + i]) != __float_as_uint(w[(size_t)cb * npx + i]))
+      diff = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) wdelta[b] = diff ? 0 : cb - b;
+}
+
+int weight_aliases(const float* weights, int nby, int nbx, int bh, int bw, int* wdelta,
+                   cudaStream_t s) {
+  const int nb = nby * nbx;
+  if (nby < 3 || nbx < 3) return cudaMemsetAsync(wdelta, 0, sizeof(int) * nb, s) == cudaSuccess
+                                     ? 0 : (set_error("wdelta memset failed"), -1);
+  k_weight_alias<<<nb, 256, 0, s>>>(weights, bh * bw, nbx + 1, wdelta);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
 template <typename T>
 int block_weights_launch(T* weights, const int* ys, const int* xs, const int* row_k0,
                          const int* row_n, const int* col_k0, const int* col_n, int nby,
@@ -1120,7 +1149,7 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
   template int oras_local_launch<T>(const T*, const uint8_t*, const double*, double,        \
                                     const int*, const int*, int, int, int, int, int, int,   \
                                     int, double, long, double, const T*, T*, cudaStream_t,  \
-                                    int, const int*, int, int, size_t);                     \
+                                    int, const int*, int, int, size_t, const int*);         \
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
                                     int, int, int, cudaStream_t, int, const int*, int,      \

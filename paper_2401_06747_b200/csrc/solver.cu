@@ -72,7 +72,8 @@ Hier::~Hier() {
   for (auto& L : lv) {
     for (void* p : {(void*)L.mask, L.values, L.u, L.b, L.r, L.corr, L.weights, (void*)L.partial,
                     (void*)L.counter, (void*)L.norms, (void*)L.ys, (void*)L.xs,
-                    (void*)L.row_k0, (void*)L.row_n, (void*)L.col_k0, (void*)L.col_n})
+                    (void*)L.row_k0, (void*)L.row_n, (void*)L.col_k0, (void*)L.col_n,
+                    (void*)L.wdelta})
       if (p) cudaFree(p);
   }
   if (d_active) cudaFree(d_active);
@@ -144,6 +145,8 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     rc |= dalloc((void**)&L.row_n, sizeof(int) * hh);
     rc |= dalloc((void**)&L.col_k0, sizeof(int) * ww);
     rc |= dalloc((void**)&L.col_n, sizeof(int) * ww);
+    L.wdelta = nullptr;
+    if (dtype != SP_F64) rc |= dalloc((void**)&L.wdelta, sizeof(int) * nb);
     h->lv.push_back(L);
     if (rc) { delete h; return -1; }
     Level& B = h->lv.back();
@@ -165,6 +168,8 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
                   : block_weights_launch<float>((float*)B.weights, B.ys, B.xs, B.row_k0,
                                                 B.row_n, B.col_k0, B.col_n, B.nby, B.nbx,
                                                 B.bh, B.bw, hh, ww, cfg.overlap, 0);
+    if (!wrc && B.wdelta)
+      wrc = weight_aliases((const float*)B.weights, B.nby, B.nbx, B.bh, B.bw, B.wdelta, 0);
     if (wrc || cudaDeviceSynchronize() != cudaSuccess) {
       set_error("partition-of-unity weights failed");
       delete h;
@@ -291,7 +296,8 @@ int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
     SP_TRY(oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
                                 L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
                                 (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
-                                h->ntile, h->d_active, h->cfg.block - h->cfg.overlap));
+                                h->ntile, h->d_active, h->cfg.block - h->cfg.overlap, 0, 0,
+                                L.wdelta));
     SP_TRY(oras_blend_launch<T>((T*)L.u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,
                                 L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
                                 s, h->ntile, h->d_active));
@@ -762,7 +768,19 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
   // algorithmic bytes (SURVEY.md section 8d conventions, mask shared by channels)
   switch (which) {
     case 0: *bytes = (double)(3 * es * vec + plane * nt); break;          // u, b, r + mask
-    case 1: *bytes = (double)(es * C * nb * npx * nt * 3 + nb * npx * nt); break;  // r, w, corr + mask
+    case 1: {
+      // r + corr per job, mask once per block, weights: the blocks whose
+      // weights are not aliased to the shared interior pattern, plus it once
+      size_t own = nb;
+      if (L.wdelta) {
+        std::vector<int> wd(nb);
+        SP_CUDA(cudaMemcpy(wd.data(), L.wdelta, sizeof(int) * nb, cudaMemcpyDeviceToHost));
+        own = 1;
+        for (int d : wd) own += d == 0;
+      }
+      *bytes = (double)(es * C * nb * npx * nt * 2 + nb * npx * nt + es * own * npx);
+      break;
+    }
     case 2: *bytes = (double)(es * C * nb * npx * nt + 2 * es * vec); break;       // corr + u rw
     case 3: *bytes = (double)(2 * es * vec + plane * nt + es * vec / 4); break;    // u, b, mask, rc
     case 4: *bytes = (double)(2 * es * vec + plane * nt + es * vec / 4); break;    // u rw, mask, e
@@ -780,7 +798,8 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
         return oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
                                     L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
                                     (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
-                                    h->ntile, h->d_active, h->cfg.block - h->cfg.overlap);
+                                    h->ntile, h->d_active, h->cfg.block - h->cfg.overlap, 0, 0,
+                                    L.wdelta);
       case 2: {
         // blend into a scratch copy so the solver state is not disturbed
         return oras_blend_launch<T>((T*)L.r, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,

@@ -34,6 +34,7 @@ struct Level {
   unsigned* counter;
   double* norms;
   int *ys, *xs, *row_k0, *row_n, *col_k0, *col_n;
+  int* wdelta;  // [nby * nbx] shared-weight aliases (float levels), or null
 };
 
 struct Hier {

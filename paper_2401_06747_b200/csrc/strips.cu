@@ -426,7 +426,8 @@ int oras_blend(StripGroup& g, int lv, cudaStream_t s) {
     SP_TRY(oras_local_launch<float>(rowp(L.r, L, 0, V.e0), mrow(L, V.e0), L.norms, L.tau_scale,
                                     V.ys, L.xs, V.nby, L.nbx, L.bh, L.bw, hv, L.W, g.C,
                                     hh->gamma, (long)npx, 1.0, (const float*)L.weights + boff,
-                                    corr, s, 1, nullptr, 0, nb, ps));
+                                    corr, s, 1, nullptr, 0, nb, ps,
+                                    L.wdelta ? L.wdelta + (size_t)V.kya * L.nbx : nullptr));
     SP_TRY(oras_blend_launch<float>(rowp(L.u, L, 0, V.e0), corr, V.ys, L.xs, V.row_k0,
                                     V.row_n, L.col_k0, L.col_n, V.nby, L.nbx, L.bh, L.bw, hv,
                                     L.W, g.C, s, 1, nullptr, nb, ps));

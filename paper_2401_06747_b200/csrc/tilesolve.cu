@@ -468,7 +468,8 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
     return oras_local_launch<float>((const float*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
                                     L.nby, L.nbx, L.bh, L.bw, L.H, L.W, C, h->gamma,
                                     (long)L.bh * L.bw, 1.0, (const float*)L.weights,
-                                    (float*)L.corr, s, nt, h->d_active, stride);
+                                    (float*)L.corr, s, nt, h->d_active, stride, 0, 0,
+                                    L.wdelta);
   };
   // V-cycles run in batches between reads of the live-block count: a block
   // that stops inside a batch is skipped by every later launch (each kernel
