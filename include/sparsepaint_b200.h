@@ -219,6 +219,10 @@ int sp_geo_accumulate(void* geo, const double* err, int voronoi, void* stream);
  * (default), 0 = global atomicMin rasteriser + pixel radix sort; both are
  * bit-identical to numba_impl.py:442-498.  v < 0 only reads the setting. */
 int sp_geo_accumulate_mode(int v);
+/* Programmatic dependent launch for the V-cycle kernels of the multigrid
+ * levels >= v (the small levels; measured neutral, so off by default: -1); -1 turns it
+ * off, v < -1 only reads the setting.  Results are identical either way. */
+int sp_pdl_from_level(int v);
 /* marks the argmax pixels of the `want` best eligible buckets in mask */
 int sp_geo_select(void* geo, uint8_t* mask, long nbuckets, long want, long* picked,
                   void* stream);

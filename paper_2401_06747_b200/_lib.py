@@ -70,6 +70,7 @@ _SIGS = {
     "sp_geo_delaunay": [P, P, P],
     "sp_geo_accumulate": [P, P, c_int, P],
     "sp_geo_accumulate_mode": [c_int],
+    "sp_pdl_from_level": [c_int],
     "sp_geo_select": [P, P, c_long, c_long, P, P],
     "sp_geo_fill_highest_error": [P, P, P, c_long, P],
     "sp_geo_load": [P, P, P, P, c_long, P],

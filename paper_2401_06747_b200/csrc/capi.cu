@@ -39,6 +39,10 @@ void retain_pool_memory() {
   done[dev] = true;
 }
 
+static thread_local bool g_pdl_now = false;
+bool pdl_now() { return g_pdl_now; }
+void pdl_set(bool on) { g_pdl_now = on; }
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -403,6 +407,10 @@ int sp_geo_voronoi(void* g, const uint8_t* mask, double start_hint, long* m, dou
 int sp_geo_delaunay(void* g, long* ntris, void* s) {
   return geo_delaunay((Geo*)g, ntris, STREAM(s));
 }
+
+// programmatic dependent launch of the V-cycle kernels on levels >= v
+// (v = -1: off; v < -1: read only); returns the setting
+int sp_pdl_from_level(int v) { return sp::pdl_from_level(v); }
 
 // accumulate implementation (A/B and tests): 1 = tile-binned rasteriser +
 // bbox-order reduction (default), 0 = global atomics + pixel sort; v < 0 reads

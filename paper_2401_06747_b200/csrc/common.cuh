@@ -50,6 +50,44 @@ void count_work(int kind, long long px_cycles);
 
 enum DType { SP_F32 = 0, SP_F64 = 1 };
 
+// ---- programmatic dependent launch (coarse multigrid levels) ---------------
+// On the small levels of a V-cycle every kernel is a few microseconds and the
+// dependent-launch gap between consecutive kernels dominates.  Launched with
+// programmatic stream serialization, a kernel is scheduled while its
+// predecessor still runs and blocks in pdl_enter() until the predecessor has
+// completed and its memory is visible; pdl_enter() then releases its own
+// successor.  Kernels that may be launched this way call pdl_enter() before
+// touching global memory (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// host side: PDL for the launches made while pdl_now() is set (solver.cu
+// sets it for the levels >= sp_pdl_from_level of a V-cycle)
+bool pdl_now();
+void pdl_set(bool on);
+int pdl_from_level(int v);  // solver.cu
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args... args) {
+  if (!pdl_now()) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 inline unsigned cdiv(long a, long b) { return (unsigned)((a + b - 1) / b); }
 
 // number of SMs of the current device (cached)

@@ -9,7 +9,9 @@ template <typename T> int neglap(const T* x, T* out, int C, int H, int W, double
 template <typename T> int inpaint_matvec(const T* x, const uint8_t* m, T* out, int C, int H, int W, double inv_h2, cudaStream_t s);
 template <typename T> int sym_matvec(const T* x, const uint8_t* m, T* out, int C, int H, int W, double inv_h2, cudaStream_t s);
 template <typename T> int sym_rhs(const T* b, const uint8_t* m, T* out, T* e, int C, int H, int W, double inv_h2, cudaStream_t s, int ntile = 1, const int* active = nullptr);
-template <typename T> int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s, int ntile = 1, const int* active = nullptr);
+// b~ = sym_rhs(where(m, x, 0)); enforce_u (optional): u = b~ on the stored
+// pixels in the same pass (sparse stores)
+template <typename T> int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s, int ntile = 1, const int* active = nullptr, T* enforce_u = nullptr);
 template <typename T> int ct_apply(const T* w, const uint8_t* m, T* out, int C, int H, int W, double inv_h2, cudaStream_t s, int ntile = 1, const int* active = nullptr);
 size_t residual_partials(int H, int W);
 template <typename T> int residual(const T* u, const T* b, const uint8_t* m, T* r, double* partial, unsigned* counter, double* norms, int C, int H, int W, double inv_h2, cudaStream_t s, int ntile = 1, const int* active = nullptr);

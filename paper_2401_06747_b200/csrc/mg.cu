@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(NT) k_sym_rhs(const T* __restrict__ b,
                                                 T* __restrict__ out, T* __restrict__ e,
                                                 int C, int H, int W, double inv_h2,
                                                 const int* __restrict__ active) {
+  pdl_enter();
   PLANE_SETUP(C);
   const size_t plane = (size_t)H * W, vo = (size_t)z * plane;
   m += (size_t)tile * plane;
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(NT) k_residual(
     T* __restrict__ r, double* __restrict__ partial, unsigned* __restrict__ counter,
     double* __restrict__ norms, int C, int H, int W, double inv_h2,
     const int* __restrict__ active) {
+  pdl_enter();
   __shared__ double s0[NT / 32];
   __shared__ bool am_last;
   PLANE_SETUP(C);
@@ -213,6 +215,7 @@ template <typename T>
 __global__ void __launch_bounds__(NT) k_residual_restrict(
     const T* __restrict__ u, const T* __restrict__ b, const uint8_t* __restrict__ m,
     T* __restrict__ rc, int C, int H, int W, double inv_h2, const int* __restrict__ active) {
+  pdl_enter();
   __shared__ T rs[BY][BX + 1];
   PLANE_SETUP(C);
   const int ch_ = (H + 1) / 2, cw = (W + 1) / 2;
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(NT) k_prolong_enforce(
     const T* __restrict__ e, T* __restrict__ u, const T* __restrict__ b,
     const uint8_t* __restrict__ m, int C, int chh, int cww, int H, int W, int add,
     const int* __restrict__ active) {
+  pdl_enter();
   PLANE_SETUP(C);
   const size_t plane = (size_t)H * W, vo = (size_t)z * plane;
   m += (size_t)tile * plane;
@@ -469,6 +473,7 @@ __global__ void __launch_bounds__(NT) k4_residual(
     T* __restrict__ r, double* __restrict__ partial, unsigned* __restrict__ counter,
     double* __restrict__ norms, int C, int H, int W, double inv_h2,
     const int* __restrict__ active) {
+  pdl_enter();
   __shared__ double s0[NT / 32];
   __shared__ bool am_last;
   PLANE_SETUP(C);
@@ -523,6 +528,7 @@ __global__ void __launch_bounds__(NT) k4_rhs(const T* __restrict__ xin,
                                              T* __restrict__ out, T* __restrict__ e, int C,
                                              int H, int W, double inv_h2,
                                              const int* __restrict__ active) {
+  pdl_enter();
   PLANE_SETUP(C);
   const size_t plane = (size_t)H * W, vo = (size_t)z * plane;
   m += (size_t)tile * plane;
@@ -541,6 +547,8 @@ __global__ void __launch_bounds__(NT) k4_rhs(const T* __restrict__ xin,
         ee.a[i] = mk ? o.a[i] : (T)0;
       } else if (MODE == 1) {
         o.a[i] = mk ? q.c.a[i] : (T)(0.0 + nbr_sum_quad(q, i, true));
+        // fused enforce (solver.py:275-281): u = b~ on the stored pixels
+        if (e && mk) e[vo + k + i] = o.a[i];
       } else {
         o.a[i] = mk ? (T)((double)q.c.a[i] + nbr_sum_quad(q, i, false) * inv_h2) : (T)0;
       }
@@ -576,6 +584,7 @@ __global__ void __launch_bounds__(NT) k4_prolong_enforce(
     const T* __restrict__ e, T* __restrict__ u, const T* __restrict__ b,
     const uint8_t* __restrict__ m, int C, int chh, int cww, int H, int W, int add,
     const int* __restrict__ active) {
+  pdl_enter();
   PLANE_SETUP(C);
   const size_t plane = (size_t)H * W, vo = (size_t)z * plane;
   m += (size_t)tile * plane;
@@ -616,6 +625,7 @@ template <typename T>
 __global__ void __launch_bounds__(NT) k4_residual_restrict(
     const T* __restrict__ u, const T* __restrict__ b, const uint8_t* __restrict__ m,
     T* __restrict__ rc, int C, int H, int W, double inv_h2, const int* __restrict__ active) {
+  pdl_enter();
   __shared__ T rs[BY][4 * BX + 1];
   PLANE_SETUP(C);
   const int ch_ = (H + 1) / 2, cw = (W + 1) / 2;
@@ -681,22 +691,27 @@ int sym_rhs(const T* b, const uint8_t* m, T* out, T* e, int C, int H, int W, dou
             cudaStream_t s, int ntile, const int* active) {
   long nz = (long)ntile * C;
   if (VEC_OK(b, m, out, e))
-    k4_rhs<T, 0><<<mg_grid4(H, W, nz), kBlock, 0, s>>>(b, m, out, e, C, H, W, inv_h2, active);
+    SP_CUDA(launch_k(k4_rhs<T, 0>, mg_grid4(H, W, nz), kBlock, 0, s, b, m, out, e, C, H, W, inv_h2, active));
   else
-    k_sym_rhs<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(b, m, out, e, C, H, W, inv_h2, active);
+    SP_CUDA(launch_k(k_sym_rhs<T>, mg_grid(H, W, nz), kBlock, 0, s, b, m, out, e, C, H, W, inv_h2, active));
   SP_CHECK_LAUNCH();
   return 0;
 }
 
 template <typename T>
 int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s,
-                   int ntile, const int* active) {
+                   int ntile, const int* active, T* enforce_u) {
   long nz = (long)ntile * C;
-  if (VEC_OK(x, m, out))
-    k4_rhs<T, 1><<<mg_grid4(H, W, nz), kBlock, 0, s>>>(x, m, out, nullptr, C, H, W, 1.0,
-                                                       active);
-  else
+  if (VEC_OK(x, m, out)) {
+    SP_CUDA(launch_k(k4_rhs<T, 1>, mg_grid4(H, W, nz), kBlock, 0, s, x, m, out, enforce_u, C, H,
+                     W, 1.0, active));
+  } else {
     k_masked_sym_rhs<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(x, m, out, C, H, W, active);
+    if (enforce_u) {
+      SP_CHECK_LAUNCH();
+      return enforce<T>(enforce_u, out, m, C, H, W, 0, s, ntile, active);
+    }
+  }
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -706,8 +721,8 @@ int ct_apply(const T* w, const uint8_t* m, T* out, int C, int H, int W, double i
              cudaStream_t s, int ntile, const int* active) {
   long nz = (long)ntile * C;
   if (VEC_OK(w, m, out))
-    k4_rhs<T, 2><<<mg_grid4(H, W, nz), kBlock, 0, s>>>(w, m, out, nullptr, C, H, W, inv_h2,
-                                                       active);
+    SP_CUDA(launch_k(k4_rhs<T, 2>, mg_grid4(H, W, nz), kBlock, 0, s, w, m, out, nullptr, C, H, W, inv_h2,
+                                                       active));
   else
     k_ct_apply<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(w, m, out, C, H, W, inv_h2, active);
   SP_CHECK_LAUNCH();
@@ -720,11 +735,11 @@ int residual(const T* u, const T* b, const uint8_t* m, T* r, double* partial,
              cudaStream_t s, int ntile, const int* active) {
   long nz = (long)ntile * C;
   if (VEC_OK(u, b, m, r))
-    k4_residual<T><<<mg_grid4(H, W, nz), kBlock, 0, s>>>(u, b, m, r, partial, counter, norms,
-                                                         C, H, W, inv_h2, active);
+    SP_CUDA(launch_k(k4_residual<T>, mg_grid4(H, W, nz), kBlock, 0, s, u, b, m, r, partial, counter, norms,
+                                                         C, H, W, inv_h2, active));
   else
-    k_residual<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(u, b, m, r, partial, counter, norms, C,
-                                                       H, W, inv_h2, active);
+    SP_CUDA(launch_k(k_residual<T>, mg_grid(H, W, nz), kBlock, 0, s, u, b, m, r, partial, counter, norms, C,
+                                                       H, W, inv_h2, active));
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -734,11 +749,11 @@ int residual_restrict(const T* u, const T* b, const uint8_t* m, T* rc, int C, in
                       double inv_h2, cudaStream_t s, int ntile, const int* active) {
   long nz = (long)ntile * C;
   if (VEC_OK(u, b, m))
-    k4_residual_restrict<T><<<mg_grid4(H, W, nz), kBlock, 0, s>>>(u, b, m, rc, C, H, W,
-                                                                  inv_h2, active);
+    SP_CUDA(launch_k(k4_residual_restrict<T>, mg_grid4(H, W, nz), kBlock, 0, s, u, b, m, rc, C, H, W,
+                                                                  inv_h2, active));
   else
-    k_residual_restrict<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(u, b, m, rc, C, H, W, inv_h2,
-                                                                active);
+    SP_CUDA(launch_k(k_residual_restrict<T>, mg_grid(H, W, nz), kBlock, 0, s, u, b, m, rc, C, H, W, inv_h2,
+                                                                active));
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -757,11 +772,11 @@ int prolong_enforce(const T* e, T* u, const T* b, const uint8_t* m, int C, int c
                     int H, int W, int add, cudaStream_t s, int ntile, const int* active) {
   long nz = (long)ntile * C;
   if (VEC_OK(u, b, m))
-    k4_prolong_enforce<T><<<mg_grid4(H, W, nz), kBlock, 0, s>>>(e, u, b, m, C, chh, cww, H, W,
-                                                                add, active);
+    SP_CUDA(launch_k(k4_prolong_enforce<T>, mg_grid4(H, W, nz), kBlock, 0, s, e, u, b, m, C, chh, cww, H, W,
+                                                                add, active));
   else
-    k_prolong_enforce<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(e, u, b, m, C, chh, cww, H, W,
-                                                              add, active);
+    SP_CUDA(launch_k(k_prolong_enforce<T>, mg_grid(H, W, nz), kBlock, 0, s, e, u, b, m, C, chh, cww, H, W,
+                                                              add, active));
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -782,7 +797,7 @@ int enforce(T* u, const T* src, const uint8_t* m, int C, int H, int W, int zero_
   template int sym_rhs<T>(const T*, const uint8_t*, T*, T*, int, int, int, double,         \
                           cudaStream_t, int, const int*);                                  \
   template int masked_sym_rhs<T>(const T*, const uint8_t*, T*, int, int, int,              \
-                                 cudaStream_t, int, const int*);                           \
+                                 cudaStream_t, int, const int*, T*);                       \
   template int ct_apply<T>(const T*, const uint8_t*, T*, int, int, int, double,            \
                            cudaStream_t, int, const int*);                                 \
   template int residual<T>(const T*, const T*, const uint8_t*, T*, double*, unsigned*,     \

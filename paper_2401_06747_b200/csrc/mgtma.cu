@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(CR * 32) k_resid_tma(
     unsigned* __restrict__ counter, double* __restrict__ norms, float* __restrict__ rcoarse,
     int C, int H, int W, const int* __restrict__ active, double* __restrict__ bandcol,
     int band0, int nbt, size_t ps, size_t cps) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
   __shared__ uint64_t bars[NS];
@@ -318,8 +319,8 @@ int launch(const float* u, const float* b, const uint8_t* m, float* r, double* p
     return -1;
   }
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)((long)C * ntile));
-  k_resid_tma<MODE, NORMS><<<grid, CR * 32, SMEM, s>>>(mp, r, partial, counter, norms, rc, C, H,
-                                                       W, active, bandcol, band0, nbt, ps, cps);
+  SP_CUDA(launch_k(k_resid_tma<MODE, NORMS>, grid, dim3(CR * 32), SMEM, s, mp, r, partial,
+                   counter, norms, rc, C, H, W, active, bandcol, band0, nbt, ps, cps));
   SP_CHECK_LAUNCH();
   return 0;
 }
@@ -360,6 +361,7 @@ __global__ void __launch_bounds__(CR * 32) k_prolong_tma(
     const __grid_constant__ PMaps mp, float* __restrict__ u, const float* __restrict__ b,
     const uint8_t* __restrict__ m, int C, int chh, int cww, int H, int W,
     const int* __restrict__ active, size_t ps) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
   __shared__ uint64_t bars[NS];
@@ -504,12 +506,8 @@ int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int 
   }
   if (!add) mp.u = mp.m;  // unused
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)nz);
-  if (add)
-    k_prolong_tma<true><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active,
-                                                     ps);
-  else
-    k_prolong_tma<false><<<grid, CR * 32, PSMEM, s>>>(mp, u, b, m, C, chh, cww, H, W, active,
-                                                      ps);
+  SP_CUDA(launch_k(add ? k_prolong_tma<true> : k_prolong_tma<false>, grid, dim3(CR * 32), PSMEM,
+                   s, mp, u, b, m, C, chh, cww, H, W, active, ps));
   SP_CHECK_LAUNCH();
   return 0;
 }

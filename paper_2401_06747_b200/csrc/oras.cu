@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
     float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps,
     const int* __restrict__ wdelta) {
+  pdl_enter();
   // FULLH: a full 32 x 32 block (bh == bw == 32): compile-time row / column
   // offsets in the job's loads and stores
   constexpr int R = 32;
@@ -780,6 +781,7 @@ __global__ void __launch_bounds__(256) k_oras_blend(
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
     const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int Cdyn,
     const int* __restrict__ active, int corr_nb, size_t ps) {
+  pdl_enter();
   const int C = CM > 0 ? CM : Cdyn;
   const int tile = blockIdx.y;
   if (active && !active[tile]) return;
@@ -888,6 +890,7 @@ __global__ void __launch_bounds__(256) k_oras_blend3(
     const int* __restrict__ xs, const int* __restrict__ row_k0, const int* __restrict__ row_n,
     const int* __restrict__ col_k0, const int* __restrict__ col_n, int nbx, int H, int W,
     const int* __restrict__ active, int nb, size_t ps) {
+  pdl_enter();
   const int tile = blockIdx.y;
   if (active && !active[tile]) return;
   const int plane = (int)ps, cplane = nb * 1024;
@@ -987,6 +990,7 @@ __global__ void __launch_bounds__(256) k_oras_blend_plane(
     const int* __restrict__ row_n, const int* __restrict__ col_k0,
     const int* __restrict__ col_n, int nby, int nbx, int bh, int bw, int H, int W, int C,
     const int* __restrict__ active, int corr_nb, size_t ps) {
+  pdl_enter();
   const int z = blockIdx.y, tile = z / C;
   if (active && !active[tile]) return;
   const int nb = corr_nb > 0 ? corr_nb : nby * nbx;
@@ -1048,10 +1052,17 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
     auto kern = oras_kernel == 7 ? SP_WARP(1, true) : (wj == 1 ? SP_WARP(1, false)
                                                                : SP_WARP(WJ, false));
 #undef SP_WARP
-    kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
-                                bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
-                                (const float*)weights, (float*)corr, active, corr_nb, ps,
-                                wdelta);
+    if (oras_kernel == 7) {
+      SP_CUDA(launch_k(kern, g4, dim3(wj * 32), 0, s, (const float*)r, m, tau_src, tau_scale, ys,
+                       xs, nbx, nbl, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
+                       (float)inv_h2, (const float*)weights, (float*)corr, active, corr_nb, ps,
+                       wdelta));
+    } else {
+      kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
+                                  bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
+                                  (const float*)weights, (float*)corr, active, corr_nb, ps,
+                                  wdelta);
+    }
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
     kern<<<grid, NTJ, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, bh, bw, H,
@@ -1090,19 +1101,19 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   if (nbx_cta < 1) nbx_cta = 1;
   dim3 grid((unsigned)nbx_cta, (unsigned)nz), blk(32, 8);
 #define SP_BLEND(CM)                                                                      \
-  k_oras_blend<T, CM><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n, \
-                                          nby, nbx, bh, bw, H, W, C, active, corr_nb, ps)
+  SP_CUDA(launch_k(k_oras_blend<T, CM>, grid, blk, 0, s, u, corr, ys, xs, row_k0, row_n,    \
+                   col_k0, col_n, nby, nbx, bh, bw, H, W, C, active, corr_nb, ps))
   const long nbt = (long)(corr_nb > 0 ? corr_nb : nby * nbx);
   if (C == 1) SP_BLEND(1);
   else if (C == 3 && sizeof(T) == 4 && bh == 32 && bw == 32 && 3 * ps < (1UL << 31) &&
            3 * nbt * 1024 < (1L << 31))
-    k_oras_blend3<<<grid, blk, 0, s>>>((float*)u, (const float*)corr, ys, xs, row_k0, row_n,
-                                       col_k0, col_n, nbx, H, W, active, (int)nbt, ps);
+    SP_CUDA(launch_k(k_oras_blend3, grid, blk, 0, s, (float*)u, (const float*)corr, ys, xs,
+                     row_k0, row_n, col_k0, col_n, nbx, H, W, active, (int)nbt, ps));
   else if (C == 3) SP_BLEND(3);
   else if (C <= 4) SP_BLEND(0);
   else
-    k_oras_blend_plane<T><<<grid, blk, 0, s>>>(u, corr, ys, xs, row_k0, row_n, col_k0, col_n,
-                                               nby, nbx, bh, bw, H, W, C, active, corr_nb, ps);
+    SP_CUDA(launch_k(k_oras_blend_plane<T>, grid, blk, 0, s, u, corr, ys, xs, row_k0, row_n,
+                     col_k0, col_n, nby, nbx, bh, bw, H, W, C, active, corr_nb, ps));
 #undef SP_BLEND
   SP_CHECK_LAUNCH();
   return 0;

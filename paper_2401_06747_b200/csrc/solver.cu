@@ -305,12 +305,25 @@ int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
   return 0;
 }
 
+// programmatic dependent launch for the V-cycle kernels of the levels
+// >= pdl_from (the launch-latency-bound small levels); < 0: off
+static int pdl_from = -1;  // measured neutral on the 4K pipeline (probe_pdl.py): off
+int pdl_from_level(int v) {
+  if (v >= -1) pdl_from = v;
+  return pdl_from;
+}
+
 // solver.py:283-300; `first_done`: level lv's residual r/norms for the
 // current u are already in place (computed by the caller's tolerance check)
 template <typename T>
 int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
   const HierCfg& cfg = h->cfg;
   int last = (int)h->lv.size() - 1;
+  const bool pdl = pdl_from >= 0 && lv >= pdl_from;
+  struct Restore {
+    ~Restore() { pdl_set(false); }
+  } restore;
+  pdl_set(pdl);
   if (lv == last) return smooth_lv<T>(h, lv, cfg.pre + cfg.post, first_done, s);
   SP_TRY(smooth_lv<T>(h, lv, cfg.pre, first_done, s));
   Level& F = h->lv[lv];
@@ -319,6 +332,7 @@ int vcycle_lv(Hier* h, int lv, bool first_done, cudaStream_t s) {
   SP_TRY(sym_rhs<T>((const T*)G.r, G.mask, (T*)G.b, (T*)G.u, h->C, G.H, G.W, 1.0, s,
                     h->ntile, h->d_active));
   SP_TRY(vcycle_lv<T>(h, lv + 1, false, s));
+  pdl_set(pdl);
   SP_TRY(prolong_lv<T>(h, lv, 1, s));
   SP_TRY(smooth_lv<T>(h, lv, cfg.post, false, s));
   return 0;
@@ -641,11 +655,15 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
   } else {
     SP_CUDA(cudaMemsetAsync(L0.u, 0, sizeof(T) * n, s));
   }
-  if (src_mode == 1)  // b~ = sym_rhs(where(mask, x, 0)) straight into level 0
-    SP_TRY(masked_sym_rhs<T>(bsym, L0.mask, (T*)L0.b, C, L0.H, L0.W, s, nt, h->d_active));
-  else
+  if (src_mode == 1) {
+    // b~ = sym_rhs(where(mask, x, 0)) straight into level 0, u = b~ on the
+    // mask in the same pass
+    SP_TRY(masked_sym_rhs<T>(bsym, L0.mask, (T*)L0.b, C, L0.H, L0.W, s, nt, h->d_active,
+                             (T*)L0.u));
+  } else {
     SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
-  SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s, nt, h->d_active));
+    SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s, nt, h->d_active));
+  }
   std::vector<int> done(nt, 0), cv(nt, 0);
   if (tol < 0) {
     // solver.py:345-350: exactly `cycles` V-cycles, converged = True

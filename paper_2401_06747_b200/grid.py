@@ -168,7 +168,10 @@ class Image:
 class Mask:
     """Binary indicator (H, W) (grid.py:86-114)."""
 
-    def __init__(self, indicator):
+    def __init__(self, indicator, count=None):
+        # count: the caller's known number of stored pixels (skips a device
+        # reduction + host sync when the solver checks for an empty mask)
+        self._count = None if count is None else int(count)
         if isinstance(indicator, torch.Tensor):
             if indicator.dim() != 2:
                 raise ValueError("mask must be 2-D")
@@ -191,7 +194,7 @@ class Mask:
 
     @indicator.setter
     def indicator(self, value):
-        self.__init__(value)
+        self.__init__(value)  # (drops any cached count)
 
     @property
     def on_device(self) -> bool:
@@ -217,6 +220,8 @@ class Mask:
 
     @property
     def count(self) -> int:
+        if self._count is not None:
+            return self._count
         if self._host is None:
             return int(self._dev.sum(dtype=torch.int64).item())
         return int(self._host.sum())
