@@ -332,6 +332,21 @@ int sp_graph_loop(int v);
  * the per-pixel kernels everywhere; v < 0 queries.  A/B measurement aid, no
  * reference counterpart. */
 int sp_march_variant(int v);
+/* Within sweep variant 2: 1 = warp-streamed TMA kernels (each warp marches
+ * its own range of 8-row chunks through a private TMA ring, default), 0 =
+ * the CTA-tile TMA kernels.  Residuals, restrictions and prolongations are
+ * bit-identical; the residual norms group their float partials differently.
+ * Applies to launches made afterwards; v < 0 queries.  A/B aid, no
+ * reference counterpart. */
+int sp_ws_variant(int v);
+/* Chunks each warp of the warp-streamed sweeps keeps prefetched into L2
+ * ahead of its shared-memory ring (cp.async.bulk.prefetch.tensor; default 0,
+ * measured slower); v < 0 queries.  Timing only, results unchanged. */
+int sp_ws_prefetch(int v);
+/* Shared-memory stages per warp of the warp-streamed sweeps: 1 or 2 for
+ * every sweep, 0 = the measured per-sweep defaults (residual 2, restriction
+ * and prolongation 1); v < 0 queries.  Timing only, results unchanged. */
+int sp_ws_stages(int v);
 /* residual r = b~ - A~ u and per-plane sum r^2 of level lv's current iterate
  * (after a solve), computed by the hierarchy's sweep kernel, into device
  * buffers r_out [ntile][C][h][w], norms_out [ntile][C] (kernel-variant

@@ -99,6 +99,9 @@ _SIGS = {
     "sp_pairwise_sum": [P, ctypes.c_longlong, P, P],
     "sp_oras_variant": [c_int],
     "sp_march_variant": [c_int],
+    "sp_ws_variant": [c_int],
+    "sp_ws_prefetch": [c_int],
+    "sp_ws_stages": [c_int],
     "sp_tile_fused": [c_int],
     "sp_channel_parallel": [c_int],
     "sp_graph_loop": [c_int],

@@ -66,7 +66,11 @@ bool tma_ok(int H, int W, size_t npart);
 int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
               const int* active, double* bandcol = nullptr, int band0 = 0, int nbt = 0,
-              size_t ps = 0);
+              size_t ps = 0, size_t npart = 0);
+// warp-streamed sweeps (default 1) vs the CTA-tile kernels (0): sp_ws_variant
+int ws_variant(int v);
+int ws_prefetch(int v);  // chunks per warp prefetched into L2 (sp_ws_prefetch, default 0)
+int ws_stages(int v);    // shared-memory stages per warp, 1 or 2 (sp_ws_stages)
 bool tma_view_ok(int W);
 int tma_prepare();  // one-time kernel attributes (outside graph capture)
 // ps / cps: fine / coarse plane strides in elements (0 = H*W / its coarse

@@ -85,6 +85,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// L2 prefetch of a tensor box (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   (uint64_t)map),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
 struct Maps {
   CUtensorMap u, b, m;
 };
@@ -441,13 +449,460 @@ __global__ void __launch_bounds__(CR * 32) k_prolong_tma(
   }
 }
 
+// ---- warp-streamed sweeps (the default: sp_ws_variant) ----------------------
+// The CTA-tile kernels above spend 60-70 issued instructions per
+// pixel-channel (ncu: issue-bound at 69-75% with the DRAM at 4.4 TB/s): one
+// row per warp, so every value is converted and mask-tested once for each
+// of the up to five stencil rows that read it, and a CTA-wide barrier per
+// chunk.  Here every WARP is an independent streaming unit:
+//   - it owns a contiguous range of the plane's 8-row x 128-column chunks,
+//     taken down one 128-column strip (consecutive chunks share their halo
+//     rows, which then come from L2);
+//   - a private ring of SPW shared-memory stages, filled by its own elected
+//     lane through TMA (the same tensor maps and boxes as above, image
+//     borders are the TMA zero fill), completion on per-stage mbarriers;
+//   - the lane owns a 4-pixel column quad and MARCHES the chunk's 8 rows:
+//     each value is converted to double and masked once and reused as the
+//     down, centre and up neighbour, no barriers at all (__syncwarp only);
+//   - the grid is sized to the resident warp slots (one wave), the chunk
+//     ranges are balanced to one chunk, so there is no tail wave.
+// Arithmetic is the kernels' above bit for bit (numba_impl.py:68-98 /
+// 147-158 / 266-284 / 316-348): the residual, the restriction and the
+// prolongation are identical per element; only the float partials of the
+// residual norms group differently (per warp range instead of per tile), and
+// they are still reduced in a fixed order (deterministic).
+constexpr int WS_NW = 8;  // warps per CTA
+
+// the value as it enters a neighbour's sum: 0 where masked (selected in
+// float, then one conversion)
+__device__ __forceinline__ double qmask(float v, uint32_t mw, int i) {
+  return (double)(((mw >> (8 * i)) & 0xFFu) ? 0.0f : v);
+}
+
+__device__ __forceinline__ unsigned char* ws_smem(unsigned char* raw) {
+  // 128-byte aligned base of the dynamic shared memory, as a shared-space
+  // pointer (LDS, not generic loads)
+  return raw + ((128u - (smem_u32(raw) & 127u)) & 127u);
+}
+
+// the warp's chunk range [q0, q1) of a plane of nq chunks split over gwp warps
+__device__ __forceinline__ void ws_range(long nq, int gw, int gwp, long& q0, long& q1) {
+  q0 = nq * gw / gwp;
+  q1 = nq * (gw + 1) / gwp;
+}
+
+// MODE 0: residual (+ norms); MODE 1: residual + 2x2 restriction
+template <int MODE, bool NORMS, int SPW>
+__global__ void __launch_bounds__(WS_NW * 32) k_ws_resid(
+    const __grid_constant__ Maps mp, float* __restrict__ r, double* __restrict__ partial,
+    unsigned* __restrict__ counter, double* __restrict__ norms, float* __restrict__ rcoarse,
+    int C, int H, int W, const int* __restrict__ active, size_t ps, size_t cps, int pf) {
+  pdl_enter();
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ uint64_t bars[WS_NW][SPW];
+  const int z = blockIdx.y, tile = z / C;
+  if (active && !active[tile]) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* sm = ws_smem(smraw) + (size_t)w * SPW * STAGE;
+  uint64_t* bar = bars[w];
+  const int nrc = (H + CR - 1) / CR;
+  const long nq = (long)((W + TC - 1) / TC) * nrc;
+  const int gwp = gridDim.x * WS_NW, gw = blockIdx.x * WS_NW + w;
+  long q0, q1;
+  ws_range(nq, gw, gwp, q0, q1);
+  const int n = (int)(q1 - q0);
+  if (lane == 0) {
+    for (int i = 0; i < SPW; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // chunks SPW.. SPW+pf-1 ahead of the ring are prefetched into L2 (more
+  // bytes in flight than the shared-memory ring holds)
+  auto prefetch = [&](int k) {
+    if (k >= n) return;
+    const long q = q0 + k;
+    const int tx = (int)(q / nrc), rc = (int)(q - (long)tx * nrc);
+    tma_prefetch_3d(&mp.u, tx * TC - 4, rc * CR - 1, z);
+    tma_prefetch_3d(&mp.b, tx * TC, rc * CR, z);
+  };
+  if (lane == 0) {
+    for (int k = 0; k < SPW && k < n; ++k) {
+      const long q = q0 + k;
+      const int tx = (int)(q / nrc), rc = (int)(q - (long)tx * nrc);
+      issue_chunk(mp, sm, bar, k, tx * TC, rc * CR, z, tile);
+    }
+    for (int k = SPW; k < SPW + pf; ++k) prefetch(k);
+  }
+  const size_t plane = ps;
+  const int cw = W / 2;
+  float sq = 0.0f;
+  for (int k = 0; k < n; ++k) {
+    const int st = k % SPW;
+    const long q = q0 + k;
+    const int tx = (int)(q / nrc), rc = (int)(q - (long)tx * nrc);
+    const int x0 = tx * TC, y0 = rc * CR, xq = x0 + 4 * lane;
+    mbar_wait(&bar[st], (uint32_t)((k / SPW) & 1));
+    const unsigned char* base = sm + st * STAGE;
+    const float* us = (const float*)(base + U_OFF) + 4 + 4 * lane;
+    const unsigned char* ms = base + M_OFF + 16 + 4 * lane;
+    const float* bs = (const float*)(base + B_OFF) + 4 * lane;
+    if (xq < W) {
+      // diagonal (numba_impl.py:80-95 counts each existing neighbour once;
+      // integer-valued, so order-free): interior rows, per lane pixel
+      float* const rrow0 = MODE == 0 ? r + (size_t)z * plane + (size_t)y0 * W + xq : nullptr;
+      double dmid[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dmid[i] = 2.0 + (xq + i > 0 ? 1.0 : 0.0) + (xq + i < W - 1 ? 1.0 : 0.0);
+      // rolling rows: a = row above, b = centre row, n = row below
+      double qa[4], qb[4];
+      float4 ub;
+      uint32_t mb;
+      {
+        const float4 u0 = *reinterpret_cast<const float4*>(us);
+        const uint32_t m0 = *reinterpret_cast<const uint32_t*>(ms);
+        ub = *reinterpret_cast<const float4*>(us + UW);
+        mb = *reinterpret_cast<const uint32_t*>(ms + MW);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          qa[i] = qmask(f4g(u0, i), m0, i);
+          qb[i] = qmask(f4g(ub, i), mb, i);
+        }
+      }
+      float4 rprev = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < CR; ++t) {
+        const int y = y0 + t;
+        const float4 un = *reinterpret_cast<const float4*>(us + (t + 2) * UW);
+        const uint32_t mn = *reinterpret_cast<const uint32_t*>(ms + (t + 2) * MW);
+        double qn[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qn[i] = qmask(f4g(un, i), mn, i);
+        float4 rr = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (y < H) {
+          const float* uc = us + (t + 1) * UW;
+          const unsigned char* mc = ms + (t + 1) * MW;
+          const double qL = (double)(mc[-1] ? 0.0f : uc[-1]);
+          const double qR = (double)(mc[4] ? 0.0f : uc[4]);
+          const float4 bb = *reinterpret_cast<const float4*>(bs + t * TC);
+          double a[4];
+          float o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double ql = i > 0 ? qb[i - 1] : qL;
+            const double qr = i < 3 ? qb[i + 1] : qR;
+            a[i] = ((qa[i] + qn[i]) + ql) + qr;
+            // d * u is exact (d <= 4, u a float), so the fused form rounds
+            // exactly like the reference's (d * u - acc); masked pixels are
+            // identity rows (branch-free select)
+            const float axu = (float)__fma_rn(dmid[i], qb[i], -a[i]);
+            const float ax = ((mb >> (8 * i)) & 0xFFu) ? f4g(ub, i) : axu;
+            o[i] = f4g(bb, i) - ax;
+          }
+          if (y == 0 || y == H - 1) {
+            // the image's first / last row: one vertical neighbour less
+            const double dtb = (y > 0 ? 0.0 : 1.0) + (y < H - 1 ? 0.0 : 1.0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float axu = (float)__fma_rn(dmid[i] - dtb, qb[i], -a[i]);
+              const float ax = ((mb >> (8 * i)) & 0xFFu) ? f4g(ub, i) : axu;
+              o[i] = f4g(bb, i) - ax;
+            }
+          }
+          rr = make_float4(o[0], o[1], o[2], o[3]);
+          if (MODE == 0) {
+            *reinterpret_cast<float4*>(rrow0 + (size_t)t * W) = rr;
+            if (NORMS) {
+              sq = __fmaf_rn(rr.x, rr.x, sq);
+              sq = __fmaf_rn(rr.y, rr.y, sq);
+              sq = __fmaf_rn(rr.z, rr.z, sq);
+              sq = __fmaf_rn(rr.w, rr.w, sq);
+            }
+          }
+        }
+        if (MODE == 1 && (t & 1)) {
+          // restrict_values (numba_impl.py:266-284): rows y-1, y -> coarse
+          // row (y-1)/2, ((a + b) + c) + d in double, a 1-row tail halves
+          const int ye = y - 1;
+          if (ye < H) {
+            float c0, c1;
+            if (y < H) {
+              c0 = (float)(((((double)rprev.x + (double)rprev.y) + (double)rr.x) + (double)rr.y) / 4.0);
+              c1 = (float)(((((double)rprev.z + (double)rprev.w) + (double)rr.z) + (double)rr.w) / 4.0);
+            } else {
+              c0 = (float)(((double)rprev.x + (double)rprev.y) / 2.0);
+              c1 = (float)(((double)rprev.z + (double)rprev.w) / 2.0);
+            }
+            *reinterpret_cast<float2*>(rcoarse + (size_t)z * cps + (size_t)(ye >> 1) * cw +
+                                       (xq >> 1)) = make_float2(c0, c1);
+          }
+        }
+        rprev = rr;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          qa[i] = qb[i];
+          qb[i] = qn[i];
+        }
+        ub = un;
+        mb = mn;
+      }
+    }
+    __syncwarp();  // every lane is done with stage st
+    if (lane == 0 && k + SPW < n) {
+      const long q2 = q + SPW;
+      const int tx2 = (int)(q2 / nrc), rc2 = (int)(q2 - (long)tx2 * nrc);
+      issue_chunk(mp, sm, bar, st, tx2 * TC, rc2 * CR, z, tile);
+      if (pf > 0) prefetch(k + SPW + pf);
+    }
+  }
+  if (MODE != 0 || !NORMS) return;
+  // deterministic norms: one double per warp (its fixed chunk range), the
+  // plane's last warp adds them in warp order
+  double d = (double)sq;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
+  unsigned last = 0;
+  if (lane == 0) {
+    partial[(size_t)z * gwp + gw] = d;
+    __threadfence();
+    last = atomicAdd(counter + z, 1u) == (unsigned)gwp - 1;
+  }
+  last = __shfl_sync(0xFFFFFFFFu, last, 0);
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = lane; i < gwp; i += 32) t += ((volatile double*)partial)[(size_t)z * gwp + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+  if (lane == 0) {
+    norms[z] = t;
+    counter[z] = 0u;
+  }
+}
+
+// prolongation + enforce, warp-streamed (the same stage layout and
+// arithmetic as k_prolong_tma): u = (ADD ? u : 0) + P e on unmasked pixels
+template <bool ADD, int SPW>
+__global__ void __launch_bounds__(WS_NW * 32) k_ws_prolong(
+    const __grid_constant__ PMaps mp, float* __restrict__ u, const float* __restrict__ b,
+    int C, int chh, int cww, int H, int W, const int* __restrict__ active, size_t ps, int pf) {
+  pdl_enter();
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ uint64_t bars[WS_NW][SPW];
+  const int z = blockIdx.y, tile = z / C;
+  if (active && !active[tile]) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* sm = ws_smem(smraw) + (size_t)w * SPW * PSTAGE;
+  uint64_t* bar = bars[w];
+  const int nrc = (H + CR - 1) / CR;
+  const long nq = (long)((W + TC - 1) / TC) * nrc;
+  const int gwp = gridDim.x * WS_NW, gw = blockIdx.x * WS_NW + w;
+  long q0, q1;
+  ws_range(nq, gw, gwp, q0, q1);
+  const int n = (int)(q1 - q0);
+  const uint32_t tx_bytes = (ADD ? PU_BYTES : 0) + PM_BYTES + PE_BYTES;
+  auto issue = [&](int st, long q) {
+    const int tx = (int)(q / nrc), rc = (int)(q - (long)tx * nrc);
+    const int x0 = tx * TC, yc = rc * CR;
+    unsigned char* base = sm + st * PSTAGE;
+    mbar_expect_tx(&bar[st], tx_bytes);
+    if (ADD) tma_load_3d(base + PU_OFF, &mp.u, x0, yc, z, &bar[st]);
+    tma_load_3d(base + PM_OFF, &mp.m, x0, yc, tile, &bar[st]);
+    tma_load_3d(base + PE_OFF, &mp.e, x0 / 2 - 4, yc / 2 - 1, z, &bar[st]);
+  };
+  if (lane == 0) {
+    for (int i = 0; i < SPW; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto prefetch = [&](int k) {
+    if (!ADD || k >= n) return;
+    const long q = q0 + k;
+    const int tx = (int)(q / nrc), rc = (int)(q - (long)tx * nrc);
+    tma_prefetch_3d(&mp.u, tx * TC, rc * CR, z);
+  };
+  if (lane == 0) {
+    for (int k = 0; k < SPW && k < n; ++k) issue(k, q0 + k);
+    for (int k = SPW; k < SPW + pf; ++k) prefetch(k);
+  }
+  const size_t plane = ps;
+  for (int k = 0; k < n; ++k) {
+    const int st = k % SPW;
+    const long q = q0 + k;
+    const int tx = (int)(q / nrc), rc = (int)(q - (long)tx * nrc);
+    const int x0 = tx * TC, yc = rc * CR, xq = x0 + 4 * lane;
+    mbar_wait(&bar[st], (uint32_t)((k / SPW) & 1));
+    const unsigned char* base = sm + st * PSTAGE;
+    if (xq < W) {
+      // x interpolation (numba_impl.py:333-344) of the lane's 4 pixels in
+      // closed form: coarse columns c-1 .. c+2 (c = xq/2), weights 1/4, 3/4;
+      // the left image edge clamps pixel 0 to (c, c+1) with weights (1, 0),
+      // the right edge clamps column c+2 to cww-1.  E columns are relative
+      // to the box origin x0/2 - 4.
+      const int c = xq >> 1, cb = c - (x0 / 2 - 4);
+      int ia[4], ib[4];
+      double wa[4], wb[4];
+      ia[0] = cb - 1; ib[0] = cb;     wa[0] = 0.25; wb[0] = 0.75;
+      ia[1] = cb;     ib[1] = cb + 1; wa[1] = 0.75; wb[1] = 0.25;
+      ia[2] = cb;     ib[2] = cb + 1; wa[2] = 0.25; wb[2] = 0.75;
+      ia[3] = cb + 1; ib[3] = c + 2 <= cww - 1 ? cb + 2 : cb + 1;
+      wa[3] = 0.75;   wb[3] = 0.25;
+      if (xq == 0) {
+        ia[0] = cb;
+        ib[0] = cww > 1 ? cb + 1 : cb;
+        wa[0] = 1.0;
+        wb[0] = 0.0;
+      }
+      const float* es = (const float*)(base + PE_OFF);
+      // one coarse row's x interpolations (exact products: the weights are
+      // 0, 1/4, 3/4 or 1 and E is float, so the fused form equals the
+      // reference's (1 - wx) * e0 + wx * e1)
+      auto hrow = [&](int l, double (&h)[4]) {
+        const float* e = es + l * EW;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          h[i] = __fma_rn(wb[i], (double)e[ib[i]], wa[i] * (double)e[ia[i]]);
+      };
+      const int yb0 = yc / 2 - 1;  // coarse row of local index 0
+      double hlo[4], hhi[4];
+      hrow(0, hlo);
+      hrow(1, hhi);
+      const uint32_t* mrow = (const uint32_t*)(base + PM_OFF) + lane;
+      const float4* urow = (const float4*)(base + PU_OFF) + lane;
+#pragma unroll
+      for (int t = 0; t < CR; ++t) {
+        if (t & 1) {
+          // generic rows: t -> coarse local rows ((t+1)/2, (t+1)/2 + 1)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) hlo[i] = hhi[i];
+          hrow((t + 1) / 2 + 1, hhi);
+        }
+        const int y = yc + t;
+        if (y >= H) break;
+        int ya, yb;
+        double wy;
+        paxis_d(y, chh, ya, yb, wy);
+        double ha[4], hb[4];
+        if (ya - yb0 == (t + 1) / 2 && yb == ya + 1) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            ha[i] = hlo[i];
+            hb[i] = hhi[i];
+          }
+        } else {  // clamped edge rows (y = 0, the last row)
+          hrow(ya - yb0, ha);
+          hrow(yb - yb0, hb);
+        }
+        const uint32_t mw = mrow[t * (TC / 4)];
+        const float4 uu = ADD ? urow[t * (TC / 4)] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float* dst = u + (size_t)z * plane + (size_t)y * W + xq;
+        // masked pixels: u == b~ there (V-cycle invariant, see k_prolong_tma)
+        // with ADD; the overwrite form reads b~
+        const float4 bb = ADD ? uu
+                              : (mw ? *reinterpret_cast<const float4*>(b + (size_t)z * plane +
+                                                                        (size_t)y * W + xq)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f));
+        float o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if ((mw >> (8 * i)) & 0xFFu) {
+            o[i] = f4g(bb, i);
+          } else {
+            const double v = (1.0 - wy) * ha[i] + wy * hb[i];
+            o[i] = ADD ? f4g(uu, i) + (float)v : (float)v;
+          }
+        }
+        *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && k + SPW < n) {
+      issue(st, q + SPW);
+      if (pf > 0) prefetch(k + SPW + pf);
+    }
+  }
+}
+
+// shared-memory stages per warp: 2 (default) or 1 (half the shared memory,
+// twice the resident warps), sp_ws_stages
+constexpr int ws_smem(int spw) { return WS_NW * spw * STAGE + 128; }
+constexpr int ws_psmem(int spw) { return WS_NW * spw * PSTAGE + 128; }
+
 }  // namespace
+
+// warp-streamed sweeps on/off (sp_ws_variant; A/B against the CTA-tile
+// kernels, which stay as the bandcol / strip-norm path)
+static int ws_on = 1;
+int ws_variant(int v) {
+  if (v >= 0) ws_on = v;
+  return ws_on;
+}
+
+// chunks each warp keeps prefetched into L2 ahead of its shared-memory ring
+// (sp_ws_prefetch)
+static int ws_pf = 0;  // measured slower at 1, 2, 4, 8 (profiles/ws_ab_r02u.txt)
+int ws_prefetch(int v) {
+  if (v >= 0) ws_pf = v;
+  return ws_pf;
+}
+
+// stages per warp (1 or 2) of launches made afterwards: the residual sweep
+// runs best with 2 stages (8 warps per SM), the restriction and the
+// prolongation with 1 (16 warps per SM): 57.5 / 51.4 / 47.4 us on the 4K RGB
+// finest level vs 61.8 / 62.0 / 48.3 with the other choice
+// (profiles/ws_ab_r02u.txt).  0 = these defaults.
+static int ws_spw = 0;
+int ws_stages(int v) {
+  if (v >= 0 && v <= 2) ws_spw = v;
+  return ws_spw;
+}
+static int spw_for(int kind) {  // 0 residual, 1 restriction, 2 prolongation
+  return ws_spw ? ws_spw : (kind == 0 ? 2 : 1);
+}
+
+// resident CTAs per SM of the warp-streamed kernels (set by tma_prepare),
+// [stages - 1]
+static int ws_occ_resid[2] = {1, 1}, ws_occ_prolong[2] = {1, 1};
+
+// CTAs per plane: fill the resident slots once (no tail wave), at most one
+// warp per chunk, and at most `cap` warps per plane (partial-sum slots)
+static unsigned ws_ctas(int occ, long nplanes, long nq, long cap) {
+  long slots = (long)num_sms() * occ;
+  long per = slots / (nplanes > 0 ? nplanes : 1);
+  long maxw = nq < cap ? nq : cap;
+  if (per * WS_NW > maxw) per = maxw / WS_NW;
+  if (per < 1) per = 1;
+  return (unsigned)per;
+}
+
+template <int SPW>
+static int ws_prepare() {
+  SP_CUDA(cudaFuncSetAttribute(k_ws_resid<0, true, SPW>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, ws_smem(SPW)));
+  SP_CUDA(cudaFuncSetAttribute(k_ws_resid<0, false, SPW>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, ws_smem(SPW)));
+  SP_CUDA(cudaFuncSetAttribute(k_ws_resid<1, false, SPW>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, ws_smem(SPW)));
+  SP_CUDA(cudaFuncSetAttribute(k_ws_prolong<true, SPW>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, ws_psmem(SPW)));
+  SP_CUDA(cudaFuncSetAttribute(k_ws_prolong<false, SPW>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, ws_psmem(SPW)));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &ws_occ_resid[SPW - 1], k_ws_resid<0, true, SPW>, WS_NW * 32, ws_smem(SPW)));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &ws_occ_prolong[SPW - 1], k_ws_prolong<true, SPW>, WS_NW * 32, ws_psmem(SPW)));
+  if (ws_occ_resid[SPW - 1] < 1) ws_occ_resid[SPW - 1] = 1;
+  if (ws_occ_prolong[SPW - 1] < 1) ws_occ_prolong[SPW - 1] = 1;
+  return 0;
+}
 
 // one-time kernel attributes (called at hierarchy / strip-group creation,
 // never inside a stream capture)
 int tma_prepare() {
   static bool done = false;
   if (done) return 0;
+  SP_TRY(ws_prepare<1>());
+  SP_TRY(ws_prepare<2>());
   SP_CUDA(cudaFuncSetAttribute(k_resid_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                SMEM));
   SP_CUDA(cudaFuncSetAttribute(k_resid_tma<0, false>,
@@ -478,12 +933,45 @@ bool tma_ok(int H, int W, size_t npart) {
   return (size_t)cdiv(W, TC) * cdiv(H, TR) <= npart;
 }
 
+// warp-streamed launch (k_ws_resid); npart: partial-sum slots per plane
+template <int MODE, bool NORMS>
+static int launch_ws(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
+                     unsigned* counter, double* norms, float* rc, int C, int H, int W,
+                     cudaStream_t s, int ntile, const int* active, size_t npart, size_t ps,
+                     size_t cps) {
+  if (!ps) ps = (size_t)H * W;
+  if (!cps) cps = (size_t)((H + 1) / 2) * (W / 2);
+  Maps mp;
+  if (!make_maps(mp, u, b, m, C, H, W, ntile, ps)) {
+    set_error("cuTensorMapEncodeTiled failed (%d x %d x %d)", C * ntile, H, W);
+    return -1;
+  }
+  const long nz = (long)C * ntile, nq = (long)cdiv(W, TC) * cdiv(H, CR);
+  const int spw = spw_for(MODE);
+  const unsigned per = ws_ctas(ws_occ_resid[spw - 1], nz, nq, NORMS ? (long)npart : (1L << 30));
+  dim3 grid(per, (unsigned)nz);
+  SP_CUDA(launch_k(spw == 1 ? k_ws_resid<MODE, NORMS, 1> : k_ws_resid<MODE, NORMS, 2>, grid,
+                   dim3(WS_NW * 32), ws_smem(spw), s, mp, r, partial, counter, norms, rc, C, H,
+                   W, active, ps, cps, ws_pf));
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+static bool ws_usable(size_t npart) { return ws_on && npart >= (size_t)WS_NW; }
+
 int resid_tma(const float* u, const float* b, const uint8_t* m, float* r, double* partial,
               unsigned* counter, double* norms, int C, int H, int W, cudaStream_t s, int ntile,
-              const int* active, double* bandcol, int band0, int nbt, size_t ps) {
+              const int* active, double* bandcol, int band0, int nbt, size_t ps, size_t npart) {
   if (bandcol)
     return launch<0, true>(u, b, m, r, partial, counter, nullptr, nullptr, C, H, W, s, ntile,
                            active, bandcol, band0, nbt, ps);
+  if (ws_usable(npart)) {
+    if (norms)
+      return launch_ws<0, true>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
+                                active, npart, ps, 0);
+    return launch_ws<0, false>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
+                               active, npart, ps, 0);
+  }
   if (norms)
     return launch<0, true>(u, b, m, r, partial, counter, norms, nullptr, C, H, W, s, ntile,
                            active);
@@ -505,6 +993,17 @@ int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int 
     return -1;
   }
   if (!add) mp.u = mp.m;  // unused
+  if (ws_on) {
+    const long nq = (long)cdiv(W, TC) * cdiv(H, CR);
+    const int spw = spw_for(2);
+    dim3 grid(ws_ctas(ws_occ_prolong[spw - 1], nz, nq, 1L << 30), (unsigned)nz);
+    auto kern = spw == 1 ? (add ? k_ws_prolong<true, 1> : k_ws_prolong<false, 1>)
+                         : (add ? k_ws_prolong<true, 2> : k_ws_prolong<false, 2>);
+    SP_CUDA(launch_k(kern, grid, dim3(WS_NW * 32), ws_psmem(spw), s, mp, u, b, C, chh, cww, H,
+                     W, active, ps, ws_pf));
+    SP_CHECK_LAUNCH();
+    return 0;
+  }
   dim3 grid(cdiv(W, TC), cdiv(H, TR), (unsigned)nz);
   SP_CUDA(launch_k(add ? k_prolong_tma<true> : k_prolong_tma<false>, grid, dim3(CR * 32), PSMEM,
                    s, mp, u, b, m, C, chh, cww, H, W, active, ps));
@@ -515,6 +1014,9 @@ int prolong_tma(const float* e, float* u, const float* b, const uint8_t* m, int 
 int resid_restrict_tma(const float* u, const float* b, const uint8_t* m, float* rc, int C,
                        int H, int W, cudaStream_t s, int ntile, const int* active, size_t ps,
                        size_t cps) {
+  if (ws_on)
+    return launch_ws<1, false>(u, b, m, nullptr, nullptr, nullptr, nullptr, rc, C, H, W, s,
+                               ntile, active, 0, ps, cps);
   return launch<1, false>(u, b, m, nullptr, nullptr, nullptr, nullptr, rc, C, H, W, s, ntile,
                           active, nullptr, 0, 0, ps, cps);
 }

@@ -250,7 +250,7 @@ static int residual_lv(Hier* h, int lv, bool with_norms, cudaStream_t s) {
   if (use_tma<T>(h, L))
     return resid_tma((const float*)L.u, (const float*)L.b, L.mask, (float*)L.r, L.partial,
                      L.counter, with_norms ? L.norms : nullptr, h->C, L.H, L.W, s, h->ntile,
-                     h->d_active);
+                     h->d_active, nullptr, 0, 0, 0, L.npart);
   if (use_march<T>(h, L))
     return resid_march((const float*)L.u, (const float*)L.b, L.mask, (float*)L.r, L.partial,
                        L.counter, with_norms ? L.norms : nullptr, h->C, L.H, L.W, s, h->ntile,

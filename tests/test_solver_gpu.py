@@ -74,22 +74,26 @@ def test_sweep_kernel_variants_agree(shape):
     f = O.synth(h, w, c, 3)
     mask = (np.random.default_rng(4).random((h, w)) < 0.05).astype(np.uint8)
     outs = []
-    prev = lib.sp_march_variant(-1)
+    prev, prev_ws = lib.sp_march_variant(-1), lib.sp_ws_variant(-1)
     try:
-        for mv in (2, 1, 0):
+        # (sweep variant, warp-streamed TMA kernels on/off)
+        for mv, ws in ((2, 1), (2, 0), (1, 1), (0, 1)):
             lib.sp_march_variant(mv)
+            lib.sp_ws_variant(ws)
             _POOL.clear()
             u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
             outs.append(u.data)
     finally:
         lib.sp_march_variant(prev)
+        lib.sp_ws_variant(prev_ws)
         _POOL.clear()
-    for o in outs[:2]:
-        rel = np.abs(o - outs[2]).max() / np.abs(outs[2]).max()
+    for o in outs[:3]:
+        rel = np.abs(o - outs[3]).max() / np.abs(outs[3]).max()
         assert rel <= 1e-6
 
 
-@pytest.mark.parametrize("shape", [(1, 128, 128), (1, 200, 256), (3, 130, 384), (3, 67, 512)])
+@pytest.mark.parametrize("shape", [(1, 128, 128), (1, 200, 256), (3, 130, 384), (3, 67, 512),
+                                   (1, 75, 272)])
 def test_sweep_kernel_residuals_bit_identical(shape):
     """The residual r = b~ - A~ u of one iterate computed by the TMA-staged,
     row-marching and per-pixel sweep kernels: bit-identical (numba_impl.py
@@ -106,11 +110,13 @@ def test_sweep_kernel_residuals_bit_identical(shape):
     mt = torch.from_numpy(mask).cuda()
     u0 = ft + torch.from_numpy(np.random.default_rng(8).standard_normal(f.shape)).float().cuda()
     bsym = _masked_rhs(ft, mt)
-    prev = lib.sp_march_variant(-1)
+    prev, prev_ws = lib.sp_march_variant(-1), lib.sp_ws_variant(-1)
     res = {}
     try:
-        for v in (0, 1, 2):
-            lib.sp_march_variant(v)
+        # 3: the CTA-tile TMA kernels (sweep 2 with the warp-streamed off)
+        for v in (0, 1, 2, 3):
+            lib.sp_march_variant(min(v, 2))
+            lib.sp_ws_variant(0 if v == 3 else 1)
             _POOL.clear()
             hier = GridHierarchy.build(sp.Mask(mt), sp.Image(ft), sp.MultigridConfig())
             hier.solve_sym(bsym, init=u0, tol=1e9)      # u = u0 (enforced), no cycle
@@ -120,8 +126,9 @@ def test_sweep_kernel_residuals_bit_identical(shape):
             res[v] = (r.cpu().numpy(), nrm.cpu().numpy())
     finally:
         lib.sp_march_variant(prev)
+        lib.sp_ws_variant(prev_ws)
         _POOL.clear()
-    for v in (1, 2):
+    for v in (1, 2, 3):
         assert np.array_equal(res[v][0], res[0][0])
         assert np.allclose(res[v][1], res[0][1], rtol=1e-6, atol=0)
 
@@ -258,3 +265,4 @@ def test_device_driven_solve_loop_identical(shape, tol):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[4], b[4])
     assert a[1:4] == b[1:4] and a[5:] == b[5:]
     assert b[5] == 2 and not b[6]
+
