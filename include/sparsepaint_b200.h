@@ -347,6 +347,10 @@ int sp_ws_prefetch(int v);
  * every sweep, 0 = the measured per-sweep defaults (residual 2, restriction
  * and prolongation 1); v < 0 queries.  Timing only, results unchanged. */
 int sp_ws_stages(int v);
+/* ORAS local-CG jobs read per-job row-mask words precomputed with the mask
+ * pyramid (1, default) or load and test their mask bytes (0); bit-identical.
+ * v < 0 queries.  A/B aid, no reference counterpart. */
+int sp_oras_offbits(int v);
 /* residual r = b~ - A~ u and per-plane sum r^2 of level lv's current iterate
  * (after a solve), computed by the hierarchy's sweep kernel, into device
  * buffers r_out [ntile][C][h][w], norms_out [ntile][C] (kernel-variant

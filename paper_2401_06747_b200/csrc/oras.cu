@@ -51,6 +51,14 @@ int oras_variant(int v) {
   return oras_kernel;
 }
 
+// the default kernel reads the precomputed per-job row-mask words (1) or
+// loads and tests the job's mask bytes itself (0); bit-identical
+static int offbits_on = 1;
+int oras_offbits(int v) {
+  if (v >= 0) offbits_on = v;
+  return offbits_on;
+}
+
 int oras_stats(int enable, unsigned long long* out) {
   if (out) SP_CUDA(cudaMemcpyFromSymbol(out, g_oras_stats, sizeof(unsigned long long) * 4));
   if (enable >= 0) {
@@ -497,7 +505,7 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
     float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps,
-    const int* __restrict__ wdelta) {
+    const int* __restrict__ wdelta, const uint32_t* __restrict__ offbits) {
   pdl_enter();
   // FULLH: a full 32 x 32 block (bh == bw == 32): compile-time row / column
   // offsets in the job's loads and stores
@@ -523,23 +531,35 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
 
   // ---- load the job (branch-free, clamped addresses; invalid zeroed)
   float res[R];
-  uint8_t mk[R];
-#pragma unroll
-  for (int s = 0; s < R; ++s) {
-    const int ic = FULLH ? s : min(s, bh - 1);
-    res[s] = rp[ic * W];
-    mk[s] = mp[ic * W];
-  }
   // off: bit s set where row s is masked or outside the block (q = 0 there,
   // and A p = p, which is 0 outside the block)
   uint32_t off = 0;
+  if (FAST && offbits) {
+    // the precomputed row-mask word of the lane's column (oras_offbits_launch)
+    off = offbits[((size_t)tile * nbl + bi) * 32 + j];
 #pragma unroll
-  for (int s = 0; s < R; ++s) {
-    const bool ok = (FULLH || s < bh) && lane_ok;
-    // FAST: the residual is 0 on masked pixels anyway (u = b~ there, so
-    // r = b~ - u = 0); zeroing it makes p = q exact for warp_cg32_fast
-    res[s] = (FAST ? ok && !mk[s] : ok) ? res[s] : 0.0f;
-    if (!ok || mk[s]) off |= 1u << s;
+    for (int s = 0; s < R; ++s) {
+      const int ic = FULLH ? s : min(s, bh - 1);
+      res[s] = rp[ic * W];
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) res[s] = ((off >> s) & 1u) ? 0.0f : res[s];
+  } else {
+    uint8_t mk[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int ic = FULLH ? s : min(s, bh - 1);
+      res[s] = rp[ic * W];
+      mk[s] = mp[ic * W];
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const bool ok = (FULLH || s < bh) && lane_ok;
+      // FAST: the residual is 0 on masked pixels anyway (u = b~ there, so
+      // r = b~ - u = 0); zeroing it makes p = q exact for warp_cg32_fast
+      res[s] = (FAST ? ok && !mk[s] : ok) ? res[s] : 0.0f;
+      if (!ok || mk[s]) off |= 1u << s;
+    }
   }
   // Robin-closed diagonal of the three row classes (k_oras_rows' float
   // addition order): top row, interior rows, bottom row
@@ -1022,7 +1042,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile, const int* active, int stride,
-                      int corr_nb, size_t ps, const int* wdelta) {
+                      int corr_nb, size_t ps, const int* wdelta, const uint32_t* offbits) {
   const int npx = bh * bw;
   if (ps && ps != (size_t)H * W &&
       !(sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
@@ -1056,12 +1076,12 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
       SP_CUDA(launch_k(kern, g4, dim3(wj * 32), 0, s, (const float*)r, m, tau_src, tau_scale, ys,
                        xs, nbx, nbl, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
                        (float)inv_h2, (const float*)weights, (float*)corr, active, corr_nb, ps,
-                       wdelta));
+                       wdelta, corr_nb > 0 || !offbits_on ? nullptr : offbits));
     } else {
       kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
                                   bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
                                   (const float*)weights, (float*)corr, active, corr_nb, ps,
-                                  wdelta);
+                                  wdelta, nullptr);
     }
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
@@ -1119,6 +1139,30 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   return 0;
 }
 
+// offbits[tile][b][j]: bit s = pixel (ys[ky] + s, xs[kx] + j) masked, or
+// row s / column j outside the bh x bw block -- the ORAS job's `off` word
+__global__ void k_offbits(const uint8_t* __restrict__ m, const int* __restrict__ ys,
+                          const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W,
+                          uint32_t* __restrict__ offbits) {
+  const int b = blockIdx.x, tile = blockIdx.y, j = threadIdx.x;
+  const int ky = b / nbx, kx = b - ky * nbx;
+  uint32_t off = 0xFFFFFFFFu;
+  if (j < bw) {
+    const uint8_t* mp = m + (size_t)tile * H * W + (size_t)ys[ky] * W + xs[kx] + j;
+    off = 0;
+    for (int s = 0; s < 32; ++s)
+      if (s >= bh || mp[(size_t)min(s, bh - 1) * W]) off |= 1u << s;
+  }
+  offbits[((size_t)tile * gridDim.x + b) * 32 + j] = off;
+}
+
+int oras_offbits_launch(const uint8_t* m, const int* ys, const int* xs, int nby, int nbx, int bh,
+                        int bw, int H, int W, int ntile, uint32_t* offbits, cudaStream_t s) {
+  k_offbits<<<dim3(nby * nbx, ntile), 32, 0, s>>>(m, ys, xs, nbx, bh, bw, H, W, offbits);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
 // wdelta[b] = cb - b when block b's weights equal block cb's bit for bit
 // (cb: the interior block (1, 1)), else 0
 __global__ void k_weight_alias(const float* __restrict__ w, int npx, int cb,
@@ -1160,7 +1204,8 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
   template int oras_local_launch<T>(const T*, const uint8_t*, const double*, double,        \
                                     const int*, const int*, int, int, int, int, int, int,   \
                                     int, double, long, double, const T*, T*, cudaStream_t,  \
-                                    int, const int*, int, int, size_t, const int*);         \
+                                    int, const int*, int, int, size_t, const int*,          \
+                                    const uint32_t*);                                       \
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
                                     int, int, int, cudaStream_t, int, const int*, int,      \

@@ -73,7 +73,7 @@ Hier::~Hier() {
     for (void* p : {(void*)L.mask, L.values, L.u, L.b, L.r, L.corr, L.weights, (void*)L.partial,
                     (void*)L.counter, (void*)L.norms, (void*)L.ys, (void*)L.xs,
                     (void*)L.row_k0, (void*)L.row_n, (void*)L.col_k0, (void*)L.col_n,
-                    (void*)L.wdelta})
+                    (void*)L.wdelta, (void*)L.offbits})
       if (p) cudaFree(p);
   }
   if (d_active) cudaFree(d_active);
@@ -147,6 +147,9 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     rc |= dalloc((void**)&L.col_n, sizeof(int) * ww);
     L.wdelta = nullptr;
     if (dtype != SP_F64) rc |= dalloc((void**)&L.wdelta, sizeof(int) * nb);
+    L.offbits = nullptr;
+    if (dtype != SP_F64 && L.bh <= 32 && L.bw <= 32)
+      rc |= dalloc((void**)&L.offbits, sizeof(uint32_t) * 32 * nb * ntile);
     h->lv.push_back(L);
     if (rc) { delete h; return -1; }
     Level& B = h->lv.back();
@@ -216,6 +219,10 @@ static int set_mask_t(Hier* h, const uint8_t* mask, const T* values, cudaStream_
     SP_TRY(restrict_mask<T>(F.mask, vals ? (const T*)F.values : nullptr, G.mask,
                             vals ? (T*)G.values : nullptr, h->C, F.H, F.W, s, h->ntile));
   }
+  for (Level& L : h->lv)
+    if (L.offbits)
+      SP_TRY(oras_offbits_launch(L.mask, L.ys, L.xs, L.nby, L.nbx, L.bh, L.bw, L.H, L.W,
+                                 h->ntile, L.offbits, s));
   h->has_values = vals;
   return 0;
 }
@@ -297,7 +304,7 @@ int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
                                 L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
                                 (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
                                 h->ntile, h->d_active, h->cfg.block - h->cfg.overlap, 0, 0,
-                                L.wdelta));
+                                L.wdelta, L.offbits));
     SP_TRY(oras_blend_launch<T>((T*)L.u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,
                                 L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
                                 s, h->ntile, h->d_active));
@@ -796,7 +803,10 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
         own = 1;
         for (int d : wd) own += d == 0;
       }
-      *bytes = (double)(es * C * nb * npx * nt * 2 + nb * npx * nt + es * own * npx);
+      // the job's row masks: one 32-bit word per column with offbits, else
+      // the mask bytes
+      const size_t mb = L.offbits && oras_offbits(-1) ? nb * 32 * 4 * nt : nb * npx * nt;
+      *bytes = (double)(es * C * nb * npx * nt * 2 + mb + es * own * npx);
       break;
     }
     case 2: *bytes = (double)(es * C * nb * npx * nt + 2 * es * vec); break;       // corr + u rw
@@ -817,7 +827,7 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
                                     L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
                                     (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
                                     h->ntile, h->d_active, h->cfg.block - h->cfg.overlap, 0, 0,
-                                    L.wdelta);
+                                    L.wdelta, L.offbits);
       case 2: {
         // blend into a scratch copy so the solver state is not disturbed
         return oras_blend_launch<T>((T*)L.r, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,

@@ -35,6 +35,10 @@ struct Level {
   double* norms;
   int *ys, *xs, *row_k0, *row_n, *col_k0, *col_n;
   int* wdelta;  // [nby * nbx] shared-weight aliases (float levels), or null
+  // [ntile][nby * nbx][32] ORAS job row masks (float levels, blocks <= 32 x
+  // 32): bit s of word j = row s of column j is masked or outside the block;
+  // rebuilt with the mask pyramid (set_mask_t), or null
+  uint32_t* offbits;
 };
 
 struct Hier {

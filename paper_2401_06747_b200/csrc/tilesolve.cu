@@ -469,7 +469,7 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
                                     L.nby, L.nbx, L.bh, L.bw, L.H, L.W, C, h->gamma,
                                     (long)L.bh * L.bw, 1.0, (const float*)L.weights,
                                     (float*)L.corr, s, nt, h->d_active, stride, 0, 0,
-                                    L.wdelta);
+                                    L.wdelta, L.offbits);
   };
   // V-cycles run in batches between reads of the live-block count: a block
   // that stops inside a batch is skipped by every later launch (each kernel

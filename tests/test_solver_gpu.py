@@ -167,6 +167,35 @@ def test_oras_warp_kernel_bit_identical(shape):
     assert np.array_equal(a, c)
 
 
+@pytest.mark.parametrize("shape", [(3, 301, 512), (1, 100, 150), (3, 40, 70)])
+def test_oras_offbits_bit_identical(shape):
+    """The default ORAS job reads its row-mask word precomputed with the mask
+    pyramid (k_offbits) instead of loading its 32 mask bytes: identical
+    V-cycles, on full and on short / narrow blocks, and in the batched RAS
+    block solves."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 3)
+    mask = (np.random.default_rng(4).random((h, w)) < 0.05).astype(np.uint8)
+    outs = []
+    prev = lib.sp_oras_offbits(-1)
+    try:
+        for v in (1, 0):
+            lib.sp_oras_offbits(v)
+            _POOL.clear()
+            u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
+            st = sp.ras_tonal(sp.Image(f), sp.Mask(mask))
+            outs.append((u.data, st.g.data, st.mse))
+    finally:
+        lib.sp_oras_offbits(prev)
+        _POOL.clear()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1]) and outs[0][2] == outs[1][2]
+
+
 def test_oras_warp_kernel_bit_identical_ras():
     """Batched-tile path (RAS local normal equations, ntile > 1)."""
     import paper_2401_06747_b200 as sp
