@@ -1141,24 +1141,33 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
 
 // offbits[tile][b][j]: bit s = pixel (ys[ky] + s, xs[kx] + j) masked, or
 // row s / column j outside the bh x bw block -- the ORAS job's `off` word
-__global__ void k_offbits(const uint8_t* __restrict__ m, const int* __restrict__ ys,
-                          const int* __restrict__ xs, int nbx, int bh, int bw, int H, int W,
-                          uint32_t* __restrict__ offbits) {
-  const int b = blockIdx.x, tile = blockIdx.y, j = threadIdx.x;
+__global__ void __launch_bounds__(256) k_offbits(const uint8_t* __restrict__ m,
+                                                 const int* __restrict__ ys,
+                                                 const int* __restrict__ xs, int nb, int nbx,
+                                                 int bh, int bw, int H, int W,
+                                                 uint32_t* __restrict__ offbits) {
+  // one warp per block, lane = column; the 32 row bytes are loaded first
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5), tile = blockIdx.y, j = threadIdx.x & 31;
+  if (b >= nb) return;
   const int ky = b / nbx, kx = b - ky * nbx;
   uint32_t off = 0xFFFFFFFFu;
   if (j < bw) {
     const uint8_t* mp = m + (size_t)tile * H * W + (size_t)ys[ky] * W + xs[kx] + j;
+    uint8_t mk[32];
+#pragma unroll
+    for (int s = 0; s < 32; ++s) mk[s] = mp[(size_t)min(s, bh - 1) * W];
     off = 0;
+#pragma unroll
     for (int s = 0; s < 32; ++s)
-      if (s >= bh || mp[(size_t)min(s, bh - 1) * W]) off |= 1u << s;
+      if (s >= bh || mk[s]) off |= 1u << s;
   }
-  offbits[((size_t)tile * gridDim.x + b) * 32 + j] = off;
+  offbits[((size_t)tile * nb + b) * 32 + j] = off;
 }
 
 int oras_offbits_launch(const uint8_t* m, const int* ys, const int* xs, int nby, int nbx, int bh,
                         int bw, int H, int W, int ntile, uint32_t* offbits, cudaStream_t s) {
-  k_offbits<<<dim3(nby * nbx, ntile), 32, 0, s>>>(m, ys, xs, nbx, bh, bw, H, W, offbits);
+  const int nb = nby * nbx;
+  k_offbits<<<dim3(cdiv(nb, 8), ntile), 256, 0, s>>>(m, ys, xs, nb, nbx, bh, bw, H, W, offbits);
   SP_CHECK_LAUNCH();
   return 0;
 }

@@ -67,13 +67,34 @@ def rep(tag, path):
         print("no data in", path)
         return
     h, units, vals = rows[0], rows[1], rows[2:]
-    name = vals[0][h.index("Kernel Name")].split("(")[0].replace("void ", "")
+    # several launches in one report: summarise the longest (the finest
+    # level), list the others
+    ti = h.index("gpu__time_duration.sum")
+    num = lambda x: float(x.replace(",", "")) if x else 0.0
+    best = max(range(len(vals)), key=lambda r: num(vals[r][ti]))
+    row = vals[best]
+    name = row[h.index("Kernel Name")].split("(")[0].replace("void ", "")
     lines = [f"# ncu --set full --clock-control none: {os.path.basename(path)}",
-             f"# kernel: {name}", ""]
+             f"# kernel: {name}" + (f" (longest of {len(vals)} launches)" if len(vals) > 1 else ""),
+             ""]
     for k in KEYS:
         if k in h:
             i = h.index(k)
-            lines.append(f"{k:60s} {vals[0][i]:>18s} {units[i]}")
+            lines.append(f"{k:60s} {row[i]:>18s} {units[i]}")
+    stalls = sorted(((num(row[i]), k) for i, k in enumerate(h)
+                     if k.startswith("smsp__pcsamp_warps_issue_stalled_")
+                     and not k.endswith("not_issued")), reverse=True)
+    tot = sum(v for v, _ in stalls) or 1.0
+    if stalls:
+        lines += ["", "# warp-state samples (top 6)"]
+        for v, k in stalls[:6]:
+            lines.append(f"{k.replace('smsp__pcsamp_warps_issue_stalled_', 'stall_'):60s} "
+                         f"{v / tot:17.1%}")
+    if len(vals) > 1:
+        gi = h.index("launch__grid_size") if "launch__grid_size" in h else None
+        lines += ["", "# all launches: grid, us"]
+        for r in vals:
+            lines.append(f"  {r[gi] if gi is not None else '':>8s} {num(r[ti]):10.2f}")
     short = name.split("::")[-1].split("<")[0]
     dst = os.path.join(OUT, f"ncu_{tag}_{short}.txt")
     open(dst, "w").write("\n".join(lines) + "\n")
