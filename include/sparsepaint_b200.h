@@ -229,6 +229,25 @@ int sp_geo_select(void* geo, uint8_t* mask, long nbuckets, long want, long* pick
 /* spatial.py:189-197 */
 int sp_geo_fill_highest_error(void* geo, const double* err, uint8_t* mask, long want,
                               void* stream);
+/* Row-strip partition of the Delaunay step and the accumulate (SURVEY.md
+ * section 8e; every rank holds the full labels -- jump flooding stays
+ * replicated).  Replaces, across P ranks, sp_geo_delaunay + sp_geo_accumulate
+ * (geometry.py:113-223) with bit-identical triangles and buckets:
+ *   corner keys of rows [r0, r1) -> all-gather -> sp_geo_delaunay_from_keys;
+ *   sp_geo_raster_rows(own rows) -> all-gather the assignment rows
+ *   (sp_geo_assign_rows) -> sp_geo_reduce_range(own triangle range) ->
+ *   all-gather the bucket ranges (sp_geo_set_buckets).
+ * A triangle's sequential f64 sum is never split across ranks. */
+int sp_geo_corner_keys(void* geo, int r0, int r1, long* nkeys, void* stream);
+int sp_geo_keys_copy(void* geo, uint64_t* dst, long n, void* stream);
+int sp_geo_delaunay_from_keys(void* geo, const uint64_t* keys, long n, long* ntris,
+                              void* stream);
+int sp_geo_raster_rows(void* geo, int r0, int r1, void* stream);
+/* dir 0: rows [r0, r1) of the assignment to buf; dir 1: from buf */
+int sp_geo_assign_rows(void* geo, int32_t* buf, int r0, int r1, int dir, void* stream);
+int sp_geo_reduce_range(void* geo, const double* err, long t0, long t1, void* stream);
+int sp_geo_set_buckets(void* geo, const double* sums, const int64_t* amax,
+                       const double* amax_val, long t0, long t1, void* stream);
 /* load caller labels (H,W) i32 + seed rows sy/sx (m) i32 into the workspace */
 int sp_geo_load(void* geo, const int32_t* labels, const int32_t* sy, const int32_t* sx,
                 long m, void* stream);

@@ -69,6 +69,13 @@ _SIGS = {
     "sp_geo_voronoi": [P, P, c_double, P, P, P, P],
     "sp_geo_delaunay": [P, P, P],
     "sp_geo_accumulate": [P, P, c_int, P],
+    "sp_geo_corner_keys": [P, c_int, c_int, P, P],
+    "sp_geo_keys_copy": [P, P, c_long, P],
+    "sp_geo_delaunay_from_keys": [P, P, c_long, P, P],
+    "sp_geo_raster_rows": [P, c_int, c_int, P],
+    "sp_geo_assign_rows": [P, P, c_int, c_int, c_int, P],
+    "sp_geo_reduce_range": [P, P, c_long, c_long, P],
+    "sp_geo_set_buckets": [P, P, P, P, c_long, c_long, P],
     "sp_geo_accumulate_mode": [c_int],
     "sp_pdl_from_level": [c_int],
     "sp_geo_select": [P, P, c_long, c_long, P, P],

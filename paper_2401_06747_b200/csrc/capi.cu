@@ -446,6 +446,69 @@ int sp_geo_load(void* gp, const int32_t* labels, const int32_t* sy, const int32_
   return 0;
 }
 
+// ---- row-strip partition of the Delaunay step and the accumulate ------------
+// (geometry.cu geo_corner_keys ...).  Row ranges are
+// image rows [r0, r1); triangle ranges [t0, t1).
+
+// sorted unique triangle keys of the corners in rows [r0, r1) (left in the
+// workspace; sp_geo_keys_copy reads them out)
+int sp_geo_corner_keys(void* g, int r0, int r1, long* nkeys, void* s) {
+  return geo_corner_keys((Geo*)g, r0, r1, nkeys, STREAM(s));
+}
+
+int sp_geo_keys_copy(void* gp, uint64_t* dst, long n, void* s) {
+  Geo* g = (Geo*)gp;
+  if (n < 0 || (size_t)n > g->key_cap) { set_error("bad key count %ld", n); return -2; }
+  if (n) SP_CUDA(cudaMemcpyAsync(dst, g->keys, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice,
+                                 STREAM(s)));
+  return 0;
+}
+
+// the triangles of the merged (concatenated) key lists of all strips
+int sp_geo_delaunay_from_keys(void* g, const uint64_t* keys, long n, long* ntris, void* s) {
+  return geo_delaunay_from_keys((Geo*)g, (const unsigned long long*)keys, n, ntris, STREAM(s));
+}
+
+// pixel -> triangle assignment of rows [r0, r1) only
+int sp_geo_raster_rows(void* g, int r0, int r1, void* s) {
+  return geo_raster_rows((Geo*)g, r0, r1, STREAM(s));
+}
+
+// assignment rows [r0, r1) to (dir 0) or from (dir 1) buf, int32 [r1-r0][W]
+int sp_geo_assign_rows(void* gp, int32_t* buf, int r0, int r1, int dir, void* s) {
+  Geo* g = (Geo*)gp;
+  if (r0 < 0 || r1 > g->H || r1 < r0) { set_error("bad row range [%d, %d)", r0, r1); return -2; }
+  const size_t off = (size_t)r0 * g->W, n = (size_t)(r1 - r0) * g->W;
+  if (!n) return 0;
+  if (dir == 0)
+    SP_CUDA(cudaMemcpyAsync(buf, g->assign + off, sizeof(int) * n, cudaMemcpyDeviceToDevice,
+                            STREAM(s)));
+  else
+    SP_CUDA(cudaMemcpyAsync(g->assign + off, buf, sizeof(int) * n, cudaMemcpyDeviceToDevice,
+                            STREAM(s)));
+  return 0;
+}
+
+// per-triangle sums / argmax of triangles [t0, t1) over the full assignment
+int sp_geo_reduce_range(void* g, const double* err, long t0, long t1, void* s) {
+  return geo_reduce_range((Geo*)g, err, t0, t1, STREAM(s));
+}
+
+// install bucket results [t0, t1) (the all-gathered ranges) for sp_geo_select
+int sp_geo_set_buckets(void* gp, const double* sums, const int64_t* amax,
+                       const double* amax_val, long t0, long t1, void* s) {
+  Geo* g = (Geo*)gp;
+  if (t0 < 0 || t1 < t0 || (size_t)t1 > g->tri_cap) { set_error("bad bucket range"); return -2; }
+  const size_t n = (size_t)(t1 - t0);
+  if (!n) return 0;
+  cudaStream_t st = STREAM(s);
+  SP_CUDA(cudaMemcpyAsync(g->sums + t0, sums, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  SP_CUDA(cudaMemcpyAsync(g->amax + t0, amax, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+  SP_CUDA(cudaMemcpyAsync(g->amax_val + t0, amax_val, sizeof(double) * n,
+                          cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
 // copies of the workspace state for the public API objects (any pointer may
 // be NULL): labels (H,W) i32, seed rows sy/sx (m) i32, triangles (T,3) i32,
 // bucket sums / argmax / argmax value (T, or m for the Voronoi partition)

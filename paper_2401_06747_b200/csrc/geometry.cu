@@ -267,13 +267,15 @@ __device__ __forceinline__ void sort3(unsigned& a, unsigned& b, unsigned& c) {
   if (a > b) { t = a; a = b; b = t; }
 }
 
+// corner rows [y0c, y1c) (a corner row y reads label rows y and y + 1; the
+// whole image is y0c = 0, y1c = H - 1)
 __global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
                               unsigned long long* __restrict__ keys,
-                              unsigned long long* __restrict__ nkeys) {
-  int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
+                              unsigned long long* __restrict__ nkeys, int y0c, int y1c) {
+  int x = blockIdx.x * BX + threadIdx.x, y = y0c + blockIdx.y * BY + threadIdx.y;
   unsigned long long k0 = 0, k1 = 0;
   int nk = 0;
-  if (x < W - 1 && y < H - 1) {
+  if (x < W - 1 && y < y1c) {
     size_t p = (size_t)y * W + x;
     int tl = lab[p], tr = lab[p + 1], bl = lab[p + W], br = lab[p + W + 1];
     int s0 = tl, s1 = tr, s2 = bl, s3 = br, t;
@@ -553,16 +555,19 @@ __device__ __forceinline__ void tri_span(int y, const int4& v, const int2& c, in
   x1 = min(h, hi);
 }
 
+// tiles tile0 + blockIdx.x; only image rows [r0, r1) are rasterised and
+// written (a row strip; the whole image is 0, H); fb == NULL: no fallback
+// list (the strip path collects it from the gathered assignment)
 __global__ void __launch_bounds__(256) k_raster_tiles(
     const unsigned* __restrict__ off, const unsigned* __restrict__ cnt,
     const int* __restrict__ list, const int4* __restrict__ tv, const int2* __restrict__ tc,
     const int4* __restrict__ tbox, const int* __restrict__ lab, const int* __restrict__ smt,
     int H, int W, int ntx, int* __restrict__ assign, unsigned long long* __restrict__ fb,
-    unsigned long long* __restrict__ nfb) {
+    unsigned long long* __restrict__ nfb, int tile0, int r0, int r1) {
   __shared__ int best[RTN];
   __shared__ unsigned wcount[8];
   __shared__ unsigned long long cbase;
-  const int tile = blockIdx.x, ty0 = (tile / ntx) * RTH, tx0 = (tile % ntx) * RTW;
+  const int tile = tile0 + blockIdx.x, ty0 = (tile / ntx) * RTH, tx0 = (tile % ntx) * RTW;
   for (int i = threadIdx.x; i < RTN; i += 256) best[i] = INT_MAX;
   __syncthreads();
   // 4 lanes per triangle, 8 triangles per warp in flight.  Rows of the
@@ -580,7 +585,7 @@ __global__ void __launch_bounds__(256) k_raster_tiles(
     const int4 v = tv[t];
     const int2 c = tc[t];
     const int4 box = tbox[t];
-    int ylo = max(box.x, ty0), yhi = min(box.z, ty0 + RTH - 1);
+    int ylo = max(max(box.x, ty0), r0), yhi = min(min(box.z, ty0 + RTH - 1), r1 - 1);
     if (by_row) {
       const int yr = ty0 + (int)(item % RTH);
       if (yr < ylo || yr > yhi) continue;
@@ -615,7 +620,7 @@ __global__ void __launch_bounds__(256) k_raster_tiles(
     bool isfb = false;
     int t = 0;
     size_t p = 0;
-    if (y < H && x < W) {
+    if (y < H && x < W && y >= r0 && y < r1) {
       p = (size_t)y * W + x;
       t = best[i];
       if (t == INT_MAX) {
@@ -627,6 +632,7 @@ __global__ void __launch_bounds__(256) k_raster_tiles(
         assign[p] = t;
       }
     }
+    if (!fb) continue;  // uniform: no fallback list
     // CTA-aggregated append of the fallback pixels
     const unsigned bal = __ballot_sync(0xFFFFFFFFu, isfb);
     if (lane == 0) wcount[w] = __popc(bal);
@@ -665,8 +671,9 @@ __global__ void __launch_bounds__(128) k_reduce_tris_small(
     const int4* __restrict__ tbox, long T, const int* __restrict__ assign,
     const double* __restrict__ err, int W, const unsigned long long* __restrict__ fb,
     const int* __restrict__ fs, const int* __restrict__ fe, double* __restrict__ sums,
-    long long* __restrict__ amax_idx, double* __restrict__ amax_val) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long* __restrict__ amax_idx, double* __restrict__ amax_val, long t0) {
+  // triangles [t0, T)
+  const long t = t0 + (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const int4 box = tbox[t];
   int fi = fs[t];
@@ -722,7 +729,8 @@ __global__ void __launch_bounds__(256) k_reduce_tris(
     long T, const int* __restrict__ assign, const double* __restrict__ err, int W,
     const unsigned long long* __restrict__ fb, const int* __restrict__ fs,
     const int* __restrict__ fe, double* __restrict__ sums, long long* __restrict__ amax_idx,
-    double* __restrict__ amax_val, unsigned* __restrict__ next) {
+    double* __restrict__ amax_val, unsigned* __restrict__ next, long t0) {
+  // triangles [t0, T)
   constexpr int RB = 4;  // rows per batch
   __shared__ double vals[8][RB * 32];
   __shared__ double fv[8][32];
@@ -733,7 +741,7 @@ __global__ void __launch_bounds__(256) k_reduce_tris(
   while (true) {
     unsigned tt = 0;
     if (lane == 0) tt = atomicAdd(next, 1u);
-    const long t = (long)__shfl_sync(0xFFFFFFFFu, tt, 0);
+    const long t = t0 + (long)__shfl_sync(0xFFFFFFFFu, tt, 0);
     if (t >= T) break;
     const int4 box = tbox[t];
     const int4 v = tv[t];
@@ -1165,6 +1173,8 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
   return 0;
 }
 
+static int sort_unique_keys(Geo* g, long nk, long* n_out, bool decode, cudaStream_t s);
+
 int geo_delaunay(Geo* g, long* T_out, cudaStream_t s) {
   const int H = g->H, W = g->W;
   g->T = 0;
@@ -1175,13 +1185,25 @@ int geo_delaunay(Geo* g, long* T_out, cudaStream_t s) {
     return -2;
   }
   SP_CUDA(cudaMemsetAsync(g->nkeys, 0, sizeof(unsigned long long) * 2, s));
-  k_corner_scan<<<grid2(W, H), dim3(BX, BY), 0, s>>>(g->lab_a, H, W, g->keys, g->nkeys);
+  k_corner_scan<<<grid2(W, H), dim3(BX, BY), 0, s>>>(g->lab_a, H, W, g->keys, g->nkeys, 0,
+                                                     H - 1);
   SP_CHECK_LAUNCH();
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   long nk = (long)((unsigned long long*)g->h_small)[0];
   if (nk == 0) return 0;
-  // sort + unique (np.unique(axis=0) on sorted triples == sorted packed keys)
+  long T = 0;
+  SP_TRY(sort_unique_keys(g, nk, &T, true, s));
+  g->T = T;
+  *T_out = T;
+  return 0;
+}
+
+// sort + unique of g->keys[0, nk) in place (np.unique(axis=0) on sorted
+// triples == sorted packed keys); decode: the triangles of the unique keys
+static int sort_unique_keys(Geo* g, long nk, long* n_out, bool decode, cudaStream_t s) {
+  *n_out = 0;
+  if (nk == 0) return 0;
   int nbits = bits_for(g->m - 1);
   int endbit = 42 + nbits;
   size_t sort_bytes = 0, uniq_bytes = 0;
@@ -1198,10 +1220,11 @@ int geo_delaunay(Geo* g, long* T_out, cudaStream_t s) {
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   long T = ((int*)g->h_small)[0];
-  k_decode_tris<<<cdiv(T, 256), 256, 0, s>>>(g->keys, T, g->tris);
-  SP_CHECK_LAUNCH();
-  g->T = T;
-  *T_out = T;
+  if (decode) {
+    k_decode_tris<<<cdiv(T, 256), 256, 0, s>>>(g->keys, T, g->tris);
+    SP_CHECK_LAUNCH();
+  }
+  *n_out = T;
   return 0;
 }
 
@@ -1248,7 +1271,8 @@ static int accumulate_tiled(Geo* g, const double* err, cudaStream_t s) {
   unsigned long long* fbk = (unsigned long long*)g->keys;  // n <= key_cap scratch keys
   SP_CUDA(cudaMemsetAsync(g->nkeys + 2, 0, sizeof(unsigned long long), s));
   k_raster_tiles<<<ntile, 256, 0, s>>>(off, cnt, (const int*)lst.p, tv, tc, tbox, g->lab_a,
-                                       g->smt, H, W, ntx, g->assign, fbk, g->nkeys + 2);
+                                       g->smt, H, W, ntx, g->assign, fbk, g->nkeys + 2, 0, 0,
+                                       H);
   SP_CHECK_LAUNCH();
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys + 2, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s));
@@ -1277,13 +1301,216 @@ static int accumulate_tiled(Geo* g, const double* err, cudaStream_t s) {
   if ((double)T * 128.0 >= (double)n) {
     // dense: boxes of a few dozen pixels, one thread per triangle
     k_reduce_tris_small<<<cdiv(T, 128), 128, 0, s>>>(tbox, T, g->assign, err, W, fsorted, fs,
-                                                     fe, g->sums, g->amax, g->amax_val);
+                                                     fe, g->sums, g->amax, g->amax_val, 0);
   } else {
     const long rblocks = std::min<long>(cdiv(T, 8), (long)num_sms() * 4);
     SP_CUDA(cudaMemsetAsync(g->nkeys + 3, 0, sizeof(unsigned long long), s));
     k_reduce_tris<<<rblocks, 256, 0, s>>>(tv, tc, tbox, T, g->assign, err, W, fsorted, fs, fe,
                                           g->sums, g->amax, g->amax_val,
-                                          (unsigned*)(g->nkeys + 3));
+                                          (unsigned*)(g->nkeys + 3), 0);
+  }
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---- row-strip partition of the Delaunay step and the accumulate (SURVEY.md
+// section 8e): every rank holds the full labels (jump flooding stays
+// replicated: each pass reads the whole previous field) and
+//   1. scans the corners of its own rows, sort + unique locally
+//      (geo_corner_keys); the ranks' key lists are all-gathered and merged
+//      by one more sort + unique (geo_delaunay_from_keys) -- the union of
+//      the corner triples in sorted order, the same triangle list and
+//      indices as the unpartitioned scan;
+//   2. rasterises its own rows (geo_raster_rows); the assignment rows are
+//      all-gathered, so every rank holds the full pixel -> triangle map;
+//   3. reduces a contiguous range of triangles over the FULL map, each in
+//      the reference's sequential row-major order (geo_reduce_range); the
+//      (sum, argmax) ranges are all-gathered.  A triangle's sum is never
+//      split across ranks, so the f64 rounding is the unpartitioned one.
+
+int geo_corner_keys(Geo* g, int r0, int r1, long* n_out, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  *n_out = 0;
+  g->T = 0;
+  if (H < 2 || W < 2 || g->m < 3) return 0;
+  if (g->m >= (1L << 21)) {
+    set_error("more than 2^21 stored pixels: triangle keys would overflow");
+    return -2;
+  }
+  const int y0c = std::max(0, r0), y1c = std::min(r1, H - 1);
+  SP_CUDA(cudaMemsetAsync(g->nkeys, 0, sizeof(unsigned long long) * 2, s));
+  if (y1c > y0c) {
+    k_corner_scan<<<dim3(cdiv(W, BX), cdiv(y1c - y0c, BY)), dim3(BX, BY), 0, s>>>(
+        g->lab_a, H, W, g->keys, g->nkeys, y0c, y1c);
+    SP_CHECK_LAUNCH();
+  }
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const long nk = (long)((unsigned long long*)g->h_small)[0];
+  return sort_unique_keys(g, nk, n_out, false, s);
+}
+
+int geo_delaunay_from_keys(Geo* g, const unsigned long long* keys, long n, long* T_out,
+                           cudaStream_t s) {
+  *T_out = 0;
+  g->T = 0;
+  if ((size_t)n > g->key_cap) {
+    set_error("%ld keys exceed the workspace's %zu", n, g->key_cap);
+    return -2;
+  }
+  if (n == 0) return 0;
+  if (keys != g->keys)
+    SP_CUDA(cudaMemcpyAsync(g->keys, keys, sizeof(unsigned long long) * n,
+                            cudaMemcpyDeviceToDevice, s));
+  long T = 0;
+  SP_TRY(sort_unique_keys(g, n, &T, true, s));
+  g->T = T;
+  *T_out = T;
+  return 0;
+}
+
+// the triangles' vertices / boxes (k_bin_count) and their per-tile lists
+struct TriBins {
+  int4* tv;
+  int4* tbox;
+  int2* tc;
+  unsigned *cnt, *off, *fill;
+  int* list;
+  int ntx, ntile;
+};
+
+static int bin_triangles(Geo* g, Scratch& scr, Scratch& lst, TriBins& b, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  const long T = g->T;
+  b.ntx = cdiv(W, RTW);
+  b.ntile = b.ntx * cdiv(H, RTH);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const unsigned*)nullptr,
+                                (unsigned*)nullptr, b.ntile, s);
+  const size_t tb = sizeof(int4) * 2 * (size_t)T + sizeof(int2) * (size_t)T;
+  const size_t ub = sizeof(unsigned) * 3 * (size_t)b.ntile + 64;
+  SP_TRY(scr.alloc(tb + ub + scan_bytes + 256));
+  b.tv = (int4*)scr.p;
+  b.tbox = b.tv + T;
+  b.tc = (int2*)(b.tbox + T);
+  b.cnt = (unsigned*)(b.tc + T);
+  b.off = b.cnt + b.ntile;
+  b.fill = b.off + b.ntile;
+  void* scan_tmp = (void*)(((uintptr_t)(b.fill + b.ntile) + 255) & ~(uintptr_t)255);
+  SP_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(unsigned) * b.ntile, s));
+  SP_CUDA(cudaMemsetAsync(b.fill, 0, sizeof(unsigned) * b.ntile, s));
+  k_bin_count<<<cdiv(T, 256), 256, 0, s>>>(g->tris, T, g->sy, g->sx, H, W, b.ntx, b.tv, b.tc,
+                                           b.tbox, b.cnt);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, b.cnt, b.off, b.ntile, s));
+  unsigned* hs = (unsigned*)g->h_small;
+  SP_CUDA(cudaMemcpyAsync(hs, b.off + b.ntile - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(hs + 1, b.cnt + b.ntile - 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const size_t nlist = (size_t)hs[0] + hs[1];
+  SP_TRY(lst.alloc(sizeof(int) * (nlist + 1)));
+  b.list = (int*)lst.p;
+  k_bin_scatter<<<cdiv(T, 256), 256, 0, s>>>(b.tbox, T, b.ntx, b.off, b.fill, b.list);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+static bool strip_geometry_ok(const Geo* g) {
+  const size_t n = (size_t)g->H * g->W;
+  return g->H < 32768 && g->W < 32768 && n < (1ull << 32) && n <= g->key_cap;
+}
+
+int geo_raster_rows(Geo* g, int r0, int r1, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  if (!strip_geometry_ok(g)) {
+    set_error("strip geometry needs < 2^15 pixels per side");
+    return -2;
+  }
+  r0 = std::max(0, r0);
+  r1 = std::min(H, r1);
+  if (g->T == 0 || r1 <= r0) return 0;
+  Scratch scr(s), lst(s);
+  TriBins b;
+  SP_TRY(bin_triangles(g, scr, lst, b, s));
+  SP_TRY(seed_min_tri<int>(g->tris, g->T, g->smt, g->m, s));
+  const int ty0 = r0 / RTH, ty1 = (r1 - 1) / RTH;
+  k_raster_tiles<<<(ty1 - ty0 + 1) * b.ntx, 256, 0, s>>>(
+      b.off, b.cnt, b.list, b.tv, b.tc, b.tbox, g->lab_a, g->smt, H, W, b.ntx, g->assign,
+      nullptr, nullptr, ty0 * b.ntx, r0, r1);
+  SP_CHECK_LAUNCH();
+  return 0;
+}
+
+// fallback pixels (assignment high bit) of the full map, (triangle, pixel) keys
+__global__ void k_fb_collect(const int* __restrict__ assign, size_t n,
+                             unsigned long long* __restrict__ fb,
+                             unsigned long long* __restrict__ nfb) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int a = p < n ? assign[p] : 0;
+  const bool isfb = p < n && (a & 0x80000000);
+  const unsigned bal = __ballot_sync(0xFFFFFFFFu, isfb);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(nfb, (unsigned long long)__popc(bal));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (isfb)
+    fb[base + __popc(bal & ((1u << lane) - 1u))] =
+        ((unsigned long long)((unsigned)a & 0x7FFFFFFFu) << 32) | (unsigned long long)p;
+}
+
+int geo_reduce_range(Geo* g, const double* err, long t0, long t1, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  const long T = g->T;
+  const size_t n = (size_t)H * W;
+  if (!strip_geometry_ok(g)) {
+    set_error("strip geometry needs < 2^15 pixels per side");
+    return -2;
+  }
+  t0 = std::max(0L, t0);
+  t1 = std::min(T, t1);
+  if (T == 0 || t1 <= t0) return 0;
+  Scratch scr(s), lst(s);
+  TriBins b;
+  SP_TRY(bin_triangles(g, scr, lst, b, s));
+  unsigned long long* fbk = (unsigned long long*)g->keys;  // n <= key_cap scratch keys
+  SP_CUDA(cudaMemsetAsync(g->nkeys + 2, 0, sizeof(unsigned long long), s));
+  k_fb_collect<<<cdiv(n, 256), 256, 0, s>>>(g->assign, n, fbk, g->nkeys + 2);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys + 2, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const long nfb = (long)((unsigned long long*)g->h_small)[0];
+  Scratch fbs(s);
+  size_t sort_bytes = 0;
+  if (nfb > 0)
+    cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                   (unsigned long long*)nullptr, (int)nfb, 0,
+                                   32 + bits_for(T), s);
+  SP_TRY(fbs.alloc(sizeof(unsigned long long) * (nfb + 1) + sizeof(int) * 2 * (size_t)T +
+                   sort_bytes + 512));
+  unsigned long long* fsorted = (unsigned long long*)fbs.p;
+  int* fs = (int*)(fsorted + nfb + 1);
+  int* fe = fs + T;
+  void* sort_tmp = (void*)(((uintptr_t)(fe + T) + 255) & ~(uintptr_t)255);
+  SP_CUDA(cudaMemsetAsync(fs, 0, sizeof(int) * 2 * (size_t)T, s));
+  if (nfb > 0) {
+    SP_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp, sort_bytes, fbk, fsorted, (int)nfb, 0,
+                                           32 + bits_for(T), s));
+    k_fb_bounds<<<cdiv(nfb, 256), 256, 0, s>>>(fsorted, nfb, fs, fe);
+    SP_CHECK_LAUNCH();
+  }
+  const long nt = t1 - t0;
+  if ((double)T * 128.0 >= (double)n) {
+    k_reduce_tris_small<<<cdiv(nt, 128), 128, 0, s>>>(b.tbox, t1, g->assign, err, W, fsorted,
+                                                      fs, fe, g->sums, g->amax, g->amax_val,
+                                                      t0);
+  } else {
+    const long rblocks = std::min<long>(cdiv(nt, 8), (long)num_sms() * 4);
+    SP_CUDA(cudaMemsetAsync(g->nkeys + 3, 0, sizeof(unsigned long long), s));
+    k_reduce_tris<<<rblocks, 256, 0, s>>>(b.tv, b.tc, b.tbox, t1, g->assign, err, W, fsorted,
+                                          fs, fe, g->sums, g->amax, g->amax_val,
+                                          (unsigned*)(g->nkeys + 3), t0);
   }
   SP_CHECK_LAUNCH();
   return 0;

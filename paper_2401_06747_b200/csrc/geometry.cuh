@@ -36,6 +36,12 @@ int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s);
 int geo_accumulate_mode(int v);
 int geo_select(Geo* g, uint8_t* mask, long nbuckets, long want, long* picked, cudaStream_t s);
 int fill_highest_error(Geo* g, const double* err, uint8_t* mask, long want, cudaStream_t s);
+// row-strip partition of the Delaunay step and the accumulate (geometry.cu)
+int geo_corner_keys(Geo* g, int r0, int r1, long* n_out, cudaStream_t s);
+int geo_delaunay_from_keys(Geo* g, const unsigned long long* keys, long n, long* T_out,
+                           cudaStream_t s);
+int geo_raster_rows(Geo* g, int r0, int r1, cudaStream_t s);
+int geo_reduce_range(Geo* g, const double* err, long t0, long t1, cudaStream_t s);
 
 // B1 building blocks
 int jfa_passes(int* a, int* b, const int* sy, const int* sx, const long long* steps,

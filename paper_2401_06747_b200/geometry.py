@@ -150,6 +150,45 @@ class GeoWorkspace:
         self.m = int(seeds.shape[0])
         self.ntris = 0
 
+    # -- row-strip partition (StripGeometry) ------------------------------
+    def corner_keys(self, r0: int, r1: int) -> torch.Tensor:
+        """Sorted unique triangle keys of the corners in rows [r0, r1)
+        (int64 view of the packed u64 keys)."""
+        n = ctypes.c_long()
+        call("sp_geo_corner_keys", self._g, int(r0), int(r1), ctypes.byref(n), stream())
+        keys = torch.empty(n.value, dtype=torch.int64, device=_lib.device())
+        if n.value:
+            call("sp_geo_keys_copy", self._g, ptr(keys), n.value, stream())
+        return keys
+
+    def delaunay_from_keys(self, keys: torch.Tensor) -> int:
+        t = ctypes.c_long()
+        keys = keys.contiguous()
+        call("sp_geo_delaunay_from_keys", self._g, ptr(keys), int(keys.numel()),
+             ctypes.byref(t), stream())
+        self.ntris = t.value
+        return self.ntris
+
+    def raster_rows(self, r0: int, r1: int):
+        call("sp_geo_raster_rows", self._g, int(r0), int(r1), stream())
+
+    def assign_rows(self, r0: int, r1: int) -> torch.Tensor:
+        out = torch.empty((r1 - r0, self.width), dtype=torch.int32, device=_lib.device())
+        call("sp_geo_assign_rows", self._g, ptr(out), int(r0), int(r1), 0, stream())
+        return out
+
+    def set_assign_rows(self, rows: torch.Tensor, r0: int, r1: int):
+        rows = rows.to(torch.int32).contiguous()
+        call("sp_geo_assign_rows", self._g, ptr(rows), int(r0), int(r1), 1, stream())
+
+    def reduce_range(self, err_t: torch.Tensor, t0: int, t1: int):
+        call("sp_geo_reduce_range", self._g, ptr(err_t), int(t0), int(t1), stream())
+
+    def set_buckets(self, sums, amax, aval, t0: int):
+        sums, amax, aval = sums.contiguous(), amax.contiguous(), aval.contiguous()
+        call("sp_geo_set_buckets", self._g, ptr(sums), ptr(amax), ptr(aval), int(t0),
+             int(t0 + sums.numel()), stream())
+
     # -- exports -----------------------------------------------------------
     def labels_tensor(self):
         lab = torch.empty((self.height, self.width), dtype=torch.int32, device=_lib.device())
@@ -178,6 +217,78 @@ class GeoWorkspace:
             call("sp_geo_export", self._g, None, None, None, None, ptr(sums), ptr(amax),
                  ptr(aval), int(n), stream())
         return sums, amax, aval
+
+
+class DistGather:
+    """All-gather of variable-length 1-D tensors over the current
+    ``torch.distributed`` group: device tensors under NCCL, host copies
+    under other backends (gloo: the CPU harness, ranks sharing one GPU)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.dev = None if dist.get_backend() == "nccl" else torch.device("cpu")
+
+    def allgather_var(self, t: torch.Tensor):
+        home = t.device
+        dev = self.dev or home
+        t = t.reshape(-1).to(dev)
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=dev)
+        ns = [torch.empty_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n)
+        ns = [int(x.item()) for x in ns]
+        pad = torch.zeros(max(ns), dtype=t.dtype, device=dev)
+        pad[:t.numel()] = t
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(out, pad)
+        return [o[:k].to(home) for o, k in zip(out, ns)]
+
+
+class StripGeometry:
+    """The Delaunay step and the accumulate of `delaunay_densify` on row
+    strips (csrc/geometry.cu geo_corner_keys ...):
+    rank `rank` of `comm` scans the corners of its rows, the sorted key lists
+    are all-gathered and merged; it rasterises its rows, the assignment rows
+    are all-gathered; it reduces its contiguous range of triangles over the
+    full map, and the bucket ranges are all-gathered.  Jump flooding and the
+    selection stay replicated.  Triangles, buckets and picks are bit-identical
+    to the unpartitioned workspace for every strip count (every triangle's
+    sequential f64 sum stays on one rank)."""
+
+    def __init__(self, ws: GeoWorkspace, rows, rank: int, comm):
+        self.ws, self.rows, self.rank, self.comm = ws, list(rows), rank, comm
+        self.P = len(self.rows)
+        self.calls = 0
+
+    def delaunay(self) -> int:
+        r0, r1 = self.rows[self.rank]
+        parts = self.comm.allgather_var(self.ws.corner_keys(r0, r1))
+        self.calls += 1
+        return self.ws.delaunay_from_keys(torch.cat(parts))
+
+    def accumulate(self, err_t: torch.Tensor):
+        ws, P, rank = self.ws, self.P, self.rank
+        r0, r1 = self.rows[rank]
+        ws.raster_rows(r0, r1)
+        parts = self.comm.allgather_var(ws.assign_rows(r0, r1))
+        for p, part in enumerate(parts):
+            if p != rank:
+                a, b = self.rows[p]
+                ws.set_assign_rows(part.view(b - a, ws.width), a, b)
+        T = ws.ntris
+        bounds = [T * p // P for p in range(P + 1)]
+        t0, t1 = bounds[rank], bounds[rank + 1]
+        ws.reduce_range(err_t, t0, t1)
+        sums, amax, aval = ws.buckets(T)
+        # one gather: sums, argmax (int64 bits) and argmax value of the range
+        mine = torch.stack([sums[t0:t1], amax[t0:t1].view(torch.float64), aval[t0:t1]])
+        got = self.comm.allgather_var(mine)
+        for p, g in enumerate(got):
+            if p != rank and g.numel():
+                g = g.view(3, -1)
+                ws.set_buckets(g[0], g[1].contiguous().view(torch.int64), g[2], bounds[p])
+        self.calls += 1
 
 
 _WS: dict = {}

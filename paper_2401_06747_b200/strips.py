@@ -409,6 +409,18 @@ class StripSolver:
     def distributed_ranks(self):
         return self.P if self._comm is not None else 1
 
+    def strip_geometry(self, ws):
+        """The densification geometry partitioned by this solver's row
+        strips (geometry.StripGeometry) when it spans several ranks, else
+        None (the workspace runs whole)."""
+        if self._comm is None or self.P < 2:
+            return None
+        from .geometry import DistGather, StripGeometry
+        rows = [(self.o0[0][p], self.o1[0][p]) for p in range(self.P)] if self.La else \
+            [(self.height * p // self.P, self.height * (p + 1) // self.P) for p in range(self.P)]
+        self.geometry = StripGeometry(ws, rows, self.rank, DistGather())
+        return self.geometry
+
     def _check(self, shape):
         if tuple(shape) != (self.height, self.width):
             raise ValueError("image does not match the strip solver's geometry")

@@ -234,3 +234,77 @@ def test_tiled_accumulate_bit_exact(sp, h, w, d, seed):
     assert np.array_equal(got[1][0], s)
     assert np.array_equal(got[1][1], ai)
     assert np.array_equal(got[1][2], av)
+
+
+class _ThreadGather:
+    """all-gather between the threads of one process (one per simulated
+    rank), for the StripGeometry partition test"""
+
+    def __init__(self, world):
+        import threading
+        self.world = world
+        self.slots = [None] * world
+        self.bar = threading.Barrier(world)
+
+    def for_rank(self, rank):
+        outer = self
+
+        class _G:
+            def allgather_var(self, t):
+                outer.slots[rank] = t.reshape(-1).clone()
+                outer.bar.wait()
+                got = list(outer.slots)
+                outer.bar.wait()
+                return got
+        return _G()
+
+
+@pytest.mark.parametrize("shape,dens,P", [((128, 160), 0.05, 2), ((128, 160), 0.004, 3),
+                                          ((301, 256), 0.02, 4), ((97, 64), 0.1, 2)])
+def test_strip_geometry_bit_identical(shape, dens, P):
+    """The row-strip partition of the Delaunay step and the accumulate
+    (geometry.StripGeometry: per-strip corner keys merged, per-strip
+    rasterisation with the assignment rows gathered, per-rank triangle ranges
+    reduced over the full map) gives every rank the unpartitioned triangles
+    and buckets bit for bit -- incl. hull-exterior (fallback) pixels of
+    sparse masks and uneven strips."""
+    import threading
+    import torch
+    from paper_2401_06747_b200.geometry import GeoWorkspace, StripGeometry
+    H, W = shape
+    rng = np.random.default_rng(11)
+    mask = torch.from_numpy((rng.random((H, W)) < dens).astype(np.uint8)).cuda()
+    err = torch.from_numpy(rng.random((H, W)) * 30.0).cuda()
+    ref = GeoWorkspace(H, W)
+    ref.voronoi(mask)
+    T = ref.delaunay()
+    ref.accumulate(err)
+    tris_ref = ref.triangles_tensor().cpu().numpy()
+    b_ref = [x.cpu().numpy() for x in ref.buckets(T)]
+    rows = [(H * p // P, H * (p + 1) // P) for p in range(P)]
+    comm = _ThreadGather(P)
+    wss = [GeoWorkspace(H, W) for _ in range(P)]
+    for ws in wss:
+        ws.voronoi(mask)
+    errs = []
+
+    def run(p):
+        try:
+            sg = StripGeometry(wss[p], rows, p, comm.for_rank(p))
+            assert sg.delaunay() == T
+            sg.accumulate(err)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            comm.bar.abort()
+
+    th = [threading.Thread(target=run, args=(p,)) for p in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    torch.cuda.synchronize()
+    for ws in wss:
+        assert np.array_equal(ws.triangles_tensor().cpu().numpy(), tris_ref)
+        for a, b in zip(ws.buckets(T), b_ref):
+            assert np.array_equal(a.cpu().numpy(), b)

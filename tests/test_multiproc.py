@@ -64,3 +64,48 @@ def test_reference_arm_rank_nonzero_exits_without_work(monkeypatch, capsys):
     assert bench.main(["--impl", "reference", "--gpus", "2", "--steps", "1",
                        "--warmup", "0"]) == 0
     assert capsys.readouterr().out == ""
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # geometry.DistGather: the strip geometry's variable-length all-gather
+        # (triangle keys, assignment rows, bucket ranges) under gloo
+        from paper_2401_06747_b200.geometry import DistGather
+        g = DistGather()
+        keys = torch.arange(rank * 10, rank * 10 + 3 + 2 * rank, dtype=torch.int64)
+        got = g.allgather_var(keys)
+        rows = torch.full((2 + rank, 4), rank, dtype=torch.int32)
+        got_rows = g.allgather_var(rows)
+        buck = torch.stack([torch.tensor([1.5 + rank], dtype=torch.float64),
+                            torch.tensor([7], dtype=torch.int64).view(torch.float64),
+                            torch.tensor([0.25], dtype=torch.float64)])
+        got_b = g.allgather_var(buck)
+        q.put((rank, [t.tolist() for t in got], [tuple(t.shape) for t in got_rows],
+               [t.view(3, -1)[1].contiguous().view(torch.int64).tolist() for t in got_b]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_strip_geometry_gather_gloo():
+    """The strip geometry's exchange (geometry.DistGather.allgather_var) on
+    two gloo ranks: ragged key lists, ragged row blocks and bit-cast int64
+    bucket argmaxes come back complete and in rank order on every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    for _, keys, shapes, amax in res:
+        assert keys == [[0, 1, 2], [10, 11, 12, 13, 14]]
+        assert shapes == [(8,), (12,)]
+        assert amax == [[7], [7]]

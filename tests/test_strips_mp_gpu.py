@@ -54,7 +54,8 @@ def _worker(rank, world, port, job, out_dir):
             s = StripSolver.distributed(h, w, c, cfg=cfg.solver().cfg, La=1, transport="host")
             mask, st, hist, _ = sp.run_pipeline(sp.Image(f), cfg, solver=s)
             np.savez(os.path.join(out_dir, f"r{rank}.npz"), m=mask.indicator, g=st.g.data,
-                     mse=st.mse, hist=np.array([r[2] for r in hist]))
+                     mse=st.mse, hist=np.array([r[2] for r in hist]),
+                     geo_calls=s.geometry.calls)
     finally:
         dist.destroy_process_group()
 
@@ -87,13 +88,18 @@ def test_two_rank_strip_solve_bit_identical(tmp_path):
 
 
 def test_two_rank_pipeline_on_strips(tmp_path):
-    """run_pipeline on a 2-rank strip solver: distributed solves plus the RAS
-    block problems sharded by rank and all-gathered (tonal.py gather_all)."""
+    """run_pipeline on a 2-rank strip solver: distributed solves, the
+    densification's Delaunay step and accumulate partitioned by the strips
+    (geometry.StripGeometry), and the RAS block problems sharded by rank and
+    all-gathered (tonal.py gather_all) -- bit-identical to one process."""
     import paper_2401_06747_b200 as sp
     from paper_2401_06747_b200.strips import StripSolver
     r0, r1 = _run("pipeline", tmp_path)
     for k in ("m", "g", "hist"):
         assert np.array_equal(r0[k], r1[k])
+    # the Delaunay step and the accumulate ran partitioned by the row strips
+    # (geometry.StripGeometry: 2 calls per densification iteration)
+    assert int(r0["geo_calls"]) > 0 and int(r1["geo_calls"]) > 0
     c, h, w = 3, 512, 768
     f = O.synth(h, w, c, 4)
     cfg = sp.PipelineConfig(iterations=4)
