@@ -18,11 +18,18 @@ one large image: a 7680x4320 RGB inpainting solve cut into one row strip
 per rank, halo exchange / norm all-reduce over NCCL (csrc/strips.cu),
 strong scaling, Mpixel-iterations/s.
 
+`strips_pipeline` (N > 1) is the same 4K pipeline on ONE image cut into
+row strips over the ranks (every solve, the Delaunay step and the
+accumulate partitioned; jump flooding replicated; RAS blocks sharded):
+strong scaling of the metric's wall time.
+
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port under oracle/: C kernel table + numpy orchestration, bit-exact
-with the reference) on the host cores, on a bounded sample of the workload,
-extrapolated to 4K with the reference's own recorded runtime slope in
-pixel count (0.789, pkg/test_output.txt:35).
+with the reference) on the host cores, on bounded samples of the 4K
+workload's own work units (finest V-cycles on the initial and final masks,
+RAS block V-cycles, JFA / Delaunay / accumulate passes), weighted by the
+unit census of the reference's own measured 4K run (oracle/sampled.py,
+tests/golden/large_cfg4.json).
 """
 
 from __future__ import annotations
@@ -230,8 +237,9 @@ def run_reference(args):
 
 def _config(args, world, strips_mode):
     return {"workload": WORKLOAD, "H": H, "W": W, "C": C, "density": 0.05,
-            "parallelism": (f"row strips x{world} (one image; solves on strips, "
-                            "geometry replicated, RAS blocks sharded)"
+            "parallelism": (f"row strips x{world} (one image; solves and the Delaunay / "
+                            "accumulate steps on strips, JFA replicated, RAS blocks "
+                            "sharded)"
                             if strips_mode else f"replicas x{world} (one image per GPU)"),
             "l2": "working set (>1 GB per step) exceeds the 126 MB L2"}
 
@@ -398,9 +406,9 @@ def run_ours(args):
     bsym = _masked_rhs(f_dev.float().contiguous(), mask.tensor())
     hier.solve_sym(bsym, tol=1e-4, cascade=True)
     import ctypes
-    names = {0: "k_resid_tma (sym_residual sweep)", 1: "k_oras_warp (ORAS local CG)",
-             2: "k_oras_blend", 3: "k_resid_tma<1> (residual + restriction)",
-             4: "k_prolong_tma (prolongation + add + enforce)"}
+    names = {0: "k_ws_resid<0> (sym_residual sweep)", 1: "k_oras_warp (ORAS local CG)",
+             2: "k_oras_blend", 3: "k_ws_resid<1> (residual + restriction)",
+             4: "k_ws_prolong (prolongation + add + enforce)"}
     for which in (0, 1, 2, 3, 4):
         t_ms, nbytes = ctypes.c_double(), ctypes.c_double()
         _lib.call("sp_hier_bench", hier._h, which, 20, ctypes.byref(t_ms), ctypes.byref(nbytes),
@@ -420,7 +428,7 @@ def run_ours(args):
                     "by nature, issue_utilization = ncu sm__inst_issued of the same capture); "
                     "stencil sweep roofline in `stencil_roofline`"}
     sten = names[0]
-    trs = _ncu_traffic("k_resid_tma")
+    trs = _ncu_traffic("k_ws_resid")
     stencil_roofline = {"bound": "hbm", "kernel": sten, "achieved": kern[sten]["gbs"],
                         "peak": peak, "unit": "GB/s", "frac": kern[sten]["frac"],
                         "traffic": trs["bytes"] if trs else None,

@@ -212,6 +212,11 @@ int sp_geo_destroy(void* geo);
 int sp_geo_voronoi(void* geo, const uint8_t* mask, double start_hint, long* m,
                    double* max_radius, int* nsteps, void* stream);
 int sp_geo_delaunay(void* geo, long* ntris, void* stream); /* syncs */
+/* Seed count from which sp_geo_delaunay sorts wide triangle keys (a, b << 32
+ * | c) by two stable radix passes instead of packed 3 x 21-bit keys
+ * (default and maximum 2^21, i.e. any mask the reference accepts works;
+ * v <= 0 queries).  Lowered only by tests of the wide path. */
+long sp_geo_wide_threshold(long v);
 /* err: device double (H, W); voronoi != 0 buckets by cell instead of triangle */
 int sp_geo_accumulate(void* geo, const double* err, int voronoi, void* stream);
 /* implementation of sp_geo_accumulate (partition "delaunay"): 1 = tile-binned

@@ -70,6 +70,7 @@ _SIGS = {
     "sp_geo_delaunay": [P, P, P],
     "sp_geo_accumulate": [P, P, c_int, P],
     "sp_geo_corner_keys": [P, c_int, c_int, P, P],
+    "sp_geo_wide_threshold": [c_long],
     "sp_geo_keys_copy": [P, P, c_long, P],
     "sp_geo_delaunay_from_keys": [P, P, c_long, P, P],
     "sp_geo_raster_rows": [P, c_int, c_int, P],
@@ -142,6 +143,7 @@ def load(require_cuda: bool = True):
         lib.sp_launch_count.argtypes = [c_int]
         lib.sp_work_count.restype = ctypes.c_longlong
         lib.sp_work_count.argtypes = [c_int, c_int]
+        lib.sp_geo_wide_threshold.restype = c_long
         lib.sp_last_error.restype = ctypes.c_char_p
         lib.sp_last_error.argtypes = []
         _lib = lib

@@ -408,6 +408,11 @@ int sp_geo_delaunay(void* g, long* ntris, void* s) {
   return geo_delaunay((Geo*)g, ntris, STREAM(s));
 }
 
+// seed count from which sp_geo_delaunay sorts wide (2 x 32-bit) triangle
+// keys instead of packed 3 x 21-bit ones (default and maximum 2^21; v <= 0
+// queries) -- lowered only to test the wide path on small images
+long sp_geo_wide_threshold(long v) { return geo_wide_threshold(v); }
+
 // programmatic dependent launch of the V-cycle kernels on levels >= v
 // (v = -1: off; v < -1: read only); returns the setting
 int sp_pdl_from_level(int v) { return sp::pdl_from_level(v); }

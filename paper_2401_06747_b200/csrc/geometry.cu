@@ -269,11 +269,20 @@ __device__ __forceinline__ void sort3(unsigned& a, unsigned& b, unsigned& c) {
 
 // corner rows [y0c, y1c) (a corner row y reads label rows y and y + 1; the
 // whole image is y0c = 0, y1c = H - 1)
+// WIDE (>= 2^21 seeds): the triple as keys2 = a (the high word) and keys =
+// b << 32 | c, sorted lexicographically by two stable passes (wide_sort)
+template <bool WIDE>
 __global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
                               unsigned long long* __restrict__ keys,
-                              unsigned long long* __restrict__ nkeys, int y0c, int y1c) {
+                              unsigned long long* __restrict__ nkeys, int y0c, int y1c,
+                              unsigned* __restrict__ keys2) {
   int x = blockIdx.x * BX + threadIdx.x, y = y0c + blockIdx.y * BY + threadIdx.y;
   unsigned long long k0 = 0, k1 = 0;
+  unsigned h0 = 0, h1 = 0;
+  auto key = [&](unsigned a, unsigned b, unsigned c, unsigned& hi) {
+    hi = a;
+    return WIDE ? (((unsigned long long)b << 32) | c) : tri_key(a, b, c);
+  };
   int nk = 0;
   if (x < W - 1 && y < y1c) {
     size_t p = (size_t)y * W + x;
@@ -289,7 +298,7 @@ __global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
     int nd = 4 - (int)d0 - (int)d1 - (int)d2;
     if (nd == 3) {
       unsigned a = s0, b = d0 ? s2 : s1, c = d2 ? s2 : s3;
-      k0 = tri_key(a, b, c);
+      k0 = key(a, b, c, h0);
       nk = 1;
     } else if (nd == 4) {
       int a = tl, b = tr, c = bl, d = br;
@@ -300,8 +309,8 @@ __global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
       else { p0 = a; p1 = b; p2 = c; q0 = b; q1 = c; q2 = d; }
       sort3(p0, p1, p2);
       sort3(q0, q1, q2);
-      k0 = tri_key(p0, p1, p2);
-      k1 = tri_key(q0, q1, q2);
+      k0 = key(p0, p1, p2, h0);
+      k1 = key(q0, q1, q2, h1);
       nk = 2;
     }
   }
@@ -332,6 +341,10 @@ __global__ void k_corner_scan(const int* __restrict__ lab, int H, int W,
   unsigned long long pos = cbase + wtot[threadIdx.y] + incl - cnt;
   if (nk >= 1) keys[pos] = k0;
   if (nk == 2) keys[pos + 1] = k1;
+  if (WIDE) {
+    if (nk >= 1) keys2[pos] = h0;
+    if (nk == 2) keys2[pos + 1] = h1;
+  }
 }
 
 __global__ void k_decode_tris(const unsigned long long* __restrict__ keys, long T,
@@ -342,6 +355,37 @@ __global__ void k_decode_tris(const unsigned long long* __restrict__ keys, long 
   tris[3 * i] = (int)(k >> 42);
   tris[3 * i + 1] = (int)((k >> 21) & 0x1FFFFFull);
   tris[3 * i + 2] = (int)(k & 0x1FFFFFull);
+}
+
+__global__ void k_decode_tris_wide(const unsigned long long* __restrict__ lo,
+                                   const unsigned* __restrict__ hi, long T,
+                                   int* __restrict__ tris) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T) return;
+  tris[3 * i] = (int)hi[i];
+  tris[3 * i + 1] = (int)(lo[i] >> 32);
+  tris[3 * i + 2] = (int)(lo[i] & 0xFFFFFFFFull);
+}
+
+// wide keys: flags of the first of every run of equal (hi, lo) pairs
+__global__ void k_wide_uniq_flags(const unsigned long long* __restrict__ lo,
+                                  const unsigned* __restrict__ hi, long n,
+                                  uint8_t* __restrict__ flag) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = i == 0 || lo[i] != lo[i - 1] || hi[i] != hi[i - 1];
+}
+
+__global__ void k_gather_u64_u32(const int* __restrict__ idx, long n,
+                                 const unsigned long long* __restrict__ lo_in,
+                                 const unsigned* __restrict__ hi_in,
+                                 unsigned long long* __restrict__ lo_out,
+                                 unsigned* __restrict__ hi_out) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = idx[i];
+  if (lo_out) lo_out[i] = lo_in[j];
+  if (hi_out) hi_out[i] = hi_in[j];
 }
 
 // ---- rasterization (numba_impl.py:442-466) --------------------------------
@@ -1044,6 +1088,7 @@ int reduce_cells(const int* assign, const double* err, long nseg, double* sums,
 
 Geo::~Geo() {
   for (void* p : {(void*)lab_a, (void*)lab_b, (void*)rank, (void*)sy, (void*)sx, (void*)keys,
+                  (void*)keys2,
                   (void*)nkeys, (void*)tris, (void*)assign, (void*)smt, (void*)sums,
                   (void*)amax, (void*)amax_val, (void*)dmax, (void*)flags, (void*)idx,
                   (void*)nsel, (void*)h_small})
@@ -1175,18 +1220,85 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
 
 static int sort_unique_keys(Geo* g, long nk, long* n_out, bool decode, cudaStream_t s);
 
+// >= 2^21 seeds: the packed 3 x 21-bit keys would overflow.  The corner
+// triples are kept as (a, b << 32 | c) pairs and sorted lexicographically by
+// two stable radix passes (low word, then high word, the payload an index),
+// then deduplicated -- the same sorted unique triangle list.
+static int delaunay_wide(Geo* g, long* T_out, cudaStream_t s) {
+  const int H = g->H, W = g->W;
+  if (!g->keys2) SP_CUDA(cudaMalloc(&g->keys2, sizeof(unsigned) * g->key_cap));
+  SP_CUDA(cudaMemsetAsync(g->nkeys, 0, sizeof(unsigned long long) * 2, s));
+  k_corner_scan<true><<<grid2(W, H), dim3(BX, BY), 0, s>>>(g->lab_a, H, W, g->keys, g->nkeys,
+                                                           0, H - 1, g->keys2);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const long nk = (long)((unsigned long long*)g->h_small)[0];
+  if (nk == 0) return 0;
+  const int nb = bits_for(g->m - 1);
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b1, (const unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (const int*)nullptr,
+                                  (int*)nullptr, (int)nk, 0, 32 + nb, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                  (const int*)nullptr, (int*)nullptr, (int)nk, 0, nb, s);
+  cub::CountingInputIterator<int> it(0);
+  cub::DeviceSelect::Flagged(nullptr, b3, it, (const uint8_t*)nullptr, (int*)nullptr,
+                             (int*)nullptr, (int)nk, s);
+  const size_t nn = (size_t)nk;
+  Scratch scr(s);
+  SP_TRY(scr.alloc(nn * (8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + std::max(b1, std::max(b2, b3)) + 1024));
+  unsigned long long* lo_s = (unsigned long long*)scr.p;
+  unsigned long long* lo_f = lo_s + nn;
+  unsigned* hi_g = (unsigned*)(lo_f + nn);
+  unsigned* hi_s = hi_g + nn;
+  int* idx0 = (int*)(hi_s + nn);
+  int* idx1 = idx0 + nn;
+  int* idx2 = idx1 + nn;
+  uint8_t* flag = (uint8_t*)(idx2 + nn);
+  void* tmp = (void*)(((uintptr_t)(flag + nn) + 255) & ~(uintptr_t)255);
+  k_iota<<<cdiv(nn, 256), 256, 0, s>>>(idx0, nn);
+  SP_CHECK_LAUNCH();
+  // pass 1: by the low word (b, c); pass 2 (stable): by the high word a
+  SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, b1, g->keys, lo_s, idx0, idx1, (int)nk, 0,
+                                          32 + nb, s));
+  k_gather_u64_u32<<<cdiv(nn, 256), 256, 0, s>>>(idx1, nk, g->keys, g->keys2, nullptr, hi_g);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, b2, hi_g, hi_s, idx1, idx2, (int)nk, 0, nb, s));
+  k_gather_u64_u32<<<cdiv(nn, 256), 256, 0, s>>>(idx2, nk, g->keys, g->keys2, lo_f, nullptr);
+  SP_CHECK_LAUNCH();
+  k_wide_uniq_flags<<<cdiv(nn, 256), 256, 0, s>>>(lo_f, hi_s, nk, flag);
+  SP_CHECK_LAUNCH();
+  SP_CUDA(cub::DeviceSelect::Flagged(tmp, b3, it, flag, idx0, g->nsel, (int)nk, s));
+  SP_CUDA(cudaMemcpyAsync(g->h_small, g->nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const long T = ((int*)g->h_small)[0];
+  // unique pairs into keys / keys2, then the triangles
+  k_gather_u64_u32<<<cdiv(T, 256), 256, 0, s>>>(idx0, T, lo_f, hi_s, g->keys, g->keys2);
+  SP_CHECK_LAUNCH();
+  k_decode_tris_wide<<<cdiv(T, 256), 256, 0, s>>>(g->keys, g->keys2, T, g->tris);
+  SP_CHECK_LAUNCH();
+  g->T = T;
+  *T_out = T;
+  return 0;
+}
+
+// seed count from which the wide keys are used (2^21; lower only for tests)
+static long wide_from = 1L << 21;
+long geo_wide_threshold(long v) {
+  if (v > 0 && v <= (1L << 21)) wide_from = v;
+  return wide_from;
+}
+
 int geo_delaunay(Geo* g, long* T_out, cudaStream_t s) {
   const int H = g->H, W = g->W;
   g->T = 0;
   *T_out = 0;
   if (H < 2 || W < 2 || g->m < 3) return 0;
-  if (g->m >= (1L << 21)) {
-    set_error("more than 2^21 stored pixels: triangle keys would overflow");
-    return -2;
-  }
   SP_CUDA(cudaMemsetAsync(g->nkeys, 0, sizeof(unsigned long long) * 2, s));
-  k_corner_scan<<<grid2(W, H), dim3(BX, BY), 0, s>>>(g->lab_a, H, W, g->keys, g->nkeys, 0,
-                                                     H - 1);
+  if (g->m >= wide_from) return delaunay_wide(g, T_out, s);
+  k_corner_scan<false><<<grid2(W, H), dim3(BX, BY), 0, s>>>(g->lab_a, H, W, g->keys, g->nkeys,
+                                                            0, H - 1, nullptr);
   SP_CHECK_LAUNCH();
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
@@ -1334,14 +1446,14 @@ int geo_corner_keys(Geo* g, int r0, int r1, long* n_out, cudaStream_t s) {
   g->T = 0;
   if (H < 2 || W < 2 || g->m < 3) return 0;
   if (g->m >= (1L << 21)) {
-    set_error("more than 2^21 stored pixels: triangle keys would overflow");
+    set_error("the strip-partitioned Delaunay step packs keys for < 2^21 stored pixels");
     return -2;
   }
   const int y0c = std::max(0, r0), y1c = std::min(r1, H - 1);
   SP_CUDA(cudaMemsetAsync(g->nkeys, 0, sizeof(unsigned long long) * 2, s));
   if (y1c > y0c) {
-    k_corner_scan<<<dim3(cdiv(W, BX), cdiv(y1c - y0c, BY)), dim3(BX, BY), 0, s>>>(
-        g->lab_a, H, W, g->keys, g->nkeys, y0c, y1c);
+    k_corner_scan<false><<<dim3(cdiv(W, BX), cdiv(y1c - y0c, BY)), dim3(BX, BY), 0, s>>>(
+        g->lab_a, H, W, g->keys, g->nkeys, y0c, y1c, nullptr);
     SP_CHECK_LAUNCH();
   }
   SP_CUDA(cudaMemcpyAsync(g->h_small, g->nkeys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));

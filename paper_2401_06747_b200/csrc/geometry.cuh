@@ -15,6 +15,7 @@ struct Geo {
   int* rank = nullptr;                     // seed index at each seed pixel
   uint8_t* flags = nullptr;
   unsigned long long* keys = nullptr;
+  unsigned* keys2 = nullptr;               // high words of wide keys (>= 2^21 seeds)
   unsigned long long* nkeys = nullptr;
   int* tris = nullptr;                     // (T, 3) ascending triples, sorted
   int* assign = nullptr;
@@ -32,6 +33,7 @@ int geo_create(Geo** out, int H, int W);
 int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* radius,
                 int* nsteps_out, cudaStream_t s);
 int geo_delaunay(Geo* g, long* T_out, cudaStream_t s);
+long geo_wide_threshold(long v);  // seeds from which the wide (2 x 32-bit) keys apply
 int geo_accumulate(Geo* g, const double* err, int voronoi, cudaStream_t s);
 int geo_accumulate_mode(int v);
 int geo_select(Geo* g, uint8_t* mask, long nbuckets, long want, long* picked, cudaStream_t s);

@@ -296,18 +296,28 @@ int prolong_lv(Hier* h, int lv, int add, cudaStream_t s) {
 }
 
 template <typename T>
+static int oras_lv(Hier* h, Level& L, cudaStream_t s) {
+  return oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs, L.nby,
+                              L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma, (long)L.bh * L.bw,
+                              1.0, (const T*)L.weights, (T*)L.corr, s, h->ntile, h->d_active,
+                              h->cfg.block - h->cfg.overlap, 0, 0, L.wdelta, L.offbits);
+}
+
+// u += the level's weighted block corrections (block order)
+template <typename T>
+static int blend_lv(Hier* h, Level& L, T* u, cudaStream_t s) {
+  return oras_blend_launch<T>(u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n, L.col_k0,
+                              L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, s, h->ntile,
+                              h->d_active);
+}
+
+template <typename T>
 int smooth_lv(Hier* h, int lv, int sweeps, bool first_done, cudaStream_t s) {
   Level& L = h->lv[lv];
   for (int sw = 0; sw < sweeps; ++sw) {
     if (!(sw == 0 && first_done)) SP_TRY(residual_lv<T>(h, lv, true, s));
-    SP_TRY(oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
-                                L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
-                                (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
-                                h->ntile, h->d_active, h->cfg.block - h->cfg.overlap, 0, 0,
-                                L.wdelta, L.offbits));
-    SP_TRY(oras_blend_launch<T>((T*)L.u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,
-                                L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
-                                s, h->ntile, h->d_active));
+    SP_TRY(oras_lv<T>(h, L, s));
+    SP_TRY(blend_lv<T>(h, L, (T*)L.u, s));
   }
   return 0;
 }
@@ -823,17 +833,10 @@ static int bench_t(Hier* h, int which, int reps, cudaStream_t s, double* ms, dou
       case 0:
         return residual_lv<T>(h, 0, true, s);
       case 1:
-        return oras_local_launch<T>((const T*)L.r, L.mask, L.norms, L.tau_scale, L.ys, L.xs,
-                                    L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, h->gamma,
-                                    (long)L.bh * L.bw, 1.0, (const T*)L.weights, (T*)L.corr, s,
-                                    h->ntile, h->d_active, h->cfg.block - h->cfg.overlap, 0, 0,
-                                    L.wdelta, L.offbits);
-      case 2: {
+        return oras_lv<T>(h, L, s);
+      case 2:
         // blend into a scratch copy so the solver state is not disturbed
-        return oras_blend_launch<T>((T*)L.r, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n,
-                                    L.col_k0, L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C,
-                                    s, h->ntile, h->d_active);
-      }
+        return blend_lv<T>(h, L, (T*)L.r, s);
       case 3:
         if (!G) { set_error("single-level hierarchy"); return -2; }
         return residual_restrict_lv<T>(h, 0, s);

@@ -308,3 +308,56 @@ def test_strip_geometry_bit_identical(shape, dens, P):
         assert np.array_equal(ws.triangles_tensor().cpu().numpy(), tris_ref)
         for a, b in zip(ws.buckets(T), b_ref):
             assert np.array_equal(a.cpu().numpy(), b)
+
+
+@pytest.mark.parametrize("shape,dens", [((128, 160), 0.05), ((97, 64), 0.3)])
+def test_delaunay_wide_keys_match_packed(shape, dens):
+    """>= 2^21 stored pixels overflow the packed 3 x 21-bit triangle keys;
+    sp_geo_delaunay then sorts (a, b << 32 | c) pairs by two stable radix
+    passes.  Forced on small masks (sp_geo_wide_threshold), the wide path
+    gives the packed path's triangles (np.unique order) and buckets."""
+    import torch
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.geometry import GeoWorkspace
+    lib = _lib.load()
+    H, W = shape
+    rng = np.random.default_rng(5)
+    mask = torch.from_numpy((rng.random((H, W)) < dens).astype(np.uint8)).cuda()
+    err = torch.from_numpy(rng.random((H, W))).cuda()
+    out = []
+    prev = lib.sp_geo_wide_threshold(0)
+    try:
+        for thr in (prev, 3):
+            lib.sp_geo_wide_threshold(thr)
+            ws = GeoWorkspace(H, W)
+            ws.voronoi(mask)
+            T = ws.delaunay()
+            ws.accumulate(err)
+            out.append((ws.triangles_tensor().cpu().numpy(),
+                        [x.cpu().numpy() for x in ws.buckets(T)]))
+    finally:
+        lib.sp_geo_wide_threshold(prev)
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_delaunay_above_2p21_seeds():
+    """A mask with more than 2^21 stored pixels (the reference accepts any
+    density): the triangulation completes, sorted unique triples of seed
+    indices, each triangle's corner pixels really adjacent in the labels."""
+    import torch
+    from paper_2401_06747_b200.geometry import GeoWorkspace
+    H, W = 1536, 1500
+    rng = np.random.default_rng(9)
+    mask = torch.from_numpy((rng.random((H, W)) < 0.95).astype(np.uint8)).cuda()
+    ws = GeoWorkspace(H, W)
+    m, _ = ws.voronoi(mask)
+    assert m >= 2 ** 21
+    T = ws.delaunay()
+    tris = ws.triangles_tensor().cpu().numpy().astype(np.int64)
+    assert T == tris.shape[0] > 0
+    assert (tris[:, 0] < tris[:, 1]).all() and (tris[:, 1] < tris[:, 2]).all()
+    assert tris.max() < m
+    key = (tris[:, 0] * m + tris[:, 1]) * m + tris[:, 2]
+    assert (np.diff(key) > 0).all()          # sorted, unique
