@@ -375,6 +375,10 @@ int sp_ws_stages(int v);
  * pyramid (1, default) or load and test their mask bytes (0); bit-identical.
  * v < 0 queries.  A/B aid, no reference counterpart. */
 int sp_oras_offbits(int v);
+/* C = 3 float blend: 1 = packed per-row / per-column cover words (one table
+ * load each, default), 0 = the cover-table chains; bit-identical.  v < 0
+ * queries.  A/B aid, no reference counterpart. */
+int sp_blend_packed(int v);
 /* residual r = b~ - A~ u and per-plane sum r^2 of level lv's current iterate
  * (after a solve), computed by the hierarchy's sweep kernel, into device
  * buffers r_out [ntile][C][h][w], norms_out [ntile][C] (kernel-variant

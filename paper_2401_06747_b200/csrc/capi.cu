@@ -562,6 +562,7 @@ extern "C" int sp_ws_variant(int v) { return sp::ws_variant(v); }
 extern "C" int sp_ws_prefetch(int v) { return sp::ws_prefetch(v); }
 extern "C" int sp_ws_stages(int v) { return sp::ws_stages(v); }
 extern "C" int sp_oras_offbits(int v) { return sp::oras_offbits(v); }
+extern "C" int sp_blend_packed(int v) { return sp::blend_packed(v); }
 namespace sp { int tile_fused(int v); int channel_parallel(int v); int graph_loop(int v); }
 extern "C" int sp_tile_fused(int v) { return sp::tile_fused(v); }
 extern "C" int sp_channel_parallel(int v) { return sp::channel_parallel(v); }

@@ -1,5 +1,6 @@
 // kernels.cuh -- launcher declarations shared by the .cu translation units.
 #pragma once
+#include <vector>
 #include "common.cuh"
 
 namespace sp {
@@ -45,7 +46,12 @@ template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile = 1,
-                      const int* active = nullptr, int corr_nb = 0, size_t ps = 0);
+                      const int* active = nullptr, int corr_nb = 0, size_t ps = 0,
+                      const int* rowinfo = nullptr, const int* colinfo = nullptr);
+// packed per-row / per-column cover words for the C = 3 float blend
+// (k_oras_blend3p); sp_blend_packed
+bool blend_pack(const std::vector<int>& starts, int size, int dim, std::vector<int>& info);
+int blend_packed(int v);
 // partition-of-unity weights [nb][bh][bw] (solver.py:142-197)
 template <typename T>
 int block_weights_launch(T* weights, const int* ys, const int* xs, const int* row_k0,

@@ -1002,6 +1002,109 @@ __global__ void __launch_bounds__(256) k_oras_blend3(
   }
 }
 
+// k_oras_blend3 with the per-row / per-column cover data packed into one
+// word each at hierarchy build (blend_pack: k0 | two << 16 | three << 17 |
+// o0 << 18 | o1 << 24): one table load per row and per column instead of the
+// dependent cover-table -> block-start chains (ncu: the blend stalls 54 % on
+// long scoreboards).  Rows or columns with three covering blocks take the
+// generic path.  Same gather, same block order: bit-identical.
+__global__ void __launch_bounds__(256) k_oras_blend3p(
+    float* __restrict__ u, const float* __restrict__ corr, const int* __restrict__ ys,
+    const int* __restrict__ xs, const int* __restrict__ row_k0, const int* __restrict__ row_n,
+    const int* __restrict__ col_k0, const int* __restrict__ col_n,
+    const int* __restrict__ rowinfo, const int* __restrict__ colinfo, int nbx, int H, int W,
+    const int* __restrict__ active, int nb, size_t ps) {
+  pdl_enter();
+  const int tile = blockIdx.y;
+  if (active && !active[tile]) return;
+  const int plane = (int)ps, cplane = nb * 1024;
+  float* ut = u + (size_t)tile * 3 * ps;
+  const float* ct = corr + (size_t)tile * 3 * (size_t)cplane;
+  const int ntx = (W + 31) >> 5, nty = (H + 15) >> 4, per = ntx * nty;
+  for (int t = blockIdx.x; t < per; t += gridDim.x) {
+    const int ty = t / ntx;
+    const int x = (t - ty * ntx) * 32 + threadIdx.x;
+    if (x >= W) continue;
+    const int ci = colinfo[x];
+    int yv[2], ri[2];
+    bool ok[2];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      yv[h2] = ty * 16 + threadIdx.y + 8 * h2;
+      ok[h2] = yv[h2] < H;
+      ri[h2] = ok[h2] ? rowinfo[yv[h2]] : 0;
+    }
+    if (((ci | ri[0] | ri[1]) >> 17) & 1) {
+      // a row or column with three covering blocks (a pulled-in last block)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        if (!ok[h2]) continue;
+        const int y = yv[h2], k = y * W + x;
+        float acc[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = ut[c * plane + k];
+        for (int a = 0; a < row_n[y]; ++a) {
+          const int ky = row_k0[y] + a;
+          const int rowoff = ky * nbx * 1024 + (y - ys[ky]) * 32;
+          for (int b2 = 0; b2 < col_n[x]; ++b2) {
+            const int kx = col_k0[x] + b2;
+            const int o = rowoff + kx * 1024 + (x - xs[kx]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[c] = acc[c] + ct[c * cplane + o];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ut[c * plane + k] = acc[c];
+      }
+      continue;
+    }
+    const int kx0 = ci & 0xFFFF, xo0 = (ci >> 18) & 63, dxo = ((ci >> 24) & 63) - xo0;
+    const bool twox = (ci >> 16) & 1;
+    int off[2][4];
+    bool on[2][4];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int r = ri[h2];
+      const int ky0 = r & 0xFFFF, yo0 = (r >> 18) & 63, dyo = ((r >> 24) & 63) - yo0;
+      const bool twoy = (r >> 16) & 1;
+      const int b00 = (ky0 * nbx + kx0) * 1024 + yo0 * 32 + xo0;
+      off[h2][0] = b00;
+      off[h2][1] = b00 + 1024 + dxo;
+      off[h2][2] = b00 + nbx * 1024 + dyo * 32;
+      off[h2][3] = off[h2][2] + 1024 + dxo;
+      on[h2][0] = ok[h2];
+      on[h2][1] = ok[h2] && twox;
+      on[h2][2] = ok[h2] && twoy;
+      on[h2][3] = ok[h2] && twox && twoy;
+    }
+    float uu[2][3], v[2][4][3];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        uu[h2][c] = ok[h2] ? ut[c * plane + yv[h2] * W + x] : 0.0f;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          v[h2][q][c] = on[h2][q] ? ct[c * cplane + off[h2][q]] : 0.0f;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      if (!ok[h2]) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float acc = uu[h2][c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (on[h2][q]) acc = acc + v[h2][q][c];
+        ut[c * plane + yv[h2] * W + x] = acc;
+      }
+    }
+  }
+}
+
 // generic channel count (C > 4): one channel plane per grid row
 template <typename T>
 __global__ void __launch_bounds__(256) k_oras_blend_plane(
@@ -1108,11 +1211,41 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   return 0;
 }
 
+// host: packed cover words of sorted block starts (k_oras_blend3p); false
+// when a block offset does not fit
+bool blend_pack(const std::vector<int>& starts, int size, int dim, std::vector<int>& info) {
+  info.assign(dim, 0);
+  for (int y = 0; y < dim; ++y) {
+    int k0 = -1, n = 0;
+    for (size_t k = 0; k < starts.size(); ++k)
+      if (starts[k] <= y && y < starts[k] + size) {
+        if (k0 < 0) k0 = (int)k;
+        ++n;
+      }
+    if (n < 1 || k0 > 0xFFFF) return false;
+    if (n > 2) {  // generic path
+      info[y] = 1 << 17;
+      continue;
+    }
+    const int o0 = y - starts[k0], o1 = n > 1 ? y - starts[k0 + 1] : o0;
+    if (o0 > 63 || o1 > 63) return false;
+    info[y] = k0 | ((n - 1) << 16) | (o0 << 18) | (o1 << 24);
+  }
+  return true;
+}
+
+static int blend_packed_on = 1;
+int blend_packed(int v) {
+  if (v >= 0) blend_packed_on = v;
+  return blend_packed_on;
+}
+
 template <typename T>
 int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const int* row_k0,
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile,
-                      const int* active, int corr_nb, size_t ps) {
+                      const int* active, int corr_nb, size_t ps, const int* rowinfo,
+                      const int* colinfo) {
   if (!ps) ps = (size_t)H * W;
   long per = (long)cdiv(W, 32) * cdiv(H, C <= 4 ? 16 : 8);
   long nz = C <= 4 ? (long)ntile : (long)ntile * C;
@@ -1124,9 +1257,14 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   SP_CUDA(launch_k(k_oras_blend<T, CM>, grid, blk, 0, s, u, corr, ys, xs, row_k0, row_n,    \
                    col_k0, col_n, nby, nbx, bh, bw, H, W, C, active, corr_nb, ps))
   const long nbt = (long)(corr_nb > 0 ? corr_nb : nby * nbx);
+  const bool b3 = C == 3 && sizeof(T) == 4 && bh == 32 && bw == 32 && 3 * ps < (1UL << 31) &&
+                  3 * nbt * 1024 < (1L << 31);
   if (C == 1) SP_BLEND(1);
-  else if (C == 3 && sizeof(T) == 4 && bh == 32 && bw == 32 && 3 * ps < (1UL << 31) &&
-           3 * nbt * 1024 < (1L << 31))
+  else if (b3 && rowinfo && colinfo && blend_packed_on)
+    SP_CUDA(launch_k(k_oras_blend3p, grid, blk, 0, s, (float*)u, (const float*)corr, ys, xs,
+                     row_k0, row_n, col_k0, col_n, rowinfo, colinfo, nbx, H, W, active,
+                     (int)nbt, ps));
+  else if (b3)
     SP_CUDA(launch_k(k_oras_blend3, grid, blk, 0, s, (float*)u, (const float*)corr, ys, xs,
                      row_k0, row_n, col_k0, col_n, nbx, H, W, active, (int)nbt, ps));
   else if (C == 3) SP_BLEND(3);
@@ -1218,7 +1356,7 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
                                     int, int, int, cudaStream_t, int, const int*, int,      \
-                                    size_t);                                                \
+                                    size_t, const int*, const int*);                        \
   template int block_weights_launch<T>(T*, const int*, const int*, const int*, const int*,  \
                                        const int*, const int*, int, int, int, int, int,     \
                                        int, int, cudaStream_t);

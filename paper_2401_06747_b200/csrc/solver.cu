@@ -73,7 +73,7 @@ Hier::~Hier() {
     for (void* p : {(void*)L.mask, L.values, L.u, L.b, L.r, L.corr, L.weights, (void*)L.partial,
                     (void*)L.counter, (void*)L.norms, (void*)L.ys, (void*)L.xs,
                     (void*)L.row_k0, (void*)L.row_n, (void*)L.col_k0, (void*)L.col_n,
-                    (void*)L.wdelta, (void*)L.offbits})
+                    (void*)L.wdelta, (void*)L.offbits, (void*)L.rowinfo, (void*)L.colinfo})
       if (p) cudaFree(p);
   }
   if (d_active) cudaFree(d_active);
@@ -150,6 +150,13 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     L.offbits = nullptr;
     if (dtype != SP_F64 && L.bh <= 32 && L.bw <= 32)
       rc |= dalloc((void**)&L.offbits, sizeof(uint32_t) * 32 * nb * ntile);
+    std::vector<int> rinfo, cinfo;
+    L.rowinfo = L.colinfo = nullptr;
+    if (dtype != SP_F64 && L.bh == 32 && L.bw == 32 && blend_pack(ys, 32, hh, rinfo) &&
+        blend_pack(xs, 32, ww, cinfo)) {
+      rc |= dalloc((void**)&L.rowinfo, sizeof(int) * hh);
+      rc |= dalloc((void**)&L.colinfo, sizeof(int) * ww);
+    }
     h->lv.push_back(L);
     if (rc) { delete h; return -1; }
     Level& B = h->lv.back();
@@ -159,7 +166,11 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
         cudaMemcpy(B.row_k0, rk0.data(), sizeof(int) * hh, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(B.row_n, rn.data(), sizeof(int) * hh, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(B.col_k0, ck0.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(B.col_n, cn.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(B.col_n, cn.data(), sizeof(int) * ww, cudaMemcpyHostToDevice) != cudaSuccess ||
+        (B.rowinfo && cudaMemcpy(B.rowinfo, rinfo.data(), sizeof(int) * hh,
+                                 cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (B.colinfo && cudaMemcpy(B.colinfo, cinfo.data(), sizeof(int) * ww,
+                                 cudaMemcpyHostToDevice) != cudaSuccess)) {
       set_error("hierarchy upload failed");
       delete h;
       return -1;
@@ -308,7 +319,7 @@ template <typename T>
 static int blend_lv(Hier* h, Level& L, T* u, cudaStream_t s) {
   return oras_blend_launch<T>(u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n, L.col_k0,
                               L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, s, h->ntile,
-                              h->d_active);
+                              h->d_active, 0, 0, L.rowinfo, L.colinfo);
 }
 
 template <typename T>

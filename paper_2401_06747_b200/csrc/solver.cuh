@@ -39,6 +39,7 @@ struct Level {
   // 32): bit s of word j = row s of column j is masked or outside the block;
   // rebuilt with the mask pyramid (set_mask_t), or null
   uint32_t* offbits;
+  int *rowinfo, *colinfo;  // packed cover words (oras.cu blend_pack), or null
 };
 
 struct Hier {

@@ -14,12 +14,14 @@ f = torch.from_numpy(O.synth(H, W, C, 0)).float().cuda()
 mask = (torch.from_numpy(np.random.default_rng(2).random((H, W)) < 0.05)).to(torch.uint8).cuda()
 bsym = _masked_rhs(f, mask)
 names = {0: "resid", 1: "oras", 2: "blend", 3: "resid+restrict", 4: "prolong"}
-# ws:prefetch:stages[:oras_offbits]
+# ws:prefetch:stages[:oras_offbits[:blend_packed]]
 variants = [tuple(map(int, a.split(":"))) for a in sys.argv[1:]] or [(0, 0, 2), (1, 2, 2)]
 for var in variants:
     ws, pf, spw = var[:3]
     ob = var[3] if len(var) > 3 else 1
+    bp = var[4] if len(var) > 4 else 1
     lib.sp_oras_offbits(ob)
+    lib.sp_blend_packed(bp)
     lib.sp_ws_variant(ws)
     lib.sp_ws_prefetch(pf)
     lib.sp_ws_stages(spw)
@@ -38,4 +40,4 @@ for var in variants:
     hier.solve_sym(bsym, init=u, tol=None, cycles=20)
     torch.cuda.synchronize()
     vc = (time.perf_counter() - t) / 20 * 1e3
-    print(f"ws={ws} pf={pf} spw={spw} offbits={ob}: V-cycle {vc:.3f} ms | " + " | ".join(out), flush=True)
+    print(f"ws={ws} pf={pf} spw={spw} offbits={ob} bpack={bp}: V-cycle {vc:.3f} ms | " + " | ".join(out), flush=True)

@@ -302,3 +302,32 @@ def test_device_driven_solve_loop_identical(shape, tol):
     assert a[1:4] == b[1:4] and a[5:] == b[5:]
     assert b[5] == 2 and not b[6]
 
+
+
+@pytest.mark.parametrize("shape", [(3, 301, 512), (3, 60, 516), (3, 540, 960), (3, 67, 1300)])
+def test_blend_packed_cover_words_bit_identical(shape):
+    """The C = 3 blend with packed per-row / per-column cover words
+    (k_oras_blend3p) vs the cover-table chains (k_oras_blend3): the same
+    corrections added in the same block order (numba_impl.py:255-263), so
+    V-cycles from the same start are bit-identical -- incl. the rows of a
+    pulled-in last block with three covers, (3, 60, 516), on the generic
+    path."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 5)
+    mask = (np.random.default_rng(6).random((h, w)) < 0.05).astype(np.uint8)
+    outs = []
+    prev = lib.sp_blend_packed(-1)
+    try:
+        for v in (1, 0):
+            lib.sp_blend_packed(v)
+            _POOL.clear()
+            u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
+            outs.append(u.data)
+    finally:
+        lib.sp_blend_packed(prev)
+        _POOL.clear()
+    assert np.array_equal(outs[0], outs[1])
