@@ -260,7 +260,8 @@ class _ThreadGather:
 
 
 @pytest.mark.parametrize("shape,dens,P", [((128, 160), 0.05, 2), ((128, 160), 0.004, 3),
-                                          ((301, 256), 0.02, 4), ((97, 64), 0.1, 2)])
+                                          ((301, 256), 0.02, 4), ((97, 64), 0.1, 2),
+                                          ((2160, 3840), 0.05, 2), ((2160, 3840), 0.0024, 3)])
 def test_strip_geometry_bit_identical(shape, dens, P):
     """The row-strip partition of the Delaunay step and the accumulate
     (geometry.StripGeometry: per-strip corner keys merged, per-strip
