@@ -92,55 +92,6 @@ __global__ void k_vi_step(const int* __restrict__ perm, const int* __restrict__ 
   g[k] = g[k] + (T)(tau * s);
 }
 
-// The same VI update with one WARP per cell and all CC channels: the lanes
-// load 32 of the cell's pixels at once (perm, w, f, u) and form the products
-// w (f - u) in double; lane 0 adds them in pixel order from shared memory,
-// so every cell sum is the sequential one of k_vi_step (bit-identical).  The
-// one-thread-per-cell kernel walked each cell alone: 32-byte sectors for 4-8
-// useful bytes, 1.05 GB of DRAM reads per 4K step (profiles/ncu_r02w_k_vi_step).
-template <typename T, int CC>
-__global__ void __launch_bounds__(256) k_vi_step_warp(
-    const int* __restrict__ perm, const int* __restrict__ start, const int* __restrict__ end,
-    const double* __restrict__ w, const T* __restrict__ f, const T* __restrict__ u,
-    const int* __restrict__ sy, const int* __restrict__ sx, int m, int W, size_t n, double tau,
-    T* __restrict__ g) {
-  __shared__ double buf[8][CC][32];
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const long gw0 = (long)blockIdx.x * 8 + wi, gws = (long)gridDim.x * 8;
-  for (long t = gw0; t < m; t += gws) {
-    const int e = end[t];
-    double acc[CC];
-#pragma unroll
-    for (int c = 0; c < CC; ++c) acc[c] = 0.0;
-    for (int i0 = start[t]; i0 < e; i0 += 32) {
-      const int i = i0 + lane;
-      const bool ok = i < e;
-      const int p = ok ? perm[i] : 0;
-      const double wv = ok ? w[p] : 0.0;
-#pragma unroll
-      for (int c = 0; c < CC; ++c)
-        buf[wi][c][lane] = ok ? wv * ((double)f[(size_t)c * n + p] - (double)u[(size_t)c * n + p])
-                              : 0.0;
-      __syncwarp();
-      if (lane == 0) {
-        const int cnt = min(32, e - i0);
-#pragma unroll
-        for (int c = 0; c < CC; ++c)
-          for (int k = 0; k < cnt; ++k) acc[c] += buf[wi][c][k];
-      }
-      __syncwarp();
-    }
-    if (lane == 0) {
-      const size_t pk = (size_t)sy[t] * W + sx[t];
-#pragma unroll
-      for (int c = 0; c < CC; ++c) {
-        const size_t k = (size_t)c * n + pk;
-        g[k] = g[k] + (T)(tau * acc[c]);
-      }
-    }
-  }
-}
-
 // out[plane] = sum x*y (mode 1) / x*x (mode 0) over `len` elements
 template <typename T>
 __global__ void __launch_bounds__(NT) k_plane_dot(const T* __restrict__ x,
@@ -361,18 +312,8 @@ template <typename T>
 int vi_step(const int* perm, const int* start, const int* end, const double* w, const T* f,
             const T* u, const int* sy, const int* sx, long m, int C, int H, int W, double tau,
             T* g, cudaStream_t s) {
-  if (C == 1 || C == 3) {
-    const long ctas = std::min<long>(cdiv(m, 8), (long)num_sms() * 8);
-    if (C == 3)
-      k_vi_step_warp<T, 3><<<ctas, 256, 0, s>>>(perm, start, end, w, f, u, sy, sx, (int)m, W,
+  k_vi_step<T><<<cdiv(m * C, 128), 128, 0, s>>>(perm, start, end, w, f, u, sy, sx, (int)m, C, W,
                                                  (size_t)H * W, tau, g);
-    else
-      k_vi_step_warp<T, 1><<<ctas, 256, 0, s>>>(perm, start, end, w, f, u, sy, sx, (int)m, W,
-                                                 (size_t)H * W, tau, g);
-  } else {
-    k_vi_step<T><<<cdiv(m * C, 128), 128, 0, s>>>(perm, start, end, w, f, u, sy, sx, (int)m, C,
-                                                   W, (size_t)H * W, tau, g);
-  }
   SP_CHECK_LAUNCH();
   return 0;
 }
