@@ -108,3 +108,46 @@ def test_two_rank_pipeline_on_strips(tmp_path):
     assert np.array_equal(r0["m"], mask.indicator)
     assert np.array_equal(r0["g"], st.g.data)
     assert float(r0["mse"]) == st.mse
+
+
+def _nccl_worker(_i, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200.strips import StripSolver
+    try:
+        c, h, w = 3, 512, 768
+        f = O.synth(h, w, c, 2)
+        mask = (np.random.default_rng(3).random((h, w)) < 0.05).astype(np.uint8)
+        s = StripSolver.distributed(h, w, c, transport="nccl")
+        u, rep = s.inpaint(sp.Image(f), sp.Mask(mask))
+        np.savez(os.path.join(out_dir, "nccl.npz"), u=u.data, it=rep.iterations,
+                 handle=int(bool(s._comm.handle.value)))
+        s._comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_bootstrap_single_rank(tmp_path):
+    """The NCCL transport's bootstrap executes on the one GPU: libnccl.so.2
+    dlopen'd by the library, rank 0's unique id broadcast through
+    torch.distributed (nccl backend, world size 1), the communicator created
+    and destroyed around a StripSolver.distributed solve; the result equals
+    the in-process P = 1 strip solve.  (Two NCCL ranks cannot share a GPU:
+    the multi-rank exchanges run under the host-staged transport above.)"""
+    import torch.multiprocessing as mp
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200.strips import StripSolver
+    mp.start_processes(_nccl_worker, args=(_port(), str(tmp_path)), nprocs=1, join=True,
+                       start_method="spawn")
+    r = np.load(os.path.join(tmp_path, "nccl.npz"))
+    assert int(r["handle"]) == 1
+    c, h, w = 3, 512, 768
+    f = O.synth(h, w, c, 2)
+    mask = (np.random.default_rng(3).random((h, w)) < 0.05).astype(np.uint8)
+    u1, rep1 = StripSolver(h, w, c, strips=1).inpaint(sp.Image(f), sp.Mask(mask))
+    assert np.array_equal(r["u"], u1.data)
+    assert int(r["it"]) == rep1.iterations
