@@ -275,6 +275,31 @@ def _cover_tables(starts, size, dim):
     return k0, nn
 
 
+_RAS_GEOM: dict = {}
+
+
+def _ras_geometry(H, W, bh, bw, stride, dev):
+    """The mask-independent RAS block tables of an (H, W) image (block
+    origins, cover tables), host and device copies, cached per geometry --
+    host numpy work and uploads that every ras_tonal call repeated."""
+    key = (H, W, bh, bw, stride, str(dev))
+    g = _RAS_GEOM.get(key)
+    if g is None:
+        if len(_RAS_GEOM) > 8:
+            _RAS_GEOM.clear()
+        ys = _starts(H, bh, stride).astype(np.int32)
+        xs = _starts(W, bw, stride).astype(np.int32)
+        oy_all = np.repeat(ys, xs.size)
+        ox_all = np.tile(xs, ys.size)
+        rk0, rn = _cover_tables(ys, bh, H)
+        ck0, cn = _cover_tables(xs, bw, W)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        g = dict(ys=ys, xs=xs, oy_all=oy_all, ox_all=ox_all, oy_t=t(oy_all), ox_t=t(ox_all),
+                 ys_t=t(ys), xs_t=t(xs), rk0=t(rk0), rn=t(rn), ck0=t(ck0), cn=t(cn))
+        _RAS_GEOM[key] = g
+    return g
+
+
 class _RasBlocks:
     """The 64x64 (block/overlap) decomposition of the tonal RAS, its
     active blocks (>= 1 stored pixel, tonal.py:349-350) as tiles of one
@@ -286,15 +311,13 @@ class _RasBlocks:
         self.H, self.W, self.C = H, W, C
         self.bh, self.bw = min(cfg.block, H), min(cfg.block, W)
         stride = cfg.block - cfg.overlap
-        ys = _starts(H, self.bh, stride).astype(np.int32)
-        xs = _starts(W, self.bw, stride).astype(np.int32)
+        geo = _ras_geometry(H, W, self.bh, self.bw, stride, dev)
+        ys, xs = geo["ys"], geo["xs"]
         self.nby, self.nbx = ys.size, xs.size
         nb = self.nby * self.nbx
-        oy_all = np.repeat(ys, self.nbx)
-        ox_all = np.tile(xs, self.nby)
+        oy_all, ox_all = geo["oy_all"], geo["ox_all"]
         # per-block stored-pixel counts on the device (one pass)
-        oy_t = torch.from_numpy(oy_all).to(dev)
-        ox_t = torch.from_numpy(ox_all).to(dev)
+        oy_t, ox_t = geo["oy_t"], geo["ox_t"]
         mt_all = torch.empty((nb, self.bh, self.bw), dtype=torch.uint8, device=dev)
         call("sp_gather_mask_tiles", ptr(mask_t), ptr(oy_t), ptr(ox_t), nb, H, W, self.bh,
              self.bw, ptr(mt_all), stream())
@@ -314,16 +337,18 @@ class _RasBlocks:
         self.t1 = min(self.nt_all, self.t0 + self.chunk)
         act_loc = act[self.t0:self.t1]
         self.nt = int(act_loc.size)
-        self.oy = torch.from_numpy(oy_all[act_loc].copy()).to(dev)
-        self.ox = torch.from_numpy(ox_all[act_loc].copy()).to(dev)
-        self.tmask = (mt_all[torch.from_numpy(act_loc).to(dev)].contiguous() if self.nt
-                      else mt_all[:0])
-        rk0, rn = _cover_tables(ys, self.bh, H)
-        ck0, cn = _cover_tables(xs, self.bw, W)
-        self.ys_t = torch.from_numpy(ys).to(dev)
-        self.xs_t = torch.from_numpy(xs).to(dev)
-        self.rk0, self.rn = torch.from_numpy(rk0).to(dev), torch.from_numpy(rn).to(dev)
-        self.ck0, self.cn = torch.from_numpy(ck0).to(dev), torch.from_numpy(cn).to(dev)
+        if self.nt == nb:
+            # every block holds a stored pixel (the usual case at a few %
+            # density): the cached origins and the gathered masks as they are
+            self.oy, self.ox, self.tmask = oy_t, ox_t, mt_all
+        else:
+            self.oy = torch.from_numpy(oy_all[act_loc].copy()).to(dev)
+            self.ox = torch.from_numpy(ox_all[act_loc].copy()).to(dev)
+            self.tmask = (mt_all[torch.from_numpy(act_loc).to(dev)].contiguous() if self.nt
+                          else mt_all[:0])
+        self.ys_t, self.xs_t = geo["ys_t"], geo["xs_t"]
+        self.rk0, self.rn = geo["rk0"], geo["rn"]
+        self.ck0, self.cn = geo["ck0"], geo["cn"]
         self.dtype = solver.cfg.torch_dtype
         self.inner_cycles = cfg.inner_cycles
         self.tol = cfg.inner_tol if cfg.inner_tol is not None else cfg.local_product_tol

@@ -28,3 +28,13 @@ for gl in (0, 1, 0, 1):
         dt = (time.perf_counter() - t) / 5 * 1e3
         print(f"graph_loop={gl} tol={tol}: {dt:.3f} ms/solve, {rep2.iterations} V-cycles "
               f"({dt / max(1, rep2.iterations):.3f} ms/cycle)", flush=True)
+        # the same number of V-cycles without tolerance tests
+        n = rep2.iterations
+        hier.solve_sym(bsym, init=ut, tol=None, cycles=n)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(5):
+            hier.solve_sym(bsym, init=ut, tol=None, cycles=n)
+        torch.cuda.synchronize()
+        dt2 = (time.perf_counter() - t) / 5 * 1e3
+        print(f"graph_loop={gl} fixed {n} cycles: {dt2:.3f} ms/solve", flush=True)
