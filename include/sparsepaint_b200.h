@@ -114,6 +114,10 @@ int sp_chan_reduce(int dtype, int mode, const void* x, const void* y, const doub
 /* e = sum_c (u_c - f_c)^2 in double, f double (spatial.py:184-186 _error_map) */
 int sp_error_map(int dtype, const void* u, const double* f, double* e, int C, long n,
                  void* stream);
+/* sp_error_map plus *total = sum of e (device double; the MSE numerator of
+ * grid.py:188-193, summed in a fixed order) in the same pass */
+int sp_error_map_sum(int dtype, const void* u, const double* f, double* e, int C, long n,
+                     double* total, void* stream);
 
 /* ======================= B2: device-resident solver ====================== */
 
@@ -375,6 +379,11 @@ int sp_ws_stages(int v);
  * pyramid (1, default) or load and test their mask bytes (0); bit-identical.
  * v < 0 queries.  A/B aid, no reference counterpart. */
 int sp_oras_offbits(int v);
+/* One-image tolerance solves form ||b~||^2 (the tolerance scale,
+ * solver.py:351-352) in the masked_sym_rhs pass (1, default) or by a
+ * separate reduction (0); the sums group differently (rounding only).
+ * v < 0 queries. */
+int sp_fused_bnorm(int v);
 /* C = 3 float blend: 1 = packed per-row / per-column cover words (one table
  * load each, default), 0 = the cover-table chains; bit-identical.  v < 0
  * queries.  A/B aid, no reference counterpart. */

@@ -43,6 +43,7 @@ _SIGS = {
     "sp_enforce": [c_int, P, P, P, c_int, c_int, c_int, c_int, P],
     "sp_chan_reduce": [c_int, c_int, P, P, P, c_long, c_int, P, P],
     "sp_error_map": [c_int, P, P, P, c_int, c_long, P],
+    "sp_error_map_sum": [c_int, P, P, P, c_int, c_long, P, P],
     "sp_hier_create": [P, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                        c_double, c_double, c_int, c_int],
     "sp_hier_destroy": [P],
@@ -111,6 +112,7 @@ _SIGS = {
     "sp_ws_prefetch": [c_int],
     "sp_ws_stages": [c_int],
     "sp_oras_offbits": [c_int],
+    "sp_fused_bnorm": [c_int],
     "sp_blend_packed": [c_int],
     "sp_tile_fused": [c_int],
     "sp_channel_parallel": [c_int],

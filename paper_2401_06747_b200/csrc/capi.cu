@@ -245,6 +245,13 @@ int sp_error_map(int dtype, const void* u, const double* f, double* e, int C, lo
            error_map<double>((const double*)u, f, e, C, (size_t)n, STREAM(s)));
 }
 
+// the error map and its total (the MSE numerator) in one pass
+int sp_error_map_sum(int dtype, const void* u, const double* f, double* e, int C, long n,
+                     double* total, void* s) {
+  DISPATCH(dtype, error_map<float>((const float*)u, f, e, C, (size_t)n, STREAM(s), total),
+           error_map<double>((const double*)u, f, e, C, (size_t)n, STREAM(s), total));
+}
+
 // ---- B2: device-resident hierarchy (solver.py:205-372) ----------------------
 
 int sp_hier_create(void** out, int dtype, int C, int H, int W, int block, int overlap,
@@ -562,6 +569,8 @@ extern "C" int sp_ws_variant(int v) { return sp::ws_variant(v); }
 extern "C" int sp_ws_prefetch(int v) { return sp::ws_prefetch(v); }
 extern "C" int sp_ws_stages(int v) { return sp::ws_stages(v); }
 extern "C" int sp_oras_offbits(int v) { return sp::oras_offbits(v); }
+namespace sp { int fused_bnorm(int v); }
+extern "C" int sp_fused_bnorm(int v) { return sp::fused_bnorm(v); }
 extern "C" int sp_blend_packed(int v) { return sp::blend_packed(v); }
 namespace sp { int tile_fused(int v); int channel_parallel(int v); int graph_loop(int v); }
 extern "C" int sp_tile_fused(int v) { return sp::tile_fused(v); }

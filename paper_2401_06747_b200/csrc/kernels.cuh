@@ -12,7 +12,9 @@ template <typename T> int sym_matvec(const T* x, const uint8_t* m, T* out, int C
 template <typename T> int sym_rhs(const T* b, const uint8_t* m, T* out, T* e, int C, int H, int W, double inv_h2, cudaStream_t s, int ntile = 1, const int* active = nullptr);
 // b~ = sym_rhs(where(m, x, 0)); enforce_u (optional): u = b~ on the stored
 // pixels in the same pass (sparse stores)
-template <typename T> int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s, int ntile = 1, const int* active = nullptr, T* enforce_u = nullptr);
+// nrm (one image): also *nrm = sum of out^2 over all planes in the same pass
+// (partial: >= 4096 doubles, counter: zeroed)
+template <typename T> int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s, int ntile = 1, const int* active = nullptr, T* enforce_u = nullptr, double* nrm = nullptr, double* partial = nullptr, unsigned* counter = nullptr);
 template <typename T> int ct_apply(const T* w, const uint8_t* m, T* out, int C, int H, int W, double inv_h2, cudaStream_t s, int ntile = 1, const int* active = nullptr);
 size_t residual_partials(int H, int W);
 template <typename T> int residual(const T* u, const T* b, const uint8_t* m, T* r, double* partial, unsigned* counter, double* norms, int C, int H, int W, double inv_h2, cudaStream_t s, int ntile = 1, const int* active = nullptr);
@@ -98,6 +100,7 @@ template <typename T>
 int chan_reduce(int mode, const T* x, const T* y, const double* z, size_t n, int C,
                 double* partial, unsigned* counter, double* out, cudaStream_t s);
 template <typename T>
-int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStream_t s);
+int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStream_t s,
+              double* total = nullptr);  // total: sum of e (deterministic), optional
 
 }  // namespace sp

@@ -24,6 +24,7 @@ namespace {
 
 constexpr int BX = 32, BY = 8, NT = BX * BY;
 constexpr long kTargetCtas = 2 * 148 * 8;
+constexpr size_t kNrmSlots = 4096;  // partial slots of the fused ||b~||^2 (>= the grid)
 
 struct PlaneTiles {
   int ntx, nty;
@@ -522,17 +523,25 @@ __global__ void __launch_bounds__(NT) k4_residual(
 }
 
 // mode 0: sym_rhs (+ optional e); 1: masked_sym_rhs; 2: ct_apply
-template <typename T, int MODE>
+// NRM (one image, MODE 1): also the sum of out^2 over all planes -- the
+// ||b~||^2 of the solve's tolerance scale (solver.py:351-352) -- in the same
+// pass: per-thread double sums, CTA partials in grid order, the last CTA of
+// the grid adds them in index order (deterministic)
+template <typename T, int MODE, bool NRM = false>
 __global__ void __launch_bounds__(NT) k4_rhs(const T* __restrict__ xin,
                                              const uint8_t* __restrict__ m,
                                              T* __restrict__ out, T* __restrict__ e, int C,
                                              int H, int W, double inv_h2,
-                                             const int* __restrict__ active) {
+                                             const int* __restrict__ active,
+                                             double* __restrict__ partial,
+                                             unsigned* __restrict__ counter,
+                                             double* __restrict__ nrm) {
   pdl_enter();
   PLANE_SETUP(C);
   const size_t plane = (size_t)H * W, vo = (size_t)z * plane;
   m += (size_t)tile * plane;
   const T* xc = xin + vo;
+  double nacc = 0.0;
   FOR_QUADS(H, W) {
     if (x0 >= W || y >= H) continue;
     size_t k = (size_t)y * W + x0;
@@ -555,6 +564,32 @@ __global__ void __launch_bounds__(NT) k4_rhs(const T* __restrict__ xin,
     }
     st4(out + vo + k, o);
     if (MODE == 0 && e) st4(e + vo + k, ee);
+    if (NRM) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) nacc += (double)o.a[i] * (double)o.a[i];
+    }
+  }
+  if (!NRM) return;
+  __shared__ double s0[NT / 32];
+  __shared__ bool am_last;
+  const unsigned ncta = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+  const double sb = cta_sum<NT>(nacc, s0);
+  const int tid = threadIdx.y * BX + threadIdx.x;
+  if (tid == 0) {
+    partial[cta] = sb;
+    __threadfence();
+    am_last = atomicAdd(counter, 1u) == ncta - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned i = tid; i < ncta; i += NT) t += ((volatile double*)partial)[i];
+  __syncthreads();
+  t = cta_sum<NT>(t, s0);
+  if (tid == 0) {
+    *nrm = t;
+    *counter = 0u;
   }
 }
 
@@ -691,7 +726,8 @@ int sym_rhs(const T* b, const uint8_t* m, T* out, T* e, int C, int H, int W, dou
             cudaStream_t s, int ntile, const int* active) {
   long nz = (long)ntile * C;
   if (VEC_OK(b, m, out, e))
-    SP_CUDA(launch_k(k4_rhs<T, 0>, mg_grid4(H, W, nz), kBlock, 0, s, b, m, out, e, C, H, W, inv_h2, active));
+    SP_CUDA(launch_k(k4_rhs<T, 0>, mg_grid4(H, W, nz), kBlock, 0, s, b, m, out, e, C, H, W, inv_h2, active,
+                     (double*)nullptr, (unsigned*)nullptr, (double*)nullptr));
   else
     SP_CUDA(launch_k(k_sym_rhs<T>, mg_grid(H, W, nz), kBlock, 0, s, b, m, out, e, C, H, W, inv_h2, active));
   SP_CHECK_LAUNCH();
@@ -700,11 +736,26 @@ int sym_rhs(const T* b, const uint8_t* m, T* out, T* e, int C, int H, int W, dou
 
 template <typename T>
 int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cudaStream_t s,
-                   int ntile, const int* active, T* enforce_u) {
+                   int ntile, const int* active, T* enforce_u, double* nrm, double* partial,
+                   unsigned* counter) {
   long nz = (long)ntile * C;
+  if (nrm && !(ntile == 1 && VEC_OK(x, m, out) && partial && counter)) {
+    set_error("fused ||b~||^2: one image, aligned quads");
+    return -2;
+  }
   if (VEC_OK(x, m, out)) {
-    SP_CUDA(launch_k(k4_rhs<T, 1>, mg_grid4(H, W, nz), kBlock, 0, s, x, m, out, enforce_u, C, H,
-                     W, 1.0, active));
+    const dim3 g = mg_grid4(H, W, nz);
+    if (nrm) {
+      if ((size_t)g.x * g.y > kNrmSlots) {
+        set_error("fused ||b~||^2: %u CTAs exceed the partial slots", g.x * g.y);
+        return -2;
+      }
+      SP_CUDA(launch_k(k4_rhs<T, 1, true>, g, kBlock, 0, s, x, m, out, enforce_u, C, H, W, 1.0,
+                       active, partial, counter, nrm));
+    } else {
+      SP_CUDA(launch_k(k4_rhs<T, 1>, g, kBlock, 0, s, x, m, out, enforce_u, C, H, W, 1.0, active,
+                       (double*)nullptr, (unsigned*)nullptr, (double*)nullptr));
+    }
   } else {
     k_masked_sym_rhs<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(x, m, out, C, H, W, active);
     if (enforce_u) {
@@ -722,7 +773,7 @@ int ct_apply(const T* w, const uint8_t* m, T* out, int C, int H, int W, double i
   long nz = (long)ntile * C;
   if (VEC_OK(w, m, out))
     SP_CUDA(launch_k(k4_rhs<T, 2>, mg_grid4(H, W, nz), kBlock, 0, s, w, m, out, nullptr, C, H, W, inv_h2,
-                                                       active));
+                     active, (double*)nullptr, (unsigned*)nullptr, (double*)nullptr));
   else
     k_ct_apply<T><<<mg_grid(H, W, nz), kBlock, 0, s>>>(w, m, out, C, H, W, inv_h2, active);
   SP_CHECK_LAUNCH();
@@ -797,7 +848,8 @@ int enforce(T* u, const T* src, const uint8_t* m, int C, int H, int W, int zero_
   template int sym_rhs<T>(const T*, const uint8_t*, T*, T*, int, int, int, double,         \
                           cudaStream_t, int, const int*);                                  \
   template int masked_sym_rhs<T>(const T*, const uint8_t*, T*, int, int, int,              \
-                                 cudaStream_t, int, const int*, T*);                       \
+                                 cudaStream_t, int, const int*, T*, double*, double*,      \
+                                 unsigned*);                                               \
   template int ct_apply<T>(const T*, const uint8_t*, T*, int, int, int, double,            \
                            cudaStream_t, int, const int*);                                 \
   template int residual<T>(const T*, const T*, const uint8_t*, T*, double*, unsigned*,     \

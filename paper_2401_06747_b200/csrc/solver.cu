@@ -23,6 +23,14 @@
 
 namespace sp {
 
+// one-image tolerance solves take ||b~||^2 from the masked_sym_rhs pass (1)
+// or from a separate reduction of b~ (0): sp_fused_bnorm
+static int fused_bnorm_on = 1;
+int fused_bnorm(int v) {
+  if (v >= 0) fused_bnorm_on = v;
+  return fused_bnorm_on;
+}
+
 // sweep kernels of new hierarchies (sp_march_variant): 2 = TMA-staged
 // residual sweeps (default), 1 = row-marching register kernels, 0 = the
 // per-pixel kernels everywhere.  The row-strip solver always uses the
@@ -199,7 +207,10 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
     hh = (hh + 1) / 2;
     ww = (ww + 1) / 2;
   }
-  size_t scratch = sizeof(double) * (1024 + 8) * (size_t)ntile + 256;
+  // reduction partials: 1024 per tile (4096 for one image: the fused
+  // ||b~||^2 of masked_sym_rhs), the norms and a counter behind them
+  const size_t nslot = ntile == 1 ? 4096 : 1024;
+  size_t scratch = sizeof(double) * (nslot + 8) * (size_t)ntile + 256;
   if (cudaMallocHost((void**)&h->h_norms, sizeof(double) * ntc) != cudaSuccess ||
       cudaMallocHost((void**)&h->h_active, sizeof(int) * ntile) != cudaSuccess ||
       cudaMallocHost(&h->h_loop, 4096) != cudaSuccess ||
@@ -683,11 +694,24 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
   } else {
     SP_CUDA(cudaMemsetAsync(L0.u, 0, sizeof(T) * n, s));
   }
+  // scratch layout: partials [nslot * nt], then ||b~||^2 [nt], then a counter
+  const size_t nslot = nt == 1 ? 4096 : 1024;
+  double* part = (double*)h->d_scratch;
+  double* bn = part + nslot * (size_t)nt;
+  unsigned* counter = (unsigned*)(bn + nt);
+  bool bn_done = false;
   if (src_mode == 1) {
     // b~ = sym_rhs(where(mask, x, 0)) straight into level 0, u = b~ on the
-    // mask in the same pass
+    // mask in the same pass -- and, for a tolerance solve of one image,
+    // ||b~||^2 of the tolerance scale (solver.py:351-352) too
+    const bool fuse = tol >= 0 && nt == 1 && sizeof(T) == 4 && fused_bnorm_on &&
+                      L0.W % 4 == 0 &&
+                      (((uintptr_t)bsym | (uintptr_t)L0.b | (uintptr_t)L0.mask) & 15u) == 0;
+    if (fuse) SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
     SP_TRY(masked_sym_rhs<T>(bsym, L0.mask, (T*)L0.b, C, L0.H, L0.W, s, nt, h->d_active,
-                             (T*)L0.u));
+                             (T*)L0.u, fuse ? bn : nullptr, fuse ? part : nullptr,
+                             fuse ? counter : nullptr));
+    bn_done = fuse;
   } else {
     SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
     SP_TRY(enforce<T>((T*)L0.u, (const T*)L0.b, L0.mask, C, L0.H, L0.W, 0, s, nt, h->d_active));
@@ -706,11 +730,10 @@ static int solve_t(Hier* h, const T* bsym, T* u_io, int init_mode, double tol, i
     if (rep) { rep->iterations = cycles; rep->converged = 1; }
   } else {
     // solver.py:351-369, per tile: ||b~|| over all channels of the tile
-    double* part = (double*)h->d_scratch;
-    double* bn = part + 1024 * (size_t)nt;
-    unsigned* counter = (unsigned*)(bn + nt);
-    SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
-    SP_TRY(chan_reduce<T>(0, (const T*)L0.b, nullptr, nullptr, per, nt, part, counter, bn, s));
+    if (!bn_done) {
+      SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
+      SP_TRY(chan_reduce<T>(0, (const T*)L0.b, nullptr, nullptr, per, nt, part, counter, bn, s));
+    }
     if (nt == 1 && h->use_graphs && graph_loop_on && h->h_loop) {
       SP_TRY(solve_loop_t<T>(h, tol, max_cycles, bn, s, done.data(), cv.data(), rep));
       count_work(0, (long long)done[0] * L0.H * L0.W);

@@ -127,14 +127,70 @@ __global__ void k_error_map(const T* __restrict__ u, const double* __restrict__ 
   e[i] = acc;
 }
 
+// the same error map plus its total sum_p e_p (the MSE numerator,
+// grid.py:188-193) in the same pass: grid-stride CTAs, double per-thread
+// sums, CTA partials added in index order by the last CTA (deterministic);
+// saves the separate f64 / u re-read of the MSE reduction
 template <typename T>
-int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStream_t s) {
-  k_error_map<T><<<cdiv(n, 256), 256, 0, s>>>(u, f, e, C, n);
+__global__ void __launch_bounds__(NT) k_error_map_sum(const T* __restrict__ u,
+                                                      const double* __restrict__ f,
+                                                      double* __restrict__ e, int C, size_t n,
+                                                      double* __restrict__ partial,
+                                                      unsigned* __restrict__ counter,
+                                                      double* __restrict__ total) {
+  __shared__ double s0[NT / 32];
+  __shared__ bool am_last;
+  double tacc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * NT + threadIdx.x; i < n; i += (size_t)gridDim.x * NT) {
+    double acc = 0.0;
+    for (int c = 0; c < C; ++c) {
+      double d = (double)u[(size_t)c * n + i] - f[(size_t)c * n + i];
+      double sq = d * d;
+      acc = c == 0 ? sq : acc + sq;
+    }
+    e[i] = acc;
+    tacc += acc;
+  }
+  const double sblk = cta_sum<NT>(tacc, s0);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = sblk;
+    __threadfence();
+    am_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += NT) t += ((volatile double*)partial)[i];
+  __syncthreads();
+  t = cta_sum<NT>(t, s0);
+  if (threadIdx.x == 0) {
+    *total = t;
+    *counter = 0u;
+  }
+}
+
+template <typename T>
+int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStream_t s,
+              double* total) {
+  if (!total) {
+    k_error_map<T><<<cdiv(n, 256), 256, 0, s>>>(u, f, e, C, n);
+    SP_CHECK_LAUNCH();
+    return 0;
+  }
+  const int nb = nblocks_for(n);
+  Scratch scr(s);
+  SP_TRY(scr.alloc(sizeof(double) * nb + 64));
+  unsigned* counter = (unsigned*)((double*)scr.p + nb);
+  SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
+  k_error_map_sum<T><<<nb, NT, 0, s>>>(u, f, e, C, n, (double*)scr.p, counter, total);
   SP_CHECK_LAUNCH();
   return 0;
 }
-template int error_map<float>(const float*, const double*, double*, int, size_t, cudaStream_t);
-template int error_map<double>(const double*, const double*, double*, int, size_t, cudaStream_t);
+template int error_map<float>(const float*, const double*, double*, int, size_t, cudaStream_t,
+                              double*);
+template int error_map<double>(const double*, const double*, double*, int, size_t, cudaStream_t,
+                               double*);
 
 template int dot_self<float>(const float*, size_t, double*, unsigned*, double*, cudaStream_t);
 template int dot_self<double>(const double*, size_t, double*, unsigned*, double*, cudaStream_t);

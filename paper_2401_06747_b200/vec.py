@@ -47,9 +47,15 @@ def mse_t(a, b) -> float:
     return float(sq_err(x, b).item()) / max(1, x.numel())
 
 
-def error_map(u, f64):
-    """spatial.py:184-186: sum_c (u - f)^2 in double -> (H, W)."""
+def error_map(u, f64, with_sum=False):
+    """spatial.py:184-186: sum_c (u - f)^2 in double -> (H, W).  with_sum:
+    also the total of the map (a device double, the MSE numerator) from the
+    same pass."""
     C, H, W = u.shape
     e = torch.empty((H, W), dtype=torch.float64, device=u.device)
-    call("sp_error_map", dcode(u), ptr(u), ptr(f64), ptr(e), C, H * W, stream())
-    return e
+    if not with_sum:
+        call("sp_error_map", dcode(u), ptr(u), ptr(f64), ptr(e), C, H * W, stream())
+        return e
+    tot = torch.empty((), dtype=torch.float64, device=u.device)
+    call("sp_error_map_sum", dcode(u), ptr(u), ptr(f64), ptr(e), C, H * W, ptr(tot), stream())
+    return e, tot
