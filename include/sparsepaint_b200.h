@@ -108,7 +108,8 @@ int sp_enforce(int dtype, void* u, const void* src, const uint8_t* mask, int C, 
 
 /* deterministic per-channel reductions over C planes of n elements; out is a
  * device double[C].  mode 0: sum x^2, 1: sum x*y, 2: sum (x - z)^2 with z a
- * double array (tonal.py:86-97 _mse/_chan_dot, grid.py:188-193 quality) */
+ * double array, 3: sum (x - y)^2 with y of x's dtype (tonal.py:86-97
+ * _mse/_chan_dot, grid.py:188-193 quality) */
 int sp_chan_reduce(int dtype, int mode, const void* x, const void* y, const double* z, long n,
                    int C, double* out, void* stream);
 /* e = sum_c (u_c - f_c)^2 in double, f double (spatial.py:184-186 _error_map) */
@@ -379,6 +380,10 @@ int sp_ws_stages(int v);
  * pyramid (1, default) or load and test their mask bytes (0); bit-identical.
  * v < 0 queries.  A/B aid, no reference counterpart. */
 int sp_oras_offbits(int v);
+/* Fused RAS block solves of a partly active batch launch their grids over
+ * the list of active blocks (1, default) or over every block with early
+ * exits (0); identical results.  v < 0 queries. */
+int sp_tile_list(int v);
 /* One-image tolerance solves form ||b~||^2 (the tolerance scale,
  * solver.py:351-352) in the masked_sym_rhs pass (1, default) or by a
  * separate reduction (0); the sums group differently (rounding only).

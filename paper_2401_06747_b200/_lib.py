@@ -112,6 +112,7 @@ _SIGS = {
     "sp_ws_prefetch": [c_int],
     "sp_ws_stages": [c_int],
     "sp_oras_offbits": [c_int],
+    "sp_tile_list": [c_int],
     "sp_fused_bnorm": [c_int],
     "sp_blend_packed": [c_int],
     "sp_tile_fused": [c_int],

@@ -225,7 +225,8 @@ int sp_enforce(int dtype, void* u, const void* src, const uint8_t* m, int C, int
 }
 
 // ---- vector reductions (deterministic; tonal.py:86-97, grid.py:188-193) ------
-// mode 0: out[c] = sum x_c^2; 1: sum x_c*y_c; 2: sum (x_c - z_c)^2 (z double)
+// mode 0: out[c] = sum x_c^2; 1: sum x_c*y_c; 2: sum (x_c - z_c)^2 (z double);
+// 3: sum (x_c - y_c)^2 (y of x's dtype)
 int sp_chan_reduce(int dtype, int mode, const void* x, const void* y, const double* z, long n,
                    int C, double* out, void* s) {
   cudaStream_t st = STREAM(s);
@@ -569,6 +570,8 @@ extern "C" int sp_ws_variant(int v) { return sp::ws_variant(v); }
 extern "C" int sp_ws_prefetch(int v) { return sp::ws_prefetch(v); }
 extern "C" int sp_ws_stages(int v) { return sp::ws_stages(v); }
 extern "C" int sp_oras_offbits(int v) { return sp::oras_offbits(v); }
+namespace sp { int tile_list(int v); }
+extern "C" int sp_tile_list(int v) { return sp::tile_list(v); }
 namespace sp { int fused_bnorm(int v); }
 extern "C" int sp_fused_bnorm(int v) { return sp::fused_bnorm(v); }
 extern "C" int sp_blend_packed(int v) { return sp::blend_packed(v); }

@@ -33,8 +33,10 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile = 1, const int* active = nullptr,
                       int stride = 0, int corr_nb = 0, size_t ps = 0,
-                      const int* wdelta = nullptr, const uint32_t* offbits = nullptr);
+                      const int* wdelta = nullptr, const uint32_t* offbits = nullptr,
+                      const int* tile_list = nullptr, int nlist = 0);
 int oras_offbits(int v);  // sp_oras_offbits
+int oras_variant(int v);  // the ORAS local-CG kernel (sp_oras_variant)
 // per-job row-mask words of the ORAS blocks ([ntile][nb][32], see Level)
 int oras_offbits_launch(const uint8_t* m, const int* ys, const int* xs, int nby, int nbx, int bh,
                         int bw, int H, int W, int ntile, uint32_t* offbits, cudaStream_t s);

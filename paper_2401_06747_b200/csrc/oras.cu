@@ -505,7 +505,8 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const int* __restrict__ xs, int nbx, int nbl, int bh, int bw, int H, int W, int stride,
     float closure, long cap, float inv_h2, const float* __restrict__ weights,
     float* __restrict__ corr, const int* __restrict__ active, int corr_nb, size_t ps,
-    const int* __restrict__ wdelta, const uint32_t* __restrict__ offbits) {
+    const int* __restrict__ wdelta, const uint32_t* __restrict__ offbits,
+    const int* __restrict__ tile_list) {
   pdl_enter();
   // FULLH: a full 32 x 32 block (bh == bw == 32): compile-time row / column
   // offsets in the job's loads and stores
@@ -516,7 +517,8 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
   }
   const int j = threadIdx.x & 31;
   const int bi = blockIdx.x * WJ + (threadIdx.x >> 5), ch = blockIdx.y, C = gridDim.y;
-  const int tile = blockIdx.z;
+  // tile_list: the grid covers only the listed tiles (a compacted active set)
+  const int tile = tile_list ? tile_list[blockIdx.z] : blockIdx.z;
   if (bi >= nbl) return;
   if (active && !active[tile]) return;
   const int nb = corr_nb > 0 ? corr_nb : nbl;
@@ -1145,7 +1147,12 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
                       const int* ys, const int* xs, int nby, int nbx, int bh, int bw, int H,
                       int W, int C, double gamma, long cap, double inv_h2, const T* weights,
                       T* corr, cudaStream_t s, int ntile, const int* active, int stride,
-                      int corr_nb, size_t ps, const int* wdelta, const uint32_t* offbits) {
+                      int corr_nb, size_t ps, const int* wdelta, const uint32_t* offbits,
+                      const int* tile_list, int nlist) {
+  if (tile_list && !(sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel >= 6)) {
+    set_error("tile lists need the one-warp float ORAS kernel");
+    return -2;
+  }
   const int npx = bh * bw;
   if (ps && ps != (size_t)H * W &&
       !(sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
@@ -1168,7 +1175,7 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
     // slot at once instead of waiting for the CTA's slowest job); 7: 6 with
     // the lean local CG (warp_cg32_fast)
     const int wj = oras_kernel == 4 ? WJ : 1;
-    dim3 g4(cdiv(nbl, wj), C, ntile);
+    dim3 g4(cdiv(nbl, wj), C, tile_list ? nlist : ntile);
 #define SP_WARP(WJN, F)                                                                   \
   (unit ? (full ? k_oras_warp<true, true, WJN, F> : k_oras_warp<true, false, WJN, F>)     \
         : (full ? k_oras_warp<false, true, WJN, F> : k_oras_warp<false, false, WJN, F>))
@@ -1179,12 +1186,12 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
       SP_CUDA(launch_k(kern, g4, dim3(wj * 32), 0, s, (const float*)r, m, tau_src, tau_scale, ys,
                        xs, nbx, nbl, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
                        (float)inv_h2, (const float*)weights, (float*)corr, active, corr_nb, ps,
-                       wdelta, corr_nb > 0 || !offbits_on ? nullptr : offbits));
+                       wdelta, corr_nb > 0 || !offbits_on ? nullptr : offbits, tile_list));
     } else {
       kern<<<g4, wj * 32, 0, s>>>((const float*)r, m, tau_src, tau_scale, ys, xs, nbx, nbl, bh,
                                   bw, H, W, stride, (float)(1.0 - gamma), cap, (float)inv_h2,
                                   (const float*)weights, (float*)corr, active, corr_nb, ps,
-                                  wdelta, nullptr);
+                                  wdelta, nullptr, nullptr);
     }
   } else if (sizeof(T) == 4 && bw <= 32 && bh <= 32 && oras_kernel != 1) {
     auto kern = inv_h2 == 1.0 ? k_oras_rows<true> : k_oras_rows<false>;
@@ -1352,7 +1359,7 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
                                     const int*, const int*, int, int, int, int, int, int,   \
                                     int, double, long, double, const T*, T*, cudaStream_t,  \
                                     int, const int*, int, int, size_t, const int*,          \
-                                    const uint32_t*);                                       \
+                                    const uint32_t*, const int*, int);                      \
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
                                     int, int, int, cudaStream_t, int, const int*, int,      \

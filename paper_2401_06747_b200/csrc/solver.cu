@@ -86,6 +86,9 @@ Hier::~Hier() {
   }
   if (d_active) cudaFree(d_active);
   if (d_scratch) cudaFree(d_scratch);
+  if (d_list) cudaFree(d_list);
+  if (h_list) cudaFreeHost(h_list);
+  if (list_ev) cudaEventDestroy(list_ev);
   if (h_norms) cudaFreeHost(h_norms);
   if (h_active) cudaFreeHost(h_active);
 }

@@ -68,6 +68,10 @@ struct Hier {
   void* loop_ctl = nullptr;
   void* h_loop = nullptr;       // pinned copy of loop_ctl (read back once)
   long long loop_nodes = 0;
+  // compacted active-tile list of the fused tile solves (tilesolve.cu)
+  int* d_list = nullptr;
+  int* h_list = nullptr;       // pinned
+  cudaEvent_t list_ev = nullptr;
   std::vector<Hier*> chv;
   std::vector<cudaStream_t> ch_streams;
   std::vector<cudaEvent_t> ch_events;

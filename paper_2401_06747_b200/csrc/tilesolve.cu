@@ -62,6 +62,7 @@ struct TV {
   int* active;           // [tile]
   int *done, *conv;      // [tile]
   int* live;             // live-block counter of the last stop test
+  const int* list;       // the grid covers these tiles (compacted active set) or null
   int C, H0, W0, H1, W1, bh0, bw0, nby0, nbx0, stride;
   double tol;
   int max_cycles;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(PT) k_tv_init(TV a) {
   __shared__ uint8_t M[TMAX * TMAX];
   __shared__ double buf[PT / 32];
   __shared__ double nrm[8];
-  const int tile = blockIdx.x;
+  const int tile = a.list ? a.list[blockIdx.x] : blockIdx.x;
   if (!a.active[tile]) return;
   const int H0 = TH0 ? TH0 : a.H0, W0 = TW0 ? TW0 : a.W0;
   const int H1 = TH1 ? TH1 : a.H1, W1 = TW1 ? TW1 : a.W1;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(PT) k_tv_down(TV a) {
   __shared__ float R1[CMAX], B1[CMAX], U1[CMAX];
   __shared__ uint8_t M1[CMAX];
   __shared__ double buf[PT / 32];
-  const int tile = blockIdx.x;
+  const int tile = a.list ? a.list[blockIdx.x] : blockIdx.x;
   if (!a.active[tile]) return;
   const int H0 = TH0 ? TH0 : a.H0, W0 = TW0 ? TW0 : a.W0;
   const int H1 = TH1 ? TH1 : a.H1, W1 = TW1 ? TW1 : a.W1;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(PT) k_tv_coarse(TV a) {
   __shared__ float U1[CMAX];
   __shared__ uint8_t M1[CMAX];
   __shared__ double buf[PT / 32];
-  const int tile = blockIdx.x;
+  const int tile = a.list ? a.list[blockIdx.x] : blockIdx.x;
   if (!a.active[tile]) return;
   const int H0 = TH0 ? TH0 : a.H0, W0 = TW0 ? TW0 : a.W0;
   const int H1 = TH1 ? TH1 : a.H1, W1 = TW1 ? TW1 : a.W1;
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(PT, 4) k_tv_up(TV a) {
   __shared__ uint8_t M[TMAX * TMAX];
   __shared__ float U1[CMAX];
   __shared__ double buf[PT / 32];
-  const int tile = blockIdx.x;
+  const int tile = a.list ? a.list[blockIdx.x] : blockIdx.x;
   if (!a.active[tile]) return;
   const int H0 = TH0 ? TH0 : a.H0, W0 = TW0 ? TW0 : a.W0;
   const int H1 = TH1 ? TH1 : a.H1, W1 = TW1 ? TW1 : a.W1;
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(PT) k_tv_close(TV a) {
   __shared__ uint8_t M[TMAX * TMAX];
   __shared__ double buf[PT / 32];
   __shared__ double nrm[8];
-  const int tile = blockIdx.x;
+  const int tile = a.list ? a.list[blockIdx.x] : blockIdx.x;
   if (!a.active[tile]) return;
   const int H0 = TH0 ? TH0 : a.H0, W0 = TW0 ? TW0 : a.W0;
   const int H1 = TH1 ? TH1 : a.H1, W1 = TW1 ? TW1 : a.W1;
@@ -414,6 +415,14 @@ __global__ void __launch_bounds__(PT) k_tv_close(TV a) {
 
 }  // namespace
 
+// partly active batches launch over the list of active tiles (1) or over
+// every tile with early exits (0): sp_tile_list
+static int tile_list_on = 1;
+int tile_list(int v) {
+  if (v >= 0) tile_list_on = v;
+  return tile_list_on;
+}
+
 bool tile_fused_ok(const Hier* h) {
   if (!tile_fused_on || h->dtype != SP_F32 || h->lv.size() != 2) return false;
   if (h->C < 1 || h->C > 8 || h->cfg.pre != 1 || h->cfg.post != 1) return false;
@@ -434,19 +443,45 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
   // the pinned flags may still feed an earlier upload (waits for that copy
   // only, not for the caller's queued work)
   SP_TRY(active_host_ready(h));
-  for (int t = 0; t < nt; ++t) h->h_active[t] = active_in ? (active_in[t] != 0) : 1;
+  int nact = 0;
+  for (int t = 0; t < nt; ++t) {
+    h->h_active[t] = active_in ? (active_in[t] != 0) : 1;
+    nact += h->h_active[t];
+  }
   SP_TRY(upload_active(h, s));
-  SP_CUDA(cudaMemcpyAsync(L0.b, bsym, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+  // the block kernels read b~ straight from the caller's batch ([nt][C][h][w],
+  // the level-0 layout): no staging copy
+  // a partly active batch (the tail of the RAS local CG: a few blocks still
+  // iterating) launches its grids over the list of active tiles only -- the
+  // full-size grids of early-exiting CTAs cost ~1 ms per solve at 4K
+  const int* list = nullptr;
+  int ngrid = nt;
+  if (nact < nt && tile_list_on && oras_variant(-1) >= 6) {  // one-warp ORAS jobs
+    if (!h->d_list) SP_CUDA(cudaMalloc(&h->d_list, sizeof(int) * nt));
+    if (!h->h_list) SP_CUDA(cudaMallocHost(&h->h_list, sizeof(int) * nt));
+    // the pinned list may still feed the previous solve's upload
+    if (h->list_ev) SP_CUDA(cudaEventSynchronize(h->list_ev));
+    else SP_CUDA(cudaEventCreateWithFlags(&h->list_ev, cudaEventDisableTiming));
+    int k = 0;
+    for (int t = 0; t < nt; ++t)
+      if (h->h_active[t]) h->h_list[k++] = t;
+    SP_CUDA(cudaMemcpyAsync(h->d_list, h->h_list, sizeof(int) * nact, cudaMemcpyHostToDevice, s));
+    SP_CUDA(cudaEventRecord(h->list_ev, s));
+    list = h->d_list;
+    ngrid = nact;
+  }
   double* scale = (double*)h->d_scratch;
   int* done = (int*)(scale + nt);
   int* cvd = done + nt;
   int* live = cvd + nt;
   TV a;
-  a.u0 = (float*)L0.u; a.b0 = (float*)L0.b; a.r0 = (float*)L0.r; a.corr0 = (float*)L0.corr;
+  a.u0 = (float*)L0.u; a.b0 = const_cast<float*>(bsym); a.r0 = (float*)L0.r;
+  a.corr0 = (float*)L0.corr;
   a.u1 = (float*)L1.u; a.b1 = (float*)L1.b; a.r1 = (float*)L1.r; a.corr1 = (float*)L1.corr;
   a.m0 = L0.mask; a.m1 = L1.mask;
   a.n0 = L0.norms; a.n1 = L1.norms;
   a.scale = scale; a.active = h->d_active; a.done = done; a.conv = cvd; a.live = live;
+  a.list = list;
   a.C = C; a.H0 = L0.H; a.W0 = L0.W; a.H1 = L1.H; a.W1 = L1.W;
   a.bh0 = L0.bh; a.bw0 = L0.bw; a.nby0 = L0.nby; a.nbx0 = L0.nbx;
   a.stride = h->cfg.block - h->cfg.overlap;
@@ -461,7 +496,15 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
   auto k_coarse = sp64 ? k_tv_coarse<64, 64, 32, 32> : k_tv_coarse<0, 0, 0, 0>;
   auto k_up = sp64 ? k_tv_up<64, 64, 32, 32> : k_tv_up<0, 0, 0, 0>;
   auto k_close = sp64 ? k_tv_close<64, 64, 32, 32> : k_tv_close<0, 0, 0, 0>;
-  k_init<<<nt, PT, 0, s>>>(a);
+  if (ngrid == 0) {
+    SP_CUDA(cudaMemcpyAsync(u_out, L0.u, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+    for (int t = 0; t < nt; ++t) {
+      if (iters) iters[t] = 0;
+      if (conv) conv[t] = 0;
+    }
+    return 0;
+  }
+  k_init<<<ngrid, PT, 0, s>>>(a);
   SP_CHECK_LAUNCH();
   int* hl = (int*)h->h_norms;  // pinned staging (>= ntile * C doubles)
   auto oras = [&](Level& L) {
@@ -469,7 +512,7 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
                                     L.nby, L.nbx, L.bh, L.bw, L.H, L.W, C, h->gamma,
                                     (long)L.bh * L.bw, 1.0, (const float*)L.weights,
                                     (float*)L.corr, s, nt, h->d_active, stride, 0, 0,
-                                    L.wdelta, L.offbits);
+                                    L.wdelta, L.offbits, list, ngrid);
   };
   // V-cycles run in batches between reads of the live-block count: a block
   // that stops inside a batch is skipped by every later launch (each kernel
@@ -481,16 +524,16 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
     for (int b = 0; b < batch; ++b) {
       SP_CUDA(cudaMemsetAsync(live, 0, sizeof(int), s));
       SP_TRY(oras(L0));                     // pre-smoothing, level 0
-      k_down<<<nt, PT, 0, s>>>(a);
+      k_down<<<ngrid, PT, 0, s>>>(a);
       SP_CHECK_LAUNCH();
       SP_TRY(oras(L1));                     // coarsest, sweep 1
-      k_coarse<<<nt, PT, 0, s>>>(a);
+      k_coarse<<<ngrid, PT, 0, s>>>(a);
       SP_CHECK_LAUNCH();
       SP_TRY(oras(L1));                     // coarsest, sweep 2
-      k_up<<<nt, PT, 0, s>>>(a);
+      k_up<<<ngrid, PT, 0, s>>>(a);
       SP_CHECK_LAUNCH();
       SP_TRY(oras(L0));                     // post-smoothing, level 0
-      k_close<<<nt, PT, 0, s>>>(a);
+      k_close<<<ngrid, PT, 0, s>>>(a);
       SP_CHECK_LAUNCH();
     }
     SP_CUDA(cudaMemcpyAsync(hl, live, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -21,7 +21,8 @@ inline int nblocks_for(size_t n) {
   return (int)b;
 }
 
-// mode 0: sum x^2; mode 1: sum x*y; mode 2: sum (x - z)^2 with z double
+// mode 0: sum x^2; mode 1: sum x*y; mode 2: sum (x - z)^2 with z double;
+// mode 3: sum (x - y)^2 with y of x's type (both widened exactly to double)
 template <typename T, int MODE>
 __global__ void __launch_bounds__(NT) k_reduce(const T* __restrict__ x,
                                                const T* __restrict__ y,
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(NT) k_reduce(const T* __restrict__ x,
       double a = (double)x[off + i];
       if (MODE == 0) acc += a * a;
       else if (MODE == 1) acc += a * (double)y[off + i];
+      else if (MODE == 3) { double d = a - (double)y[off + i]; acc += d * d; }
       else { double d = a - z[off + i]; acc += d * d; }
     }
     double s = cta_sum<NT>(acc, (c & 1) ? s1 : s0);
@@ -75,6 +77,7 @@ __global__ void __launch_bounds__(NT) k_reduce_seg(const T* __restrict__ x,
     double a = (double)x[off + i];
     if (MODE == 0) acc += a * a;
     else if (MODE == 1) acc += a * (double)y[off + i];
+    else if (MODE == 3) { double d = a - (double)y[off + i]; acc += d * d; }
     else { double d = a - z[off + i]; acc += d * d; }
   }
   double s = cta_sum<NT>(acc, s0);
@@ -101,12 +104,14 @@ int chan_reduce(int mode, const T* x, const T* y, const double* z, size_t n, int
   if (C >= 2 * num_sms() && n <= (size_t)NT * 64) {
     if (mode == 0) k_reduce_seg<T, 0><<<C, NT, 0, s>>>(x, y, z, n, out);
     else if (mode == 1) k_reduce_seg<T, 1><<<C, NT, 0, s>>>(x, y, z, n, out);
+    else if (mode == 3) k_reduce_seg<T, 3><<<C, NT, 0, s>>>(x, y, z, n, out);
     else k_reduce_seg<T, 2><<<C, NT, 0, s>>>(x, y, z, n, out);
     SP_CHECK_LAUNCH();
     return 0;
   }
   if (mode == 0) k_reduce<T, 0><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
   else if (mode == 1) k_reduce<T, 1><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
+  else if (mode == 3) k_reduce<T, 3><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
   else k_reduce<T, 2><<<nb, NT, 0, s>>>(x, y, z, n, C, partial, counter, out);
   SP_CHECK_LAUNCH();
   return 0;

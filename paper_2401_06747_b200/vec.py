@@ -41,6 +41,9 @@ def sq_err(x, z):
 
 def mse_t(a, b) -> float:
     """MSE over all channels in double (grid.py:188-193, tonal.py:86-88)."""
+    if a.dtype == b.dtype and a.dtype in (torch.float32, torch.float64):
+        # both widened exactly in the kernel: no f64 copy of either
+        return float(chan_reduce(3, a, y=b, channels=1).item()) / max(1, a.numel())
     if a.dtype == torch.float64 and b.dtype != torch.float64:
         a, b = b, a
     x = a if a.dtype in (torch.float32, torch.float64) else a.to(torch.float64)

@@ -196,3 +196,31 @@ def test_fused_tile_solver_ras_mse(sp):
     (ma, ia), (mb, ib) = _with_tile_fused(1, run), _with_tile_fused(0, run)
     assert ia == ib
     assert abs(ma - mb) <= 1e-6 * mb
+
+
+@pytest.mark.parametrize("shape", [(3, 256, 320), (1, 300, 200)])
+def test_ras_tile_list_bit_identical(shape):
+    """The fused RAS block solves of a partly active batch (the tail of the
+    local CG) launch over the list of active blocks instead of every block
+    with early exits: the same blocks run the same kernels, so ras_tonal is
+    bit-identical either way (tonal.py:267-294)."""
+    import paper_2401_06747_b200 as sp
+    from paper_2401_06747_b200 import _lib
+    from paper_2401_06747_b200.solver import _POOL
+    lib = _lib.load()
+    c, h, w = shape
+    f = O.synth(h, w, c, 7)
+    mask = (np.random.default_rng(8).random((h, w)) < 0.05).astype(np.uint8)
+    outs = []
+    prev = lib.sp_tile_list(-1)
+    try:
+        for v in (1, 0):
+            lib.sp_tile_list(v)
+            _POOL.clear()
+            st = sp.ras_tonal(sp.Image(f), sp.Mask(mask))
+            outs.append((st.g.data, st.mse, st.iterations))
+    finally:
+        lib.sp_tile_list(prev)
+        _POOL.clear()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
