@@ -475,7 +475,14 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
   int* cvd = done + nt;
   int* live = cvd + nt;
   TV a;
-  a.u0 = (float*)L0.u; a.b0 = const_cast<float*>(bsym); a.r0 = (float*)L0.r;
+  // with every block active the block kernels iterate in the caller's output
+  // directly (each block's u is written by k_tv_init before any read); a
+  // partly active batch keeps the hierarchy's buffer and copies it out whole
+  // (the inactive blocks' stale values, as the unfused path returns them)
+  const bool direct = nact == nt && (u_out + n <= bsym || bsym + n <= u_out);
+  a.u0 = direct ? u_out : (float*)L0.u;
+  a.b0 = const_cast<float*>(bsym);
+  a.r0 = (float*)L0.r;
   a.corr0 = (float*)L0.corr;
   a.u1 = (float*)L1.u; a.b1 = (float*)L1.b; a.r1 = (float*)L1.r; a.corr1 = (float*)L1.corr;
   a.m0 = L0.mask; a.m1 = L1.mask;
@@ -541,7 +548,8 @@ int tile_solve_fused(Hier* h, const float* bsym, float* u_out, double tol, int m
     if (hl[0] == 0) break;
     batch = 1;
   }
-  SP_CUDA(cudaMemcpyAsync(u_out, L0.u, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+  if (!direct)
+    SP_CUDA(cudaMemcpyAsync(u_out, L0.u, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
   SP_CUDA(cudaMemcpyAsync(hl, done, sizeof(int) * 2 * nt, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   long long cyc = 0;
