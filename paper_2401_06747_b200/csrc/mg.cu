@@ -570,27 +570,20 @@ __global__ void __launch_bounds__(NT) k4_rhs(const T* __restrict__ xin,
     }
   }
   if (!NRM) return;
+  // one partial per CTA (grid order); k_sum_parts adds them in index order --
+  // no atomics: with the grid-stride loop every CTA ends at the same time
   __shared__ double s0[NT / 32];
-  __shared__ bool am_last;
-  const unsigned ncta = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
   const double sb = cta_sum<NT>(nacc, s0);
-  const int tid = threadIdx.y * BX + threadIdx.x;
-  if (tid == 0) {
-    partial[cta] = sb;
-    __threadfence();
-    am_last = atomicAdd(counter, 1u) == ncta - 1;
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
+  if (threadIdx.y * BX + threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = sb;
+}
+
+__global__ void __launch_bounds__(1024) k_sum_parts(const double* __restrict__ partial, int n,
+                                                    double* __restrict__ total) {
+  __shared__ double s0[1024 / 32];
   double t = 0.0;
-  for (unsigned i = tid; i < ncta; i += NT) t += ((volatile double*)partial)[i];
-  __syncthreads();
-  t = cta_sum<NT>(t, s0);
-  if (tid == 0) {
-    *nrm = t;
-    *counter = 0u;
-  }
+  for (int i = threadIdx.x; i < n; i += 1024) t += partial[i];
+  t = cta_sum<1024>(t, s0);
+  if (threadIdx.x == 0) *total = t;
 }
 
 template <typename T>
@@ -752,6 +745,8 @@ int masked_sym_rhs(const T* x, const uint8_t* m, T* out, int C, int H, int W, cu
       }
       SP_CUDA(launch_k(k4_rhs<T, 1, true>, g, kBlock, 0, s, x, m, out, enforce_u, C, H, W, 1.0,
                        active, partial, counter, nrm));
+      SP_CHECK_LAUNCH();
+      k_sum_parts<<<1, 1024, 0, s>>>(partial, (int)(g.x * g.y), nrm);
     } else {
       SP_CUDA(launch_k(k4_rhs<T, 1>, g, kBlock, 0, s, x, m, out, enforce_u, C, H, W, 1.0, active,
                        (double*)nullptr, (unsigned*)nullptr, (double*)nullptr));

@@ -132,47 +132,38 @@ __global__ void k_error_map(const T* __restrict__ u, const double* __restrict__ 
   e[i] = acc;
 }
 
-// the same error map plus its total sum_p e_p (the MSE numerator,
-// grid.py:188-193) in the same pass: grid-stride CTAs, double per-thread
-// sums, CTA partials added in index order by the last CTA (deterministic);
-// saves the separate f64 / u re-read of the MSE reduction
+// the same error map plus one partial sum per CTA (the MSE numerator,
+// grid.py:188-193): one pixel per thread like k_error_map, a fixed-order
+// CTA sum; k_sum_partials adds the CTA partials in index order (no atomics:
+// a last-CTA reduction serialised ~1,000 same-address atomics at the end of
+// a grid whose CTAs all finish together)
 template <typename T>
-__global__ void __launch_bounds__(NT) k_error_map_sum(const T* __restrict__ u,
-                                                      const double* __restrict__ f,
-                                                      double* __restrict__ e, int C, size_t n,
-                                                      double* __restrict__ partial,
-                                                      unsigned* __restrict__ counter,
-                                                      double* __restrict__ total) {
-  __shared__ double s0[NT / 32];
-  __shared__ bool am_last;
-  double tacc = 0.0;
-  for (size_t i = (size_t)blockIdx.x * NT + threadIdx.x; i < n; i += (size_t)gridDim.x * NT) {
-    double acc = 0.0;
+__global__ void __launch_bounds__(256) k_error_map_part(const T* __restrict__ u,
+                                                       const double* __restrict__ f,
+                                                       double* __restrict__ e, int C, size_t n,
+                                                       double* __restrict__ partial) {
+  __shared__ double s0[256 / 32];
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  if (i < n) {
     for (int c = 0; c < C; ++c) {
       double d = (double)u[(size_t)c * n + i] - f[(size_t)c * n + i];
       double sq = d * d;
       acc = c == 0 ? sq : acc + sq;
     }
     e[i] = acc;
-    tacc += acc;
   }
-  const double sblk = cta_sum<NT>(tacc, s0);
-  if (threadIdx.x == 0) {
-    partial[blockIdx.x] = sblk;
-    __threadfence();
-    am_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
+  const double sb = cta_sum<256>(acc, s0);
+  if (threadIdx.x == 0) partial[blockIdx.x] = sb;
+}
+
+__global__ void __launch_bounds__(1024) k_sum_partials(const double* __restrict__ partial,
+                                                       int n, double* __restrict__ total) {
+  __shared__ double s0[1024 / 32];
   double t = 0.0;
-  for (unsigned i = threadIdx.x; i < gridDim.x; i += NT) t += ((volatile double*)partial)[i];
-  __syncthreads();
-  t = cta_sum<NT>(t, s0);
-  if (threadIdx.x == 0) {
-    *total = t;
-    *counter = 0u;
-  }
+  for (int i = threadIdx.x; i < n; i += 1024) t += partial[i];
+  t = cta_sum<1024>(t, s0);
+  if (threadIdx.x == 0) *total = t;
 }
 
 template <typename T>
@@ -183,12 +174,12 @@ int error_map(const T* u, const double* f, double* e, int C, size_t n, cudaStrea
     SP_CHECK_LAUNCH();
     return 0;
   }
-  const int nb = nblocks_for(n);
+  const unsigned nb = cdiv(n, 256);
   Scratch scr(s);
   SP_TRY(scr.alloc(sizeof(double) * nb + 64));
-  unsigned* counter = (unsigned*)((double*)scr.p + nb);
-  SP_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
-  k_error_map_sum<T><<<nb, NT, 0, s>>>(u, f, e, C, n, (double*)scr.p, counter, total);
+  k_error_map_part<T><<<nb, 256, 0, s>>>(u, f, e, C, n, (double*)scr.p);
+  SP_CHECK_LAUNCH();
+  k_sum_partials<<<1, 1024, 0, s>>>((const double*)scr.p, (int)nb, total);
   SP_CHECK_LAUNCH();
   return 0;
 }
