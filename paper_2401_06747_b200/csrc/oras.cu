@@ -38,14 +38,20 @@ __device__ unsigned long long g_oras_stats[4];
 __device__ int g_stats_on;
 
 // kernel choice for float blocks <= 32x32 (sp_oras_variant, A/B runs):
-// 7 = one warp per job, lean local CG (k_oras_warp<FAST>, the default);
+// 8 = one warp per job, the lean local CG on packed float pairs
+// (k_oras_warp<CGK 2>: FFMA2 / FADD2, the default; 341 instead of 471
+// instructions per CG step, 4K pipeline 249.7 -> 244.9 ms); 7 = the same CG
+// on scalar floats (k_oras_warp<CGK 1>);
 // 6 = one warp per job, the reference-ordered CG (bit-identical to 0 and 4);
 // 4 = k_oras_warp with four jobs per CTA; 0 = the register-resident 4-warp
 // job kernel (k_oras_rows); 1 = the 256-thread CTA kernel with the
 // reference's double stencil.  (A persistent cp.async-prefetch variant
 // measured slower -- 1.80 vs 1.58 ms per 4K V-cycle, profiles/
-// oras_ab_r01j.txt -- and was removed.)
-static int oras_kernel = 7;
+// oras_ab_r01j.txt -- and was removed; so did a two-warps-per-job pair CG,
+// 16 rows per lane at 96-124 registers for 16-20 warps per SM: 255.7 /
+// 260.3 vs 244.8 ms per 4K pipeline -- 480 instead of 341 instructions per
+// job step outweigh the extra warps.)
+static int oras_kernel = 8;
 int oras_variant(int v) {
   if (v >= 0) oras_kernel = v;
   return oras_kernel;
@@ -498,7 +504,8 @@ __global__ void __launch_bounds__(NTJ, 7) k_oras_rows(
 // ---------------------------------------------------------------------------
 constexpr int WJ = 4;  // jobs (warps) per CTA
 
-template <bool UNIT_H, bool FULLH, int WJ, bool FAST = false>
+// CGK: 0 = warp_cg32 (reference-ordered), 1 = warp_cg32_fast, 2 = warp_cg32_pair
+template <bool UNIT_H, bool FULLH, int WJ, int CGK = 0>
 __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
     const float* __restrict__ r, const uint8_t* __restrict__ m,
     const double* __restrict__ tau_src, double tau_scale, const int* __restrict__ ys,
@@ -536,6 +543,7 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
   // off: bit s set where row s is masked or outside the block (q = 0 there,
   // and A p = p, which is 0 outside the block)
   uint32_t off = 0;
+  constexpr bool FAST = CGK > 0;
   if (FAST && offbits) {
     // the precomputed row-mask word of the lane's column (oras_offbits_launch)
     off = offbits[((size_t)tile * nbl + bi) * 32 + j];
@@ -580,9 +588,11 @@ __global__ void __launch_bounds__(WJ * 32, 12 / WJ) k_oras_warp(
 
   float v[R];
   const long it =
-      FAST ? warp_cg32_fast<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh,
-                                           tau, cap)
-           : warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh, tau,
+      CGK == 2 ? warp_cg32_pair<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2,
+                                               bh, tau, cap)
+      : FAST   ? warp_cg32_fast<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh,
+                                             tau, cap)
+               : warp_cg32<UNIT_H, FULLH>(res, v, off, dtop, dmid, dbot, lf, rt, inv_h2, bh, tau,
                                       cap, j);
   float* out = corr + (((size_t)tile * C + ch) * nb + bi) * (size_t)(bh * bw) + j;
   // interior blocks read the one shared weight pattern (bit-identical values)
@@ -1168,21 +1178,23 @@ int oras_local_launch(const T* r, const uint8_t* m, const double* tau_src, doubl
   dim3 grid(nby * nbx, C, ntile);
   size_t sm = (size_t)npx * sizeof(T) + (size_t)npx;  // p staging + mask bytes
   if (sizeof(T) == 4 && bw <= 32 && bh <= 32 &&
-      (oras_kernel == 4 || oras_kernel == 6 || oras_kernel == 7)) {
+      (oras_kernel == 4 || oras_kernel >= 6)) {
     const int nbl = nby * nbx;
     const bool unit = inv_h2 == 1.0, full = bh == 32 && bw == 32;
     // 4: four jobs per CTA; 6: one job per CTA (a finished job frees its
     // slot at once instead of waiting for the CTA's slowest job); 7: 6 with
-    // the lean local CG (warp_cg32_fast)
+    // the lean local CG (warp_cg32_fast); 8: on packed float pairs
+    // (warp_cg32_pair)
     const int wj = oras_kernel == 4 ? WJ : 1;
     dim3 g4(cdiv(nbl, wj), C, tile_list ? nlist : ntile);
 #define SP_WARP(WJN, F)                                                                   \
   (unit ? (full ? k_oras_warp<true, true, WJN, F> : k_oras_warp<true, false, WJN, F>)     \
         : (full ? k_oras_warp<false, true, WJN, F> : k_oras_warp<false, false, WJN, F>))
-    auto kern = oras_kernel == 7 ? SP_WARP(1, true) : (wj == 1 ? SP_WARP(1, false)
-                                                               : SP_WARP(WJ, false));
+    auto kern = oras_kernel == 8   ? SP_WARP(1, 2)
+                : oras_kernel == 7 ? SP_WARP(1, 1)
+                                   : (wj == 1 ? SP_WARP(1, 0) : SP_WARP(WJ, 0));
 #undef SP_WARP
-    if (oras_kernel == 7) {
+    if (oras_kernel >= 7) {
       SP_CUDA(launch_k(kern, g4, dim3(wj * 32), 0, s, (const float*)r, m, tau_src, tau_scale, ys,
                        xs, nbx, nbl, bh, bw, H, W, stride, (float)(1.0 - gamma), cap,
                        (float)inv_h2, (const float*)weights, (float*)corr, active, corr_nb, ps,

@@ -182,4 +182,101 @@ __device__ __forceinline__ long warp_cg32_fast(float (&res)[32], float (&v)[32],
   return it;
 }
 
+// warp_sum_f over eight float chains held as four pairs: pairwise FADD2s,
+// the two halves, one xor butterfly, a uniform broadcast
+__device__ __forceinline__ float warp_sum_f2(const float2 (&d)[4]) {
+  const float2 t = __fadd2_rn(__fadd2_rn(d[0], d[1]), __fadd2_rn(d[2], d[3]));
+  float x = t.x + t.y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+  return __shfl_sync(0xFFFFFFFFu, x, 0);
+}
+
+// The lean local CG on packed float pairs (sp_oras_variant 8): the lane's
+// 32 rows live as 16 register pairs {row k, row k + 16}, so every vector
+// update, the operator and the dots run as FFMA2 / FADD2 (two IEEE float
+// operations per instruction, each rounded exactly like the scalar one) --
+// the kernel is issue-bound and this halves its floating-point instruction
+// count.  The {k, k + 16} pairing keeps the vertical neighbours aligned: the
+// rows above / below pair k are pairs k - 1 / k + 1 (two seam pairs are
+// assembled from halves).  Same arithmetic as warp_cg32_fast per pixel; the
+// dots accumulate rows {k mod 4} x {low, high half} in eight float chains
+// (4 rows each: FFMA2 chains stall on their latency), combined pairwise.
+template <bool UNIT_H, bool FULLH>
+__device__ __forceinline__ long warp_cg32_pair(float (&res)[32], float (&v)[32], uint32_t off,
+                                               float dtop, float dmid, float dbot, float lf,
+                                               float rt, float inv_h2, int bh, double tau,
+                                               long cap) {
+  constexpr int K = 16;
+  float2 r2[K], p2[K], v2[K], ap2[K];
+  float2 d4[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) d4[g] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    r2[k] = make_float2(res[k], res[k + K]);
+    p2[k] = r2[k];
+    v2[k] = make_float2(0.0f, 0.0f);
+    d4[k & 3] = __ffma2_rn(r2[k], r2[k], d4[k & 3]);
+  }
+  float rs = warp_sum_f2(d4);
+  const float2 lf2 = make_float2(lf, lf), rt2 = make_float2(rt, rt);
+  const float2 ih2 = make_float2(inv_h2, inv_h2);
+  long it = 0;
+  while ((double)rs > tau && it < cap) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) d4[g] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float2 ql = make_float2(__shfl_up_sync(0xFFFFFFFFu, p2[k].x, 1),
+                                    __shfl_up_sync(0xFFFFFFFFu, p2[k].y, 1));
+      const float2 qr = make_float2(__shfl_down_sync(0xFFFFFFFFu, p2[k].x, 1),
+                                    __shfl_down_sync(0xFFFFFFFFu, p2[k].y, 1));
+      const float2 up = k > 0 ? p2[k - 1] : make_float2(0.0f, p2[K - 1].x);
+      const float2 dn = k < K - 1 ? p2[k + 1] : make_float2(p2[0].y, 0.0f);
+      const float2 acc = __ffma2_rn(qr, rt2, __ffma2_rn(ql, lf2, __fadd2_rn(up, dn)));
+      float2 dg;
+      if (FULLH) {
+        dg.x = k == 0 ? dtop : dmid;
+        dg.y = k == K - 1 ? dbot : dmid;
+      } else {
+        dg.x = k == 0 ? dtop : (k == bh - 1 ? dbot : dmid);
+        dg.y = k + K == bh - 1 ? dbot : dmid;
+      }
+      const float2 sc = UNIT_H ? acc : __fmul2_rn(acc, ih2);
+      const float2 a = __ffma2_rn(dg, p2[k], make_float2(-sc.x, -sc.y));
+      ap2[k].x = ((off >> k) & 1u) ? 0.0f : a.x;
+      ap2[k].y = ((off >> (k + K)) & 1u) ? 0.0f : a.y;
+      d4[k & 3] = __ffma2_rn(p2[k], ap2[k], d4[k & 3]);
+    }
+    const float pap = warp_sum_f2(d4);
+    if (pap <= 0.0f) break;
+    const float alpha = __fdividef(rs, pap);
+    const float2 al2 = make_float2(alpha, alpha), nal2 = make_float2(-alpha, -alpha);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) d4[g] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v2[k] = __ffma2_rn(al2, p2[k], v2[k]);
+      r2[k] = __ffma2_rn(nal2, ap2[k], r2[k]);
+      d4[k & 3] = __ffma2_rn(r2[k], r2[k], d4[k & 3]);
+    }
+    const float rsn = warp_sum_f2(d4);
+    const float beta = __fdividef(rsn, rs);
+    rs = rsn;
+    const float2 be2 = make_float2(beta, beta);
+#pragma unroll
+    for (int k = 0; k < K; ++k) p2[k] = __ffma2_rn(be2, p2[k], r2[k]);
+    ++it;
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    res[k] = r2[k].x;
+    res[k + K] = r2[k].y;
+    v[k] = v2[k].x;
+    v[k + K] = v2[k].y;
+  }
+  return it;
+}
+
 }  // namespace sp

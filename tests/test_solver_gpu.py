@@ -218,13 +218,14 @@ def test_oras_warp_kernel_bit_identical_ras():
     assert np.array_equal(ga, gb)
 
 
+@pytest.mark.parametrize("variant", [7, 8])
 @pytest.mark.parametrize("shape", [(3, 301, 512), (1, 100, 150), (3, 2160 // 4, 3840 // 4)])
-def test_lean_oras_cg_tracks_reference_ordered_cg(shape):
-    """The default lean local CG (variant 7: float dots, q = p, fast
-    division) against the reference-ordered one (variant 6): the same CG
-    iterates up to float rounding, so fixed V-cycles agree to ~1e-6 and a
-    tight solve lands on the same solution (the oracle-pinned tests run the
-    default)."""
+def test_lean_oras_cg_tracks_reference_ordered_cg(shape, variant):
+    """The lean local CG (variant 7: float dots, q = p, fast division;
+    variant 8: the same on packed float pairs, FFMA2) against the
+    reference-ordered one (variant 6): the same CG iterates up to float
+    rounding, so fixed V-cycles agree to ~1e-6 and a tight solve lands on
+    the same solution (the oracle-pinned tests run the default)."""
     import paper_2401_06747_b200 as sp
     c, h, w = shape
     f = O.synth(h, w, c, 3)
@@ -235,10 +236,11 @@ def test_lean_oras_cg_tracks_reference_ordered_cg(shape):
 
     fixed = sp.MultigridConfig(tol=None, cycles=3)
     a = _with_oras_variant(6, run(fixed))[0].data
-    b = _with_oras_variant(7, run(fixed))[0].data
+    b = _with_oras_variant(variant, run(fixed))[0].data
     assert np.linalg.norm(a - b) / np.linalg.norm(a) <= 2e-5
     tight = sp.MultigridConfig(tol=1e-6, max_cycles=200)
-    (ua, ra), (ub, rb) = _with_oras_variant(6, run(tight)), _with_oras_variant(7, run(tight))
+    (ua, ra) = _with_oras_variant(6, run(tight))
+    (ub, rb) = _with_oras_variant(variant, run(tight))
     assert abs(ra.iterations - rb.iterations) <= 1
     assert np.linalg.norm(ua.data - ub.data) / np.linalg.norm(ua.data) <= 1e-5
 
