@@ -119,7 +119,15 @@ __global__ void k_seed_init(const int* __restrict__ idx, long m, int W, int* __r
 // becomes "lower key wins".  A pass then needs no seed-table gathers (the
 // index form reads sy/sx of all nine candidates, 18 scattered L2 reads per
 // pixel); the keys are mapped back to indices once at the end.
-constexpr unsigned KNONE = 0xFFFFFFFFu;
+//
+// "No seed yet" is the key of a phantom seed at (32767, 32767): for images
+// of at most kKeyMax rows and columns its squared distance (>= 2 * 16767^2)
+// exceeds every real one (<= 2 * 16000^2) and its key every real key, so
+// the pass rule "nearer wins, lower key wins a tie, unlabelled candidates
+// are skipped, an unlabelled pixel takes any labelled candidate" is exactly
+// the minimum of the 64-bit word (d2 << 32 | key) -- no special cases.
+constexpr unsigned KNONE = 0x7FFF7FFFu;
+constexpr int kKeyMax = 16000;
 
 __global__ void k_jfa_key_init(const uint8_t* __restrict__ m, unsigned* __restrict__ lab, int H,
                                int W) {
@@ -129,17 +137,18 @@ __global__ void k_jfa_key_init(const uint8_t* __restrict__ m, unsigned* __restri
   lab[k] = m[k] ? (((unsigned)y << 16) | (unsigned)x) : KNONE;
 }
 
-__device__ __forceinline__ int key_d2(unsigned key, int y, int x) {
+// (squared distance of the key's seed to (y, x)) << 32 | key
+__device__ __forceinline__ unsigned long long key_dk(unsigned key, int y, int x) {
   const int dy = y - (int)(key >> 16), dx = x - (int)(key & 0xFFFFu);
-  return dy * dy + dx * dx;
+  const unsigned d = (unsigned)(dy * dy) + (unsigned)(dx * dx);
+  return ((unsigned long long)d << 32) | key;
 }
 
 __global__ void k_jfa_pass_key(const unsigned* __restrict__ cur, unsigned* __restrict__ nxt,
                                int step, int H, int W) {
   int x = blockIdx.x * BX + threadIdx.x, y = blockIdx.y * BY + threadIdx.y;
   if (x >= W || y >= H) return;
-  unsigned best = cur[(size_t)y * W + x];
-  int bd = best != KNONE ? key_d2(best, y, x) : 4 * (H * H + W * W);
+  unsigned long long best = key_dk(cur[(size_t)y * W + x], y, x);
 #pragma unroll
   for (int oy = -1; oy <= 1; ++oy) {
     int ny = y + oy * step;
@@ -149,16 +158,11 @@ __global__ void k_jfa_pass_key(const unsigned* __restrict__ cur, unsigned* __res
       if (oy == 0 && ox == 0) continue;
       int nx = x + ox * step;
       if (nx < 0 || nx >= W) continue;
-      unsigned cand = cur[(size_t)ny * W + nx];
-      if (cand == KNONE) continue;
-      int cd = key_d2(cand, y, x);
-      if (cd < bd || (cd == bd && best != KNONE && cand < best)) {
-        bd = cd;
-        best = cand;
-      }
+      const unsigned long long c = key_dk(cur[(size_t)ny * W + nx], y, x);
+      best = c < best ? c : best;
     }
   }
-  nxt[(size_t)y * W + x] = best;
+  nxt[(size_t)y * W + x] = (unsigned)best;
 }
 
 // four pixels per thread for steps that are multiples of 4 (W % 4 == 0): the
@@ -171,11 +175,8 @@ __global__ void k_jfa_pass_key4(const unsigned* __restrict__ cur, unsigned* __re
   const int x0 = (blockIdx.x * BX + threadIdx.x) * 4, y = blockIdx.y * BY + threadIdx.y;
   if (x0 >= W || y >= H) return;
   const uint4 self = *reinterpret_cast<const uint4*>(cur + (size_t)y * W + x0);
-  unsigned best[4] = {self.x, self.y, self.z, self.w};
-  int bd[4];
-  const int big = 4 * (H * H + W * W);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) bd[i] = best[i] != KNONE ? key_d2(best[i], y, x0 + i) : big;
+  unsigned long long best[4] = {key_dk(self.x, y, x0), key_dk(self.y, y, x0 + 1),
+                                key_dk(self.z, y, x0 + 2), key_dk(self.w, y, x0 + 3)};
 #pragma unroll
   for (int oy = -1; oy <= 1; ++oy) {
     const int ny = y + oy * step;
@@ -189,16 +190,13 @@ __global__ void k_jfa_pass_key4(const unsigned* __restrict__ cur, unsigned* __re
       const unsigned cand[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        if (cand[i] == KNONE) continue;
-        const int cd = key_d2(cand[i], y, x0 + i);
-        if (cd < bd[i] || (cd == bd[i] && best[i] != KNONE && cand[i] < best[i])) {
-          bd[i] = cd;
-          best[i] = cand[i];
-        }
+        const unsigned long long c = key_dk(cand[i], y, x0 + i);
+        best[i] = c < best[i] ? c : best[i];
       }
     }
   }
-  *reinterpret_cast<uint4*>(nxt + (size_t)y * W + x0) = make_uint4(best[0], best[1], best[2], best[3]);
+  *reinterpret_cast<uint4*>(nxt + (size_t)y * W + x0) =
+      make_uint4((unsigned)best[0], (unsigned)best[1], (unsigned)best[2], (unsigned)best[3]);
 }
 
 // keys -> seed indices (rank of the seed pixel), in place; fused with the
@@ -1175,7 +1173,7 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
   }
   g->m = m;
   std::vector<long long> steps = steps_for(std::max(H, W), hint);
-  const bool keyed = H < 65536 && W < 65536 && 4.0 * ((double)H * H + (double)W * W) < 2.0e9;
+  const bool keyed = H <= kKeyMax && W <= kKeyMax;
   if (keyed) {
     // packed-coordinate labels (k_jfa_pass_key); rank[] maps keys back
     k_seed_init<<<cdiv(m, 256), 256, 0, s>>>(g->idx, m, W, g->sy, g->sx, g->rank);
