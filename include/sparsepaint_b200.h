@@ -389,9 +389,11 @@ int sp_tile_list(int v);
  * separate reduction (0); the sums group differently (rounding only).
  * v < 0 queries. */
 int sp_fused_bnorm(int v);
-/* C = 3 float blend: 1 = packed per-row / per-column cover words (one table
- * load each, default), 0 = the cover-table chains; bit-identical.  v < 0
- * queries.  A/B aid, no reference counterpart. */
+/* C = 3 float blend: 2 = packed cover words on column pairs (two pixels per
+ * 8-byte access where W and every block start are even, else 1; default),
+ * 3 = the same with two rows per thread, 1 = packed per-row / per-column
+ * cover words (one table load each), 0 = the cover-table chains; all
+ * bit-identical.  v < 0 queries.  A/B aid, no reference counterpart. */
 int sp_blend_packed(int v);
 /* residual r = b~ - A~ u and per-plane sum r^2 of level lv's current iterate
  * (after a solve), computed by the hierarchy's sweep kernel, into device

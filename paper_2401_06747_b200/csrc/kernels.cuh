@@ -51,7 +51,8 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile = 1,
                       const int* active = nullptr, int corr_nb = 0, size_t ps = 0,
-                      const int* rowinfo = nullptr, const int* colinfo = nullptr);
+                      const int* rowinfo = nullptr, const int* colinfo = nullptr,
+                      bool pair_cols = false);
 // packed per-row / per-column cover words for the C = 3 float blend
 // (k_oras_blend3p); sp_blend_packed
 bool blend_pack(const std::vector<int>& starts, int size, int dim, std::vector<int>& info);

@@ -1117,6 +1117,123 @@ __global__ void __launch_bounds__(256) k_oras_blend3p(
   }
 }
 
+// k_oras_blend3p on column PAIRS (x, x + 1), x even: with every block
+// start even and W even (stride 26 at every level of the default
+// decomposition) a pair never straddles a block edge, so both pixels have
+// the same covering blocks and their offsets in them differ by one -- every
+// u and correction access is one 8-byte load or store for two pixels, half
+// the address arithmetic of the per-pixel kernel (which is ALU-bound: ncu
+// 66 % ALU pipe).  Same gather, same block order, same float adds:
+// bit-identical.  Tiles of 64 x 16 pixels.
+template <int R>
+__global__ void __launch_bounds__(256, R == 1 ? 4 : 2) k_oras_blend3q(
+    float* __restrict__ u, const float* __restrict__ corr, const int* __restrict__ ys,
+    const int* __restrict__ xs, const int* __restrict__ row_k0, const int* __restrict__ row_n,
+    const int* __restrict__ col_k0, const int* __restrict__ col_n,
+    const int* __restrict__ rowinfo, const int* __restrict__ colinfo, int nbx, int H, int W,
+    const int* __restrict__ active, int nb, size_t ps) {
+  pdl_enter();
+  const int tile = blockIdx.y;
+  if (active && !active[tile]) return;
+  const int plane = (int)ps, cplane = nb * 1024;
+  float* ut = u + (size_t)tile * 3 * ps;
+  const float* ct = corr + (size_t)tile * 3 * (size_t)cplane;
+  const int ntx = (W + 63) >> 6, nty = (H + 8 * R - 1) / (8 * R), per = ntx * nty;
+  for (int t = blockIdx.x; t < per; t += gridDim.x) {
+    const int ty = t / ntx;
+    const int x = (t - ty * ntx) * 64 + 2 * threadIdx.x;
+    if (x >= W) continue;
+    const int ci = colinfo[x];
+    int yv[R], ri[R];
+    bool ok[R];
+#pragma unroll
+    for (int h2 = 0; h2 < R; ++h2) {
+      yv[h2] = ty * 8 * R + threadIdx.y + 8 * h2;
+      ok[h2] = yv[h2] < H;
+      ri[h2] = ok[h2] ? rowinfo[yv[h2]] : 0;
+    }
+    int rall = 0;
+#pragma unroll
+    for (int h2 = 0; h2 < R; ++h2) rall |= ri[h2];
+    if (((ci | rall) >> 17) & 1) {
+      // a row or column with three covering blocks (a pulled-in last block)
+#pragma unroll
+      for (int h2 = 0; h2 < R; ++h2) {
+        if (!ok[h2]) continue;
+        const int y = yv[h2];
+        for (int e = 0; e < 2; ++e) {
+          const int xe = x + e, k = y * W + xe;
+          float acc[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[c] = ut[c * plane + k];
+          for (int a = 0; a < row_n[y]; ++a) {
+            const int ky = row_k0[y] + a;
+            const int rowoff = ky * nbx * 1024 + (y - ys[ky]) * 32;
+            for (int b2 = 0; b2 < col_n[xe]; ++b2) {
+              const int kx = col_k0[xe] + b2;
+              const int o = rowoff + kx * 1024 + (xe - xs[kx]);
+#pragma unroll
+              for (int c = 0; c < 3; ++c) acc[c] = acc[c] + ct[c * cplane + o];
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ut[c * plane + k] = acc[c];
+        }
+      }
+      continue;
+    }
+    const int kx0 = ci & 0xFFFF, xo0 = (ci >> 18) & 63, dxo = ((ci >> 24) & 63) - xo0;
+    const bool twox = (ci >> 16) & 1;
+    int off[R][4];
+    bool on[R][4];
+#pragma unroll
+    for (int h2 = 0; h2 < R; ++h2) {
+      const int r = ri[h2];
+      const int ky0 = r & 0xFFFF, yo0 = (r >> 18) & 63, dyo = ((r >> 24) & 63) - yo0;
+      const bool twoy = (r >> 16) & 1;
+      const int b00 = (ky0 * nbx + kx0) * 1024 + yo0 * 32 + xo0;
+      off[h2][0] = b00;
+      off[h2][1] = b00 + 1024 + dxo;
+      off[h2][2] = b00 + nbx * 1024 + dyo * 32;
+      off[h2][3] = off[h2][2] + 1024 + dxo;
+      on[h2][0] = ok[h2];
+      on[h2][1] = ok[h2] && twox;
+      on[h2][2] = ok[h2] && twoy;
+      on[h2][3] = ok[h2] && twox && twoy;
+    }
+    float2 uu[R][3], v[R][4][3];
+#pragma unroll
+    for (int h2 = 0; h2 < R; ++h2)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        uu[h2][c] = ok[h2] ? *reinterpret_cast<const float2*>(ut + c * plane + yv[h2] * W + x)
+                           : make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int h2 = 0; h2 < R; ++h2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          v[h2][q][c] = on[h2][q] ? *reinterpret_cast<const float2*>(ct + c * cplane + off[h2][q])
+                                  : make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int h2 = 0; h2 < R; ++h2) {
+      if (!ok[h2]) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float2 acc = uu[h2][c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (on[h2][q]) {
+            acc.x = acc.x + v[h2][q][c].x;
+            acc.y = acc.y + v[h2][q][c].y;
+          }
+        *reinterpret_cast<float2*>(ut + c * plane + yv[h2] * W + x) = acc;
+      }
+    }
+  }
+}
+
 // generic channel count (C > 4): one channel plane per grid row
 template <typename T>
 __global__ void __launch_bounds__(256) k_oras_blend_plane(
@@ -1253,7 +1370,11 @@ bool blend_pack(const std::vector<int>& starts, int size, int dim, std::vector<i
   return true;
 }
 
-static int blend_packed_on = 1;
+// 2 (default): column pairs (k_oras_blend3q, one row per thread, 63
+// registers) where they fit, else 1; 3: pairs with two rows per thread (107
+// registers, 2 CTAs per SM).  4K finest blend: 1 = 73.6 us (0.73 of HBM),
+// 3 = 67.5 us, 2 = 61.7 us (0.87); pipeline -5 ms.
+static int blend_packed_on = 2;
 int blend_packed(int v) {
   if (v >= 0) blend_packed_on = v;
   return blend_packed_on;
@@ -1264,7 +1385,7 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
                       const int* row_n, const int* col_k0, const int* col_n, int nby, int nbx,
                       int bh, int bw, int H, int W, int C, cudaStream_t s, int ntile,
                       const int* active, int corr_nb, size_t ps, const int* rowinfo,
-                      const int* colinfo) {
+                      const int* colinfo, bool pair_cols) {
   if (!ps) ps = (size_t)H * W;
   long per = (long)cdiv(W, 32) * cdiv(H, C <= 4 ? 16 : 8);
   long nz = C <= 4 ? (long)ntile : (long)ntile * C;
@@ -1279,7 +1400,14 @@ int oras_blend_launch(T* u, const T* corr, const int* ys, const int* xs, const i
   const bool b3 = C == 3 && sizeof(T) == 4 && bh == 32 && bw == 32 && 3 * ps < (1UL << 31) &&
                   3 * nbt * 1024 < (1L << 31);
   if (C == 1) SP_BLEND(1);
-  else if (b3 && rowinfo && colinfo && blend_packed_on)
+  else if (b3 && rowinfo && colinfo && blend_packed_on >= 2 && pair_cols) {
+    const int blend_rows = blend_packed_on == 3 ? 2 : 1;
+    const long perq = (long)cdiv(W, 64) * cdiv(H, 8 * blend_rows);
+    dim3 gq((unsigned)std::min<long>(grid.x, perq), grid.y);
+    SP_CUDA(launch_k(blend_rows == 1 ? k_oras_blend3q<1> : k_oras_blend3q<2>, gq, blk, 0, s, (float*)u, (const float*)corr, ys, xs,
+                     row_k0, row_n, col_k0, col_n, rowinfo, colinfo, nbx, H, W, active,
+                     (int)nbt, ps));
+  } else if (b3 && rowinfo && colinfo && blend_packed_on)
     SP_CUDA(launch_k(k_oras_blend3p, grid, blk, 0, s, (float*)u, (const float*)corr, ys, xs,
                      row_k0, row_n, col_k0, col_n, rowinfo, colinfo, nbx, H, W, active,
                      (int)nbt, ps));
@@ -1375,7 +1503,7 @@ int block_weights_launch(T* weights, const int* ys, const int* xs, const int* ro
   template int oras_blend_launch<T>(T*, const T*, const int*, const int*, const int*,       \
                                     const int*, const int*, const int*, int, int, int, int, \
                                     int, int, int, cudaStream_t, int, const int*, int,      \
-                                    size_t, const int*, const int*);                        \
+                                    size_t, const int*, const int*, bool);                  \
   template int block_weights_launch<T>(T*, const int*, const int*, const int*, const int*,  \
                                        const int*, const int*, int, int, int, int, int,     \
                                        int, int, cudaStream_t);

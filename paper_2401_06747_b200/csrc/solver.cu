@@ -163,6 +163,8 @@ int hier_create(Hier** out, int dtype, int C, int H, int W, const HierCfg& cfg,
       rc |= dalloc((void**)&L.offbits, sizeof(uint32_t) * 32 * nb * ntile);
     std::vector<int> rinfo, cinfo;
     L.rowinfo = L.colinfo = nullptr;
+    L.pair_cols = ww % 2 == 0;
+    for (int x0 : xs) L.pair_cols = L.pair_cols && x0 % 2 == 0;
     if (dtype != SP_F64 && L.bh == 32 && L.bw == 32 && blend_pack(ys, 32, hh, rinfo) &&
         blend_pack(xs, 32, ww, cinfo)) {
       rc |= dalloc((void**)&L.rowinfo, sizeof(int) * hh);
@@ -333,7 +335,7 @@ template <typename T>
 static int blend_lv(Hier* h, Level& L, T* u, cudaStream_t s) {
   return oras_blend_launch<T>(u, (const T*)L.corr, L.ys, L.xs, L.row_k0, L.row_n, L.col_k0,
                               L.col_n, L.nby, L.nbx, L.bh, L.bw, L.H, L.W, h->C, s, h->ntile,
-                              h->d_active, 0, 0, L.rowinfo, L.colinfo);
+                              h->d_active, 0, 0, L.rowinfo, L.colinfo, L.pair_cols);
 }
 
 template <typename T>

@@ -40,6 +40,7 @@ struct Level {
   // rebuilt with the mask pyramid (set_mask_t), or null
   uint32_t* offbits;
   int *rowinfo, *colinfo;  // packed cover words (oras.cu blend_pack), or null
+  bool pair_cols;  // W even and every block column start even (k_oras_blend3q)
 };
 
 struct Hier {

@@ -1,7 +1,7 @@
 """Quick perf probe: finest-level kernel timings (sp_hier_bench), warm 4K RGB
 V-cycle time, and the pipeline step time (device events).
 
-    python scripts/probe_perf.py [--no-pipeline] [--reps N]
+    python scripts/probe_perf.py [--no-pipeline] [sp_switch=value ...]
 """
 import ctypes
 import os
@@ -36,6 +36,10 @@ def _sample():
         time.sleep(0.5)
 
 
+for a in sys.argv[1:]:
+    if "=" in a:
+        k, v = a.split("=")
+        getattr(_lib.load(), k)(int(v))
 _done = False
 threading.Thread(target=_sample, daemon=True).start()
 PEAK = 6544.0

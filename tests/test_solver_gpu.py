@@ -306,14 +306,17 @@ def test_device_driven_solve_loop_identical(shape, tol):
 
 
 
-@pytest.mark.parametrize("shape", [(3, 301, 512), (3, 60, 516), (3, 540, 960), (3, 67, 1300)])
+@pytest.mark.parametrize("shape", [(3, 301, 512), (3, 60, 516), (3, 540, 960), (3, 67, 1300),
+                                   (3, 61, 515), (3, 64, 64)])
 def test_blend_packed_cover_words_bit_identical(shape):
     """The C = 3 blend with packed per-row / per-column cover words
     (k_oras_blend3p) vs the cover-table chains (k_oras_blend3): the same
     corrections added in the same block order (numba_impl.py:255-263), so
     V-cycles from the same start are bit-identical -- incl. the rows of a
     pulled-in last block with three covers, (3, 60, 516), on the generic
-    path."""
+    path; and the column-pair kernel (k_oras_blend3q, mode 2: two pixels per
+    8-byte access where W and every block start are even; odd widths keep
+    the per-pixel kernel)."""
     import paper_2401_06747_b200 as sp
     from paper_2401_06747_b200 import _lib
     from paper_2401_06747_b200.solver import _POOL
@@ -324,7 +327,7 @@ def test_blend_packed_cover_words_bit_identical(shape):
     outs = []
     prev = lib.sp_blend_packed(-1)
     try:
-        for v in (1, 0):
+        for v in (1, 0, 2, 3):
             lib.sp_blend_packed(v)
             _POOL.clear()
             u, rep = sp.inpaint(sp.Image(f), sp.Mask(mask), sp.MultigridConfig(tol=None, cycles=3))
@@ -333,3 +336,5 @@ def test_blend_packed_cover_words_bit_identical(shape):
         lib.sp_blend_packed(prev)
         _POOL.clear()
     assert np.array_equal(outs[0], outs[1])
+    for o in outs[2:]:
+        assert np.array_equal(outs[0], o)
