@@ -1117,6 +1117,57 @@ __global__ void __launch_bounds__(256) k_oras_blend3p(
   }
 }
 
+// k_oras_blend3q's path for a pixel pair on a row or column with three
+// covering blocks (a pulled-in last block), out of line so the common path
+// keeps its compact code: the cover tables, then the block starts, then each
+// block row's corrections load as independent batches (a loop of chained
+// table -> start -> correction loads costs several us per launch on the
+// small levels)
+__device__ __noinline__ void blend3q_generic(float* __restrict__ ut, const float* __restrict__ ct,
+                                             const int* __restrict__ ys,
+                                             const int* __restrict__ xs,
+                                             const int* __restrict__ row_k0,
+                                             const int* __restrict__ row_n,
+                                             const int* __restrict__ col_k0,
+                                             const int* __restrict__ col_n, int nbx, int W,
+                                             int plane, int cplane, int x, int y) {
+  const int nc = col_n[x], c0 = col_k0[x];
+  const int nr = row_n[y], r0 = row_k0[y];
+  int xsb[3], ysb[3];
+#pragma unroll
+  for (int b2 = 0; b2 < 3; ++b2) xsb[b2] = b2 < nc ? xs[c0 + b2] : 0;
+#pragma unroll
+  for (int a2 = 0; a2 < 3; ++a2) ysb[a2] = a2 < nr ? ys[r0 + a2] : 0;
+  const int k = y * W + x;
+  float2 acc[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) acc[c] = *reinterpret_cast<const float2*>(ut + c * plane + k);
+#pragma unroll
+  for (int a2 = 0; a2 < 3; ++a2) {
+    if (a2 >= nr) break;
+    const int rowoff = (r0 + a2) * nbx * 1024 + (y - ysb[a2]) * 32;
+    float2 v[3][3];
+#pragma unroll
+    for (int b2 = 0; b2 < 3; ++b2)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        v[b2][c] = b2 < nc ? *reinterpret_cast<const float2*>(ct + c * cplane + rowoff +
+                                                              (c0 + b2) * 1024 + (x - xsb[b2]))
+                           : make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int b2 = 0; b2 < 3; ++b2) {
+      if (b2 >= nc) break;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        acc[c].x = acc[c].x + v[b2][c].x;
+        acc[c].y = acc[c].y + v[b2][c].y;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) *reinterpret_cast<float2*>(ut + c * plane + k) = acc[c];
+}
+
 // k_oras_blend3p on column PAIRS (x, x + 1), x even: with every block
 // start even and W even (stride 26 at every level of the default
 // decomposition) a pair never straddles a block edge, so both pixels have
@@ -1158,28 +1209,10 @@ __global__ void __launch_bounds__(256, R == 1 ? 4 : 2) k_oras_blend3q(
     if (((ci | rall) >> 17) & 1) {
       // a row or column with three covering blocks (a pulled-in last block)
 #pragma unroll
-      for (int h2 = 0; h2 < R; ++h2) {
-        if (!ok[h2]) continue;
-        const int y = yv[h2];
-        for (int e = 0; e < 2; ++e) {
-          const int xe = x + e, k = y * W + xe;
-          float acc[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) acc[c] = ut[c * plane + k];
-          for (int a = 0; a < row_n[y]; ++a) {
-            const int ky = row_k0[y] + a;
-            const int rowoff = ky * nbx * 1024 + (y - ys[ky]) * 32;
-            for (int b2 = 0; b2 < col_n[xe]; ++b2) {
-              const int kx = col_k0[xe] + b2;
-              const int o = rowoff + kx * 1024 + (xe - xs[kx]);
-#pragma unroll
-              for (int c = 0; c < 3; ++c) acc[c] = acc[c] + ct[c * cplane + o];
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < 3; ++c) ut[c * plane + k] = acc[c];
-        }
-      }
+      for (int h2 = 0; h2 < R; ++h2)
+        if (ok[h2])
+          blend3q_generic(ut, ct, ys, xs, row_k0, row_n, col_k0, col_n, nbx, W, plane, cplane,
+                          x, yv[h2]);
       continue;
     }
     const int kx0 = ci & 0xFFFF, xo0 = (ci >> 18) & 63, dxo = ((ci >> 24) & 63) - xo0;
