@@ -389,6 +389,10 @@ int sp_tile_list(int v);
  * separate reduction (0); the sums group differently (rounding only).
  * v < 0 queries. */
 int sp_fused_bnorm(int v);
+/* Multigrid levels with fewer than v pixels per plane run the per-pixel
+ * sweep kernels instead of the TMA / warp-streamed ones (identical
+ * results); v < 0 queries. */
+long sp_tma_min_pixels(long v);
 /* C = 3 float blend: 2 = packed cover words on column pairs (two pixels per
  * 8-byte access where W and every block start are even, else 1; default),
  * 3 = the same with two rows per thread, 1 = packed per-row / per-column

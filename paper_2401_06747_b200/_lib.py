@@ -114,6 +114,7 @@ _SIGS = {
     "sp_oras_offbits": [c_int],
     "sp_tile_list": [c_int],
     "sp_fused_bnorm": [c_int],
+    "sp_tma_min_pixels": [c_long],
     "sp_blend_packed": [c_int],
     "sp_tile_fused": [c_int],
     "sp_channel_parallel": [c_int],
@@ -148,6 +149,7 @@ def load(require_cuda: bool = True):
         lib.sp_work_count.restype = ctypes.c_longlong
         lib.sp_work_count.argtypes = [c_int, c_int]
         lib.sp_geo_wide_threshold.restype = c_long
+        lib.sp_tma_min_pixels.restype = c_long
         lib.sp_last_error.restype = ctypes.c_char_p
         lib.sp_last_error.argtypes = []
         _lib = lib

@@ -269,9 +269,22 @@ template <typename T>
 static bool aligned_level(const Level& L) {
   return (((uintptr_t)L.u | (uintptr_t)L.b | (uintptr_t)L.r | (uintptr_t)L.mask) & 15u) == 0;
 }
+// levels below this many pixels per plane take the per-pixel sweep kernels
+// instead of the TMA ones (whose fixed start-up -- descriptor prefetch,
+// barrier init, the one-wave grid's partial sums -- dominates a small
+// plane): sp_tma_min_pixels.  300,000: at 4K the levels from 270 x 480 down
+// (ws residual 6.9-9.5 us vs 4.3 us per-pixel); warm V-cycle 0.971 ->
+// 0.951 ms, pipeline -2 ms (probe_perf.py / probe_switch.py)
+static long tma_min_px = 300000;
+long tma_min_pixels(long v) {
+  if (v >= 0) tma_min_px = v;
+  return tma_min_px;
+}
+
 template <typename T>
 static bool use_tma(const Hier* h, const Level& L) {
-  return sizeof(T) == 4 && h->sweep == 2 && tma_ok(L.H, L.W, L.npart) && aligned_level<T>(L);
+  return sizeof(T) == 4 && h->sweep == 2 && (long)L.H * L.W >= tma_min_px &&
+         tma_ok(L.H, L.W, L.npart) && aligned_level<T>(L);
 }
 template <typename T>
 static bool use_march(const Hier* h, const Level& L) {
@@ -312,7 +325,8 @@ template <typename T>
 int prolong_lv(Hier* h, int lv, int add, cudaStream_t s) {
   Level& F = h->lv[lv];
   Level& G = h->lv[lv + 1];
-  if (sizeof(T) == 4 && h->sweep == 2 && tma_prolong_ok(F.H, F.W) && aligned_level<T>(F))
+  if (sizeof(T) == 4 && h->sweep == 2 && (long)F.H * F.W >= tma_min_px &&
+      tma_prolong_ok(F.H, F.W) && aligned_level<T>(F))
     return prolong_tma((const float*)G.u, (float*)F.u, (const float*)F.b, F.mask, h->C, G.H,
                        G.W, F.H, F.W, add, s, h->ntile, h->d_active);
   if (use_march<T>(h, F))

@@ -82,6 +82,8 @@ def test_sweep_kernel_variants_agree(shape):
     mask = (np.random.default_rng(4).random((h, w)) < 0.05).astype(np.uint8)
     outs = []
     prev, prev_ws = lib.sp_march_variant(-1), lib.sp_ws_variant(-1)
+    prev_px = lib.sp_tma_min_pixels(-1)
+    lib.sp_tma_min_pixels(0)  # the TMA kernels on every level that fits them
     try:
         # (sweep variant, warp-streamed TMA kernels on/off)
         for mv, ws in ((2, 1), (2, 0), (1, 1), (0, 1)):
@@ -93,6 +95,7 @@ def test_sweep_kernel_variants_agree(shape):
     finally:
         lib.sp_march_variant(prev)
         lib.sp_ws_variant(prev_ws)
+        lib.sp_tma_min_pixels(prev_px)
         _POOL.clear()
     for o in outs[:3]:
         rel = np.abs(o - outs[3]).max() / np.abs(outs[3]).max()
@@ -118,6 +121,8 @@ def test_sweep_kernel_residuals_bit_identical(shape):
     u0 = ft + torch.from_numpy(np.random.default_rng(8).standard_normal(f.shape)).float().cuda()
     bsym = _masked_rhs(ft, mt)
     prev, prev_ws = lib.sp_march_variant(-1), lib.sp_ws_variant(-1)
+    prev_px = lib.sp_tma_min_pixels(-1)
+    lib.sp_tma_min_pixels(0)  # the TMA kernels on every level that fits them
     res = {}
     try:
         # 3: the CTA-tile TMA kernels (sweep 2 with the warp-streamed off)
@@ -134,6 +139,7 @@ def test_sweep_kernel_residuals_bit_identical(shape):
     finally:
         lib.sp_march_variant(prev)
         lib.sp_ws_variant(prev_ws)
+        lib.sp_tma_min_pixels(prev_px)
         _POOL.clear()
     for v in (1, 2, 3):
         assert np.array_equal(res[v][0], res[0][0])
