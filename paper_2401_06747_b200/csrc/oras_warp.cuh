@@ -183,13 +183,17 @@ __device__ __forceinline__ long warp_cg32_fast(float (&res)[32], float (&v)[32],
 }
 
 // warp_sum_f over eight float chains held as four pairs: pairwise FADD2s,
-// the two halves, one xor butterfly, a uniform broadcast
+// the two halves, one xor butterfly.  No closing broadcast: at every level
+// lanes i and i ^ o add the same two operands (IEEE addition commutes), so
+// all lanes hold the same bits; the CG's exit tests vote on them
+// (__all_sync / __any_sync) to give the compiler its uniform branches, which
+// takes a shuffle latency off each of the step's two reductions.
 __device__ __forceinline__ float warp_sum_f2(const float2 (&d)[4]) {
   const float2 t = __fadd2_rn(__fadd2_rn(d[0], d[1]), __fadd2_rn(d[2], d[3]));
   float x = t.x + t.y;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-  return __shfl_sync(0xFFFFFFFFu, x, 0);
+  return x;
 }
 
 // The lean local CG on packed float pairs (sp_oras_variant 8): the lane's
@@ -223,7 +227,7 @@ __device__ __forceinline__ long warp_cg32_pair(float (&res)[32], float (&v)[32],
   const float2 lf2 = make_float2(lf, lf), rt2 = make_float2(rt, rt);
   const float2 ih2 = make_float2(inv_h2, inv_h2);
   long it = 0;
-  while ((double)rs > tau && it < cap) {
+  while (__all_sync(0xFFFFFFFFu, (double)rs > tau) && it < cap) {
 #pragma unroll
     for (int g = 0; g < 4; ++g) d4[g] = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -250,7 +254,7 @@ __device__ __forceinline__ long warp_cg32_pair(float (&res)[32], float (&v)[32],
       d4[k & 3] = __ffma2_rn(p2[k], ap2[k], d4[k & 3]);
     }
     const float pap = warp_sum_f2(d4);
-    if (pap <= 0.0f) break;
+    if (__any_sync(0xFFFFFFFFu, pap <= 0.0f)) break;
     const float alpha = __fdividef(rs, pap);
     const float2 al2 = make_float2(alpha, alpha), nal2 = make_float2(-alpha, -alpha);
 #pragma unroll
