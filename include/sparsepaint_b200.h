@@ -393,6 +393,10 @@ int sp_fused_bnorm(int v);
  * sweep kernels instead of the TMA / warp-streamed ones (identical
  * results); v < 0 queries. */
 long sp_tma_min_pixels(long v);
+/* Jump-flooding passes of step 1 and 2 on pixel quads with aligned 16-byte
+ * candidate loads (1, default) or per pixel (0); bit-identical labels.
+ * v < 0 queries. */
+int sp_jfa_short4(int v);
 /* C = 3 float blend: 2 = packed cover words on column pairs (two pixels per
  * 8-byte access where W and every block start are even, else 1; default),
  * 3 = the same with two rows per thread, 1 = packed per-row / per-column

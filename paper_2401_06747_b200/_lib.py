@@ -115,6 +115,7 @@ _SIGS = {
     "sp_tile_list": [c_int],
     "sp_fused_bnorm": [c_int],
     "sp_tma_min_pixels": [c_long],
+    "sp_jfa_short4": [c_int],
     "sp_blend_packed": [c_int],
     "sp_tile_fused": [c_int],
     "sp_channel_parallel": [c_int],

@@ -572,6 +572,8 @@ extern "C" int sp_ws_stages(int v) { return sp::ws_stages(v); }
 extern "C" int sp_oras_offbits(int v) { return sp::oras_offbits(v); }
 namespace sp { int tile_list(int v); }
 extern "C" int sp_tile_list(int v) { return sp::tile_list(v); }
+namespace sp { int jfa_short4(int v); }
+extern "C" int sp_jfa_short4(int v) { return sp::jfa_short4(v); }
 namespace sp { long tma_min_pixels(long v); }
 extern "C" long sp_tma_min_pixels(long v) { return sp::tma_min_pixels(v); }
 namespace sp { int fused_bnorm(int v); }

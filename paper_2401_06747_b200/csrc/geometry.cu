@@ -199,6 +199,43 @@ __global__ void k_jfa_pass_key4(const unsigned* __restrict__ cur, unsigned* __re
       make_uint4((unsigned)best[0], (unsigned)best[1], (unsigned)best[2], (unsigned)best[3]);
 }
 
+// four pixels per thread for the short steps (1, 2; W % 4 == 0): the
+// candidate columns x0 - step .. x0 + 3 + step of a row lie in the three
+// aligned quads at x0 - 4, x0, x0 + 4, so each candidate row is three
+// 16-byte loads instead of twelve scalar ones; out-of-image candidates are
+// the phantom "no seed" key, which never wins.  Same minimum as
+// k_jfa_pass_key (the rule is a total order): bit-identical labels.
+__global__ void k_jfa_pass_key4s(const unsigned* __restrict__ cur, unsigned* __restrict__ nxt,
+                                 int step, int H, int W) {
+  const int x0 = (blockIdx.x * BX + threadIdx.x) * 4, y = blockIdx.y * BY + threadIdx.y;
+  if (x0 >= W || y >= H) return;
+  const uint4 none = make_uint4(KNONE, KNONE, KNONE, KNONE);
+  unsigned long long best[4];
+#pragma unroll
+  for (int oy = -1; oy <= 1; ++oy) {
+    const int ny = y + oy * step;
+    const bool rok = ny >= 0 && ny < H;
+    const unsigned* row = cur + (size_t)(rok ? ny : y) * W;
+    const uint4 l = rok && x0 > 0 ? *reinterpret_cast<const uint4*>(row + x0 - 4) : none;
+    const uint4 c = rok ? *reinterpret_cast<const uint4*>(row + x0) : none;
+    const uint4 r = rok && x0 + 4 < W ? *reinterpret_cast<const uint4*>(row + x0 + 4) : none;
+    const unsigned w[12] = {l.x, l.y, l.z, l.w, c.x, c.y, c.z, c.w, r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (oy == -1) best[i] = ~0ull;
+      // step is 1 or 2: the window index of x0 + i + ox * step
+      const unsigned long long a = key_dk(step == 1 ? w[3 + i] : w[2 + i], y, x0 + i);
+      const unsigned long long m = key_dk(w[4 + i], y, x0 + i);
+      const unsigned long long b = key_dk(step == 1 ? w[5 + i] : w[6 + i], y, x0 + i);
+      unsigned long long t = a < m ? a : m;
+      t = b < t ? b : t;
+      best[i] = t < best[i] ? t : best[i];
+    }
+  }
+  *reinterpret_cast<uint4*>(nxt + (size_t)y * W + x0) =
+      make_uint4((unsigned)best[0], (unsigned)best[1], (unsigned)best[2], (unsigned)best[3]);
+}
+
 // keys -> seed indices (rank of the seed pixel), in place; fused with the
 // max squared distance of jfa_dist2 (unlabelled pixels: numba's seeds[-1])
 __global__ void k_jfa_key_finish(unsigned* __restrict__ lab, const int* __restrict__ rank,
@@ -1133,6 +1170,13 @@ int geo_create(Geo** out, int H, int W) {
 }
 
 // geometry.py:76-89
+// short JFA steps on pixel quads (k_jfa_pass_key4s, 1) or per pixel (0)
+static int jfa_short4_on = 1;
+int jfa_short4(int v) {
+  if (v >= 0) jfa_short4_on = v;
+  return jfa_short4_on;
+}
+
 static std::vector<long long> steps_for(int max_dim, double hint) {
   long long start;
   if (hint >= 1.0) {
@@ -1185,6 +1229,8 @@ int geo_voronoi(Geo* g, const uint8_t* mask, double hint, long* m_out, double* r
     for (size_t i = 0; i < steps.size(); ++i) {
       if (steps[i] % 4 == 0 && W % 4 == 0)
         k_jfa_pass_key4<<<grid2(W / 4, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
+      else if (steps[i] <= 2 && W % 4 == 0 && jfa_short4_on)
+        k_jfa_pass_key4s<<<grid2(W / 4, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
       else
         k_jfa_pass_key<<<grid2(W, H), dim3(BX, BY), 0, s>>>(cur, nxt, (int)steps[i], H, W);
       SP_CHECK_LAUNCH();

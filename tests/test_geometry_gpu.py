@@ -137,6 +137,30 @@ def test_jfa_against_oracle_with_hints(sp):
             assert np.array_equal(mesh.edges, eo)
 
 
+@pytest.mark.parametrize("short4", [0, 1])
+def test_jfa_short_steps_on_quads_match_oracle(sp, short4):
+    """Passes of step 1 and 2 on pixel quads (k_jfa_pass_key4s: aligned
+    16-byte candidate loads, out-of-image candidates as the phantom key) and
+    per pixel (k_jfa_pass_key): labels equal to the oracle's bit for bit, on
+    widths that are multiples of 4 (the quad kernel's domain) incl. the
+    image edges."""
+    from paper_2401_06747_b200 import _lib
+    lib = _lib.load()
+    prev = lib.sp_jfa_short4(-1)
+    rng = np.random.default_rng(12)
+    try:
+        lib.sp_jfa_short4(short4)
+        for (h, w, d) in ((96, 160, 0.02), (37, 52, 0.1), (8, 4, 0.3), (200, 256, 0.005)):
+            m = (rng.random((h, w)) < d).astype(np.uint8)
+            m.ravel()[rng.integers(0, h * w)] = 1
+            for hint in (None, 1.0, 2.0, 6.0):
+                lab = sp.jump_flood_voronoi(sp.Mask(m), hint)
+                lo, _, rad = O.jump_flood_voronoi(m, hint)
+                assert np.array_equal(lab.labels, lo) and lab.max_radius == rad
+    finally:
+        lib.sp_jfa_short4(prev)
+
+
 def test_reference_geometry_kats(sp):
     """test_geometry.py:24-103 known answers."""
     def mask_from(h, w, pts):
