@@ -15,7 +15,11 @@ L=$(python -c "import json;print(json.loads(open('gpurun_out/bench_$TAG.json').r
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3 * L)) -c $L --csv \
     --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-strips > gpurun_out/launches_bench_$TAG.log 2>&1
-bash scripts/ncu_kernels.sh $TAG k_oras_warp k_ws_resid:9 k_oras_blend k_ws_prolong:4
+# in the warm V-cycle the first k_ws_resid is the finest residual + norms,
+# the second the finest residual + restriction; the TMA prolongations run
+# coarse to fine over the levels >= 300,000 px (three at 4K)
+bash scripts/ncu_kernels.sh $TAG k_oras_warp k_ws_resid:0 k_ws_resid:1:k_ws_resid_restrict \
+    k_oras_blend k_ws_prolong:2
 
 # fused RAS block kernels (tilesolve.cu) on the 4K block set
 for K in k_tv_down k_tv_close; do
