@@ -59,8 +59,16 @@ def _ncu_traffic(kernel):
     (profiles/ncu_<tag>_<kernel>.txt, scripts/summarize_prof.py), or None."""
     import glob
     import re
-    # newest round tag last (ncu_r01a_... < ncu_r01w_...)
+    # the tag named in profiles/LATEST (the newest profile round), else the
+    # lexicographically last tag
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_*_{kernel}.txt")))
+    try:
+        with open(os.path.join(ROOT, "profiles", "LATEST")) as fh:
+            latest = os.path.join(ROOT, "profiles", f"ncu_{fh.read().strip()}_{kernel}.txt")
+        if os.path.exists(latest):
+            files.append(latest)
+    except OSError:
+        pass
     if not files:
         return None
     tot = 0.0
